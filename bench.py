@@ -1,0 +1,362 @@
+"""Benchmark: candidate plans evaluated/sec on B200 (BASELINE.json metric).
+
+One step = one pass of the hot path over one batch: K1 evaluates B candidate
+operator orders of the named training graph (peak memory of each, as
+reference peak_memory(g, sequential_schedule(g, o)) -- graph.py:401-468) and
+selects the first strict minimum (planner.py:209-216); with N>1 GPUs each rank
+evaluates its own contiguous id range (weak scaling) and the per-rank best
+(peak, id) is exchanged with one NCCL all_gather.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config gpt2-small]
+  python bench.py --impl reference ...   # the reference algorithm on host cores
+
+Default workload: BASELINE config 2, GPT-2 small fwd+bwd+Adam training graph
+(batch 8, seq 1024), 16,384 candidates per GPU.  Candidates are counter-RNG
+Kahn orders (seed 0, ids rank*B ...), generated on device before timing
+(generation timed separately).  L2 is flushed (512 MiB write) between timed
+steps; each step is timed with CUDA events on the launching stream.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "candidate plans evaluated/sec"
+UNIT = "candidates/s"
+DEFAULT_BATCH = {"gpt2-small": 16384, "layered": 16384, "bert-large": 16384, "gpt2-xl": 131072}
+WORKLOAD = {
+    "gpt2-small": "GPT-2 small fwd+bwd+Adam training graph (batch 8, seq 1024), candidate orders",
+    "bert-large": "BERT-large fwd+bwd+Adam training graph (batch 8, seq 512), candidate orders",
+    "gpt2-xl": "GPT2-XL fwd+bwd+Adam training graph (batch 1, seq 1024), candidate orders",
+    "layered": "synthetic layered DAG 1k ops / 3k tensors seed 0, candidate orders",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="gpt2-small", choices=sorted(WORKLOAD))
+    ap.add_argument("--batch", type=int, default=0, help="candidates per GPU")
+    ap.add_argument("--cpu-seconds", type=float, default=3.0, help="wall budget of the CPU baseline")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/cpu)")
+    return ap.parse_args()
+
+
+def measured_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text())
+    return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+class ClockSampler:
+    """Polls NVML (SM clock, throttle reasons) every ~2 ms while running."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.samples: list[int] = []
+        self.reasons: set[str] = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self) -> dict:
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples), "source": "nvml" if self.nv else "unavailable"}
+
+
+def graph_for(config: str):
+    from paper_2310_19295_b200 import graphgen as gg
+    from paper_2310_19295_b200.graph import load_graph
+    return load_graph(gg.config_doc(config))
+
+
+def ncu_traffic(config: str, batch: int):
+    """dram bytes/launch of K1 from a committed ncu --set full summary."""
+    p = ROOT / "profiles" / "k1_ncu_summary.json"
+    if not p.exists():
+        return None
+    try:
+        d = json.loads(p.read_text())
+        ent = d.get(config)
+        if ent and int(ent.get("batch", -1)) == batch:
+            return int(ent["dram_bytes_read"]) + int(ent["dram_bytes_write"])
+    except Exception:
+        return None
+    return None
+
+
+# ------------------------------------------------------------ reference arm
+
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import coracle
+    g = graph_for(args.config)
+    cg = coracle.CGraph(g)
+    cores = os.cpu_count() or 1
+    # bounded sample of the same workload (same candidate ids as rank 0)
+    sample = 2048
+    orders = coracle.kahn_orders(cg, 0, 0, sample, threads=cores)
+    for _ in range(max(args.warmup, 1)):
+        coracle.eval_orders(cg, orders, threads=cores)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        coracle.eval_orders(cg, orders, threads=cores)
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * sum(times) / len(times)
+    value = sample / (ms / 1e3)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": f"{WORKLOAD[args.config]}: bounded sample of {sample} per step",
+                   "graph": args.config, "n_ops": cg.n, "n_tensors": cg.T},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{sample} counter-RNG Kahn candidates (seed 0, ids 0..{sample - 1}) "
+                                   f"per step; oracle/peak_oracle.c restating graph.py:375-468, "
+                                   f"{cores} pthreads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ----------------------------------------------------------------- our arm
+
+def main() -> None:
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2310_19295_b200 import evaluator as ev
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    B = args.batch or DEFAULT_BATCH[args.config]
+    g = graph_for(args.config)
+    dg = ev.device_graph(g)
+    info = dg.info()
+    n = info["n_ops"]
+    first_id = rank * B
+    stream = torch.cuda.current_stream()
+
+    # candidates materialised in HBM before timing; generation timed separately
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g0.record()
+    orders = ev.generate_orders(g, 0, first_id, B, device=dev)
+    g1.record()
+    torch.cuda.synchronize()
+    gen_ms = g0.elapsed_time(g1)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        peak, arg, val = ev.evaluate_orders(g, orders)          # K1
+        best = ev.select_device(peak, val, first_id)             # argmin kernel
+        if world > 1:
+            allb = torch.empty(world * 2, dtype=torch.int64, device=dev)
+            dist.all_gather_into_tensor(allb, best)
+            pk = allb.view(world, 2)
+            k = torch.argmin(pk[:, 0])                           # ties -> lowest rank = lowest id
+            best = pk[k]
+        return best
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    K = args.steps
+    ev_s = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ev_k1 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ev_e = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    sampler = ClockSampler(local)
+    launches0 = ev.launch_count()
+    with sampler:
+        for i in range(K):
+            flush.zero_()                                        # untimed: L2 flush
+            ev_s[i].record(stream)
+            peak, arg, val = ev.evaluate_orders(g, orders)
+            ev_k1[i].record(stream)
+            best = ev.select_device(peak, val, first_id)
+            if world > 1:
+                allb = torch.empty(world * 2, dtype=torch.int64, device=dev)
+                dist.all_gather_into_tensor(allb, best)
+                pk = allb.view(world, 2)
+                best = pk[torch.argmin(pk[:, 0])]
+            ev_e[i].record(stream)
+        torch.cuda.synchronize()
+    launches = ev.launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms = [ev_s[i].elapsed_time(ev_e[i]) for i in range(K)]
+    k1_ms = [ev_s[i].elapsed_time(ev_k1[i]) for i in range(K)]
+    tot_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    ms_per_step = tot_ms / K
+    value = world * B * K / (tot_ms / 1e3)
+    best_host = [int(x) for x in best.cpu().tolist()]
+
+    # roofline of K1: algorithmic bytes per launch / average K1 duration
+    meta_bytes = (2 * n * (2 if not info["wide_index"] else 4) + 16 * info["n_values"]
+                  + 4 * info["n_check_edges"] + 8 * info["n_multi"] + 2 * info["n_multi_cons"])
+    alg_bytes = B * (4 * n + 16) + meta_bytes
+    k1_avg = sum(k1_ms) / K
+    peaks = measured_peaks()
+    achieved = alg_bytes / (k1_avg / 1e3) / 1e9
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    traffic = ncu_traffic(args.config, B)
+
+    # end to end through the public API with HOST buffers: H2D of the orders
+    # from pinned memory, K1 + argmin, D2H of per-candidate results + best
+    host_orders = torch.empty((B, n), dtype=torch.int32, pin_memory=True)
+    host_orders.copy_(orders.cpu())
+    host_np = host_orders.numpy()
+    for _ in range(2):
+        ev.evaluate_and_select(g, host_np, id_base=first_id)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ke = max(3, min(K, 10))
+    t0 = time.perf_counter()
+    for _ in range(ke):
+        hp, ha, hv, hbest = ev.evaluate_and_select(g, host_np, id_base=first_id)
+        if world > 1:
+            b = torch.tensor(hbest, dtype=torch.int64, device=dev)
+            allb = torch.empty(world * 2, dtype=torch.int64, device=dev)
+            dist.all_gather_into_tensor(allb, b)
+            pk = allb.view(world, 2).cpu()
+            hbest = tuple(int(x) for x in pk[int(torch.argmin(pk[:, 0]))])
+    e2e_s = (time.perf_counter() - t0) / ke
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    assert tuple(hbest) == tuple(best_host), (hbest, best_host)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
+        from oracle import coracle
+        cg = coracle.CGraph(g)
+        cores = os.cpu_count() or 1
+        S = min(B, 4096)
+        sample = host_np[:S]
+        want = coracle.eval_orders(cg, sample, threads=cores)  # warm + parity check
+        gp, ga, gv = hp[:S], ha[:S], hv[:S]
+        parity = bool(np.array_equal(gv, want[2]) and np.array_equal(gp[gv], want[0][want[2]])
+                      and np.array_equal(ga[gv], want[1][want[2]]))
+        if not parity:
+            raise SystemExit("GPU results differ from the CPU oracle on the bench sample")
+        done, t0 = 0, time.perf_counter()
+        while True:
+            coracle.eval_orders(cg, sample, threads=cores)
+            done += S
+            if time.perf_counter() - t0 >= args.cpu_seconds:
+                break
+        cps = done / (time.perf_counter() - t0)
+        cpu = {"value": cps, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"first {S} of this run's candidates, repeated for >= {args.cpu_seconds:g} s "
+                         f"wall; oracle/peak_oracle.c restating graph.py:375-468 on {cores} pthreads; "
+                         f"bit-exact parity with the GPU results on the sample: {parity}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {"workload": f"{WORKLOAD[args.config]}: {B} per GPU", "graph": args.config,
+                       "n_ops": n, "n_tensors": info["n_tensors"], "candidates_per_gpu": B,
+                       "candidate_ids": f"rank r evaluates [r*{B}, (r+1)*{B})",
+                       "l2": "flushed between timed steps (512 MiB write, outside the events)",
+                       "parallelism": f"candidate-sharded dp{world}" + (" + NCCL all_gather argmin" if world > 1 else ""),
+                       "generation_ms": gen_ms},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": traffic,
+                         "kernel": "k1_eval_orders", "k1_ms": k1_avg,
+                         "alg_bytes_per_launch": alg_bytes,
+                         "alg_bytes_formula": "B*(4n+16) + graph metadata",
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst)" if "_fallback" not in peaks
+                         else "fallback 6650 GB/s (B200_PROFILING.md)"},
+            "e2e": {"value": world * B / e2e_s, "unit": UNIT,
+                    "h2d_bytes_per_step": B * n * 4,
+                    "d2h_bytes_per_step": B * (8 + 4 + 1) + 16,
+                    "api": "evaluate_and_select(g, pinned_host_orders) -> rm_eval_select"},
+            "gpu_launches": launches,
+            "clocks": sampler.summary(),
+            "best": {"peak": best_host[0], "id": best_host[1]},
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

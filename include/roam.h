@@ -1,0 +1,235 @@
+/*
+ * roam.h -- C ABI of libroam, the B200 (sm_100a) implementation of the ROAM
+ * planner's data-parallel hot path (arXiv 2310.19295; reference:
+ * /root/reference/pkg/src/memplan).
+ *
+ * Plain C types only: pointers, sizes, int status codes.  Every entry point
+ * returns RM_OK (0) or a negative RmStatus; rm_last_error() gives a
+ * thread-local message for the last failure on the calling thread.
+ *
+ * Memory: the caller owns every input and output buffer.  Unless a call
+ * takes RM_DEVICE_PTRS in its flags, pointers are HOST pointers (pinned or
+ * pageable) and the call stages them through the device itself and returns
+ * only after the results are back on the host.  With RM_DEVICE_PTRS all
+ * array arguments are device pointers and the call is asynchronous on
+ * `stream` (a cudaStream_t; NULL = legacy default stream).
+ *
+ * The only library-owned memory is the immutable RmGraph handle (graph CSR
+ * + derived evaluation metadata, host and device copies).  Calls never share
+ * scratch, so they are re-entrant across threads and streams (the reference's
+ * ThreadPoolExecutor contract, planner.py:119-124).
+ */
+#ifndef ROAM_H_
+#define ROAM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  RM_OK = 0,
+  RM_ERR_INVALID_ARG = -1,
+  RM_ERR_CUDA = -2,
+  RM_ERR_OVERFLOW = -3,
+  RM_ERR_NO_DEVICE = -4,
+  RM_ERR_CAPACITY = -5,
+  RM_ERR_GRAPH = -6
+} RmStatus;
+
+enum {
+  RM_DEVICE_PTRS = 1u << 0,  /* array arguments are device pointers; async */
+  RM_NO_REDUCE = 1u << 1     /* rm_graph_create: skip transitive reduction */
+};
+
+/* ------------------------------------------------------------------ graph */
+
+/* CSR description of a graph with dense ids (reference graph.py:59-135,
+ * load_graph 188-278).  cons_idx keeps one entry per input occurrence
+ * (graph.py:227-231); in_idx keeps each op's inputs in document order. */
+typedef struct {
+  int32_t n_ops;
+  int32_t n_tensors;
+  const int64_t* size;      /* [T] bytes */
+  const int32_t* producer;  /* [T] */
+  const int32_t* cons_ptr;  /* [T+1] */
+  const int32_t* cons_idx;  /* [E] */
+  const int32_t* in_ptr;    /* [n+1] */
+  const int32_t* in_idx;    /* [E] */
+  const int32_t* out_ptr;   /* [n+1] */
+  const int32_t* out_idx;   /* [sum outputs] */
+} RmGraphDesc;
+
+typedef struct RmGraph RmGraph;
+
+typedef struct {
+  int32_t n_ops, n_tensors;
+  int64_t n_cons;           /* E */
+  int64_t n_pred_edges;     /* P: deduplicated, self-free direct_preds edges */
+  int64_t n_check_edges;    /* edges K1 checks (transitive reduction of P) */
+  int64_t n_multi;          /* tensors with >= 2 maximal consumers */
+  int64_t n_multi_cons;     /* their maximal-consumer entries */
+  int64_t n_slots;          /* distinct ops closing a multi-consumer lifetime */
+  int64_t n_values;         /* distinct (out_bytes, free_bytes) op classes */
+  int32_t reduced;          /* 1 when the reduction ran */
+  int32_t wide_index;       /* 1 when ids need int32 (n > 65535) */
+  int64_t total_bytes;      /* sum of |size| */
+} RmGraphInfo;
+
+/* Validate + marshal a graph; computes the order-evaluation metadata on the
+ * host (transitive reduction, maximal consumers, per-op event classes) and,
+ * when a device is present, uploads it.  With no CUDA device the handle is
+ * host-only: rm_graph_info works, every device entry point fails with
+ * RM_ERR_NO_DEVICE. */
+int rm_graph_create(const RmGraphDesc* desc, uint32_t flags, RmGraph** out);
+int rm_graph_destroy(RmGraph* g);
+int rm_graph_info(const RmGraph* g, RmGraphInfo* info);
+
+/* Host copy of the K1 metadata (sizes from rm_graph_info): per-op event class
+ * and slot (-1 = none), class table (out_bytes, free_bytes), checked edges,
+ * multi-consumer CSR.  Any pointer may be NULL.  Host-only; no device needed. */
+int rm_graph_k1_export(const RmGraph* g, int32_t* vidx, int32_t* slot, int64_t* out_tab,
+                       int64_t* fs_tab, int32_t* edge_u, int32_t* edge_v, int32_t* mptr,
+                       int32_t* mcons, int64_t* msize);
+
+/* ----------------------------------------------------- K1: order batches */
+
+/* Evaluate B candidate orders (orders is int32[B, n_ops], row-major), each as
+ * peak_memory(g, sequential_schedule(g, order)) (reference graph.py:401-409,
+ * 461-468):
+ *   valid[b]  = 1 iff the row is a permutation respecting every direct pred
+ *               (validate_schedule, graph.py:375-398);
+ *   peak[b]   = max over timesteps of live bytes;
+ *   argmax[b] = first timestep attaining it.
+ * Rows with valid == 0 have unspecified peak/argmax (the reference raises
+ * ScheduleError for them).  Replaces graph.py:461 peak_memory in a loop. */
+int rm_eval_orders(RmGraph* g, const int32_t* orders, int64_t B, uint32_t flags,
+                   int64_t* peak, int32_t* argmax, uint8_t* valid, void* stream);
+
+/* rm_eval_orders followed by rm_argmin in one call: the candidate-plan
+ * selection step of the planner (planner.py:209-216) -- best = {peak, id}
+ * of the first strict minimum, ids numbered from id_base.  With host
+ * pointers the orders are staged through the device in chunks (copy/compute
+ * overlap) and every output is back on the host when the call returns. */
+int rm_eval_select(RmGraph* g, const int32_t* orders, int64_t B, int64_t id_base, uint32_t flags,
+                   int64_t* peak, int32_t* argmax, uint8_t* valid, int64_t* best /* [2] */,
+                   void* stream);
+
+/* First strict minimum over valid candidates, i.e. the lexicographic min of
+ * (peak, id) -- reference tests/oracles.py:46-56 and planner.py:209-216.
+ * out_best = {peak, id + id_base} or {INT64_MAX, -1} when none is valid. */
+int rm_argmin(const int64_t* peak, const uint8_t* valid, int64_t B, int64_t id_base,
+              uint32_t flags, int64_t* out_best /* [2] */, void* stream);
+
+/* Counter-RNG candidate generator: row c is the Kahn topological order that
+ * breaks ties by the smallest (splitmix64(seed ^ splitmix64(id)) ^ op, op)
+ * key with id = first_id + c (oracle: oracle/memplan_oracle.py kahn_candidate).
+ * Always device output (orders_dev int32[B, n]); async on stream. */
+int rm_gen_orders(RmGraph* g, uint64_t seed, int64_t first_id, int64_t B,
+                  int32_t* orders_dev, void* stream);
+
+/* ------------------------------------------- single schedule (drop-ins) */
+
+typedef struct {
+  int32_t status;        /* 0 ok, else RM_SCHED_* below (first failing check) */
+  int32_t detail_a;      /* RM_SCHED_PRED: op v */
+  int32_t detail_b;      /* RM_SCHED_PRED: predecessor p */
+  int32_t n_steps;
+  int64_t peak;
+  int32_t argmax;
+  int32_t _pad;
+} RmScheduleResult;
+
+enum {
+  RM_SCHED_OK = 0,
+  RM_SCHED_NOT_PERMUTATION = 1,   /* graph.py:377-378 */
+  RM_SCHED_TIMESTEPS_LEN = 2,     /* graph.py:379-380 */
+  RM_SCHED_OPS_PER_STEP = 3,      /* graph.py:381-382 (ConfigError) */
+  RM_SCHED_DECREASING = 4,        /* graph.py:385-389 */
+  RM_SCHED_STEP_OVERFULL = 5,     /* graph.py:390-394 */
+  RM_SCHED_PRED = 6               /* graph.py:395-398 */
+};
+
+enum {
+  RM_SCHED_VALIDATE = 1u << 8,    /* run validate_schedule first (peak_memory) */
+  RM_SCHED_PEAK = 1u << 9         /* compute peak/argmax */
+};
+
+/* General schedule evaluation (any timesteps, ops_per_step): validation
+ * (graph.py:375-398), tensor_lifetimes (440-449), live_bytes_by_timestep
+ * (452-458), peak_memory (461-468).  birth/death (int32[T]) and live
+ * (int64[n_steps]) are optional outputs (NULL to skip).  Timesteps must be
+ * in [0, 2^31). */
+int rm_eval_schedule(RmGraph* g, const int32_t* order, int64_t order_len,
+                     const int32_t* timesteps, int64_t ts_len, int32_t ops_per_step,
+                     uint32_t flags, RmScheduleResult* res, int32_t* birth, int32_t* death,
+                     int64_t* live, void* stream);
+
+/* ------------------------------------------------- K2: layout checks */
+
+/* Items: tensor i has inclusive lifetime [start, end], size, offset and a
+ * has_offset flag (layout.py:20-29, 305-329).  Finds every pair i < j of items
+ * with offsets overlapping in time AND address; pairs are returned as
+ * (i, j) item indices sorted lexicographically (layout_violations order).
+ * item_flags[i] bit0 = no offset, bit1 = negative offset, bit2 = extent
+ * exceeds capacity.  max_extent = max(off+size) over items with offsets (0 if
+ * none), the replay_static actual peak (simulator.py:129-145).  If the
+ * number of pairs exceeds max_pairs, n_pairs reports the full count and only
+ * the first max_pairs (in sorted order) are written.  Host pointers only. */
+int rm_layout_violations(int64_t N, const int32_t* start, const int32_t* end,
+                         const int64_t* size, const int64_t* offset, const uint8_t* has_offset,
+                         int64_t capacity, uint8_t* item_flags, int64_t* pairs /* [2*max] */,
+                         int64_t max_pairs, int64_t* n_pairs, int64_t* max_extent, void* stream);
+
+/* ---------------------------------------------- K3: batched LLFB packer */
+
+enum {
+  RM_LLFB_PLAIN = 0,        /* llfb_layout (layout.py:100-118) */
+  RM_LLFB_CONSTRAINED = 1,  /* constrained_llfb_layout (layout.py:121-146) */
+  RM_LLFB_COMPONENTS = 2    /* exact_layout's per-component incumbent + bound
+                               (layout.py:165-225), activations_at_bottom */
+};
+
+/* P independent layout problems; problem p owns items [item_ptr[p],
+ * item_ptr[p+1]).  Per item: tensor id, inclusive [start, end], size,
+ * is_activation.  Outputs: offset[item] (int64), capacity[p]; for
+ * RM_LLFB_COMPONENTS also bound[p] = 1 iff every component's incumbent met
+ * its lower bound (the reference returns without search), comp[item] = the
+ * component root tensor id (-1 for pre-placed activations) and
+ * comp_cap[item] = that component's incumbent capacity.  Host pointers. */
+int rm_llfb_batch(int32_t P, const int64_t* item_ptr, const int32_t* tensor,
+                  const int32_t* start, const int32_t* end, const int64_t* size,
+                  const uint8_t* is_act, int32_t mode, int64_t* offset, int64_t* capacity,
+                  uint8_t* bound_met, int32_t* comp, int64_t* comp_cap, void* stream);
+
+/* ------------------------------------------- K4: batched window greedy */
+
+/* W greedy_order problems (ordering.py:78-180) over one graph.  Window w
+ * owns ops win_ops[win_ptr[w] .. win_ptr[w+1]) (sorted ascending) and the
+ * live_in / live_out tensor sets lin_idx[lin_ptr[w]..], lout_idx[lout_ptr[w]..].
+ * Outputs: order[win_ptr[w]..] (op ids), peak[w].  status[w] = 0 ok, 1 a
+ * live-in tensor with no local consumer that is not live-out (ConfigError,
+ * ordering.py:107-110), 2 precedence cycle.  Host pointers. */
+int rm_greedy_windows(RmGraph* g, int32_t W, const int64_t* win_ptr, const int32_t* win_ops,
+                      const int64_t* lin_ptr, const int32_t* lin_idx,
+                      const int64_t* lout_ptr, const int32_t* lout_idx,
+                      int32_t* order, int64_t* peak, int32_t* status, int32_t* bad_tensor,
+                      void* stream);
+
+/* ------------------------------------------------------------- misc */
+
+const char* rm_last_error(void);
+int rm_device_count(int* count);
+/* Kernel launches made by this process through libroam so far. */
+int64_t rm_launch_count(void);
+/* Device time (ms) of the last rm_eval_orders K1 launch on this thread when
+ * timing was requested through rm_set_timing(1); -1 if unavailable. */
+int rm_set_timing(int enable);
+double rm_last_kernel_ms(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ROAM_H_ */

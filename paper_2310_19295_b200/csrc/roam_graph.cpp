@@ -1,0 +1,379 @@
+// Host half of libroam: error plumbing, graph validation/marshalling, and
+// the once-per-graph K1 metadata (transitive reduction of direct_preds,
+// maximal consumer sets, per-op event classes) described in roam_internal.h.
+//
+// Reference semantics being restated (pkg/src/memplan/graph.py):
+//   direct_preds  97-104  producers of inputs, dedup, self discarded
+//   tensor_lifetimes 440-449  birth = ts[producer], death = max ts[consumers]
+//                              (horizon if none), clamped >= birth
+//   validate_schedule 375-398 permutation + preds-before
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <map>
+#include <unordered_map>
+
+#include "roam_internal.h"
+
+namespace roam {
+
+static thread_local std::string g_last_error;
+static std::atomic<int64_t> g_launches{0};
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+int fail(int status, const std::string& msg) {
+  g_last_error = msg;
+  return status;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+  g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+  return RM_ERR_CUDA;
+}
+void note_launch(int64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+DevBuf::~DevBuf() {
+  if (p) cudaFree(p);
+}
+cudaError_t DevBuf::upload(const void* host, size_t nbytes) {
+  bytes = nbytes;
+  cudaError_t e = cudaMalloc(&p, nbytes ? nbytes : 16);
+  if (e != cudaSuccess) return e;
+  if (nbytes) e = cudaMemcpy(p, host, nbytes, cudaMemcpyHostToDevice);
+  return e;
+}
+
+Scratch::~Scratch() {
+  for (void* p : ptrs) cudaFreeAsync(p, s);
+}
+
+static const int kReduceLimit = 20000;  // ops; n^2/8 bytes of reachability bitsets
+
+// Reachability bitsets desc[v] (strict descendants) over direct_succs, in
+// reverse topological order.  Returns false on a cycle.
+static bool descendants(const RmGraph& g, std::vector<uint64_t>& desc, size_t& words) {
+  const int n = g.n;
+  words = (size_t(n) + 63) / 64;
+  std::vector<int32_t> indeg(n), topo;
+  topo.reserve(n);
+  for (int v = 0; v < n; ++v) indeg[v] = g.pred_ptr[v + 1] - g.pred_ptr[v];
+  for (int v = 0; v < n; ++v)
+    if (!indeg[v]) topo.push_back(v);
+  for (size_t h = 0; h < topo.size(); ++h) {
+    int u = topo[h];
+    for (int k = g.succ_ptr[u]; k < g.succ_ptr[u + 1]; ++k)
+      if (--indeg[g.succ_idx[k]] == 0) topo.push_back(g.succ_idx[k]);
+  }
+  if ((int)topo.size() != n) return false;
+  desc.assign(words * size_t(n), 0);
+  for (int h = n - 1; h >= 0; --h) {
+    int u = topo[h];
+    uint64_t* du = &desc[size_t(u) * words];
+    for (int k = g.succ_ptr[u]; k < g.succ_ptr[u + 1]; ++k) {
+      int w = g.succ_idx[k];
+      const uint64_t* dw = &desc[size_t(w) * words];
+      for (size_t i = 0; i < words; ++i) du[i] |= dw[i];
+      du[w >> 6] |= 1ull << (w & 63);
+    }
+  }
+  return true;
+}
+
+static int build_k1_host(RmGraph& g, bool allow_reduce) {
+  const int n = g.n, T = g.T;
+  std::vector<uint64_t> desc;
+  size_t words = 0;
+  bool reduced = allow_reduce && n <= kReduceLimit && n > 0 && descendants(g, desc, words);
+  auto reach = [&](int a, int b) {  // b is a strict descendant of a
+    return (desc[size_t(a) * words + (b >> 6)] >> (b & 63)) & 1ull;
+  };
+
+  // checked edges: transitive reduction of direct_preds (or all of them)
+  g.h_edge_u.clear();
+  g.h_edge_v.clear();
+  std::vector<uint64_t> R(reduced ? words : 0);
+  for (int u = 0; u < n; ++u) {
+    if (reduced) {
+      std::fill(R.begin(), R.end(), 0);
+      for (int k = g.succ_ptr[u]; k < g.succ_ptr[u + 1]; ++k) {
+        const uint64_t* dw = &desc[size_t(g.succ_idx[k]) * words];
+        for (size_t i = 0; i < words; ++i) R[i] |= dw[i];
+      }
+    }
+    for (int k = g.succ_ptr[u]; k < g.succ_ptr[u + 1]; ++k) {
+      int v = g.succ_idx[k];
+      if (reduced && ((R[v >> 6] >> (v & 63)) & 1ull)) continue;
+      g.h_edge_u.push_back(u);
+      g.h_edge_v.push_back(v);
+    }
+  }
+
+  // births and frees
+  std::vector<int64_t> out(n, 0), fs(n, 0);
+  for (int t = 0; t < T; ++t) out[g.producer[t]] += g.size[t];
+  g.h_mptr.assign(1, 0);
+  g.h_mcons.clear();
+  g.h_msize.clear();
+  std::vector<int32_t> C, maxc;
+  for (int t = 0; t < T; ++t) {
+    C.assign(g.cons_idx.begin() + g.cons_ptr[t], g.cons_idx.begin() + g.cons_ptr[t + 1]);
+    if (C.empty()) continue;  // graph output: live to the horizon, never freed
+    std::sort(C.begin(), C.end());
+    C.erase(std::unique(C.begin(), C.end()), C.end());
+    maxc.clear();
+    for (int c : C) {
+      bool dominated = false;
+      if (reduced)
+        for (int c2 : C)
+          if (c2 != c && reach(c, c2)) { dominated = true; break; }
+      if (!dominated) maxc.push_back(c);
+    }
+    if (maxc.size() == 1) {
+      fs[maxc[0]] += g.size[t];
+    } else {
+      for (int c : maxc) g.h_mcons.push_back(c);
+      g.h_mptr.push_back((int32_t)g.h_mcons.size());
+      g.h_msize.push_back(g.size[t]);
+    }
+  }
+
+  // per-op event classes (distinct (out, fs) pairs, first-appearance order)
+  std::map<std::pair<int64_t, int64_t>, int32_t> cls;
+  g.h_vidx.assign(n, 0);
+  g.h_out.clear();
+  g.h_fs.clear();
+  for (int v = 0; v < n; ++v) {
+    auto key = std::make_pair(out[v], fs[v]);
+    auto it = cls.find(key);
+    if (it == cls.end()) {
+      it = cls.emplace(key, (int32_t)g.h_out.size()).first;
+      g.h_out.push_back(out[v]);
+      g.h_fs.push_back(fs[v]);
+    }
+    g.h_vidx[v] = it->second;
+  }
+  // slots: ops that can close a multi-consumer lifetime
+  g.h_slot.assign(n, -1);
+  int32_t K = 0;
+  for (int32_t c : g.h_mcons)
+    if (g.h_slot[c] < 0) g.h_slot[c] = K++;
+
+  RmGraphInfo& I = g.info;
+  I.n_check_edges = (int64_t)g.h_edge_u.size();
+  I.n_multi = (int64_t)g.h_msize.size();
+  I.n_multi_cons = (int64_t)g.h_mcons.size();
+  I.n_slots = K;
+  I.n_values = (int64_t)g.h_out.size();
+  I.reduced = reduced ? 1 : 0;
+  I.wide_index = n > 65535 ? 1 : 0;
+  return RM_OK;
+}
+
+template <class IdxT>
+static cudaError_t upload_k1(RmGraph& g) {
+  const int n = g.n;
+  const IdxT none = (IdxT)-1;
+  std::vector<IdxT> om(2 * size_t(n));
+  for (int v = 0; v < n; ++v) {
+    om[2 * v] = (IdxT)g.h_vidx[v];
+    om[2 * v + 1] = g.h_slot[v] < 0 ? none : (IdxT)g.h_slot[v];
+  }
+  std::vector<int64_t> tab(2 * g.h_out.size());
+  for (size_t i = 0; i < g.h_out.size(); ++i) {
+    tab[2 * i] = g.h_out[i];
+    tab[2 * i + 1] = g.h_fs[i];
+  }
+  std::vector<IdxT> ed(2 * g.h_edge_u.size());
+  for (size_t i = 0; i < g.h_edge_u.size(); ++i) {
+    ed[2 * i] = (IdxT)g.h_edge_u[i];
+    ed[2 * i + 1] = (IdxT)g.h_edge_v[i];
+  }
+  std::vector<IdxT> mc(g.h_mcons.begin(), g.h_mcons.end());
+  cudaError_t e;
+  if ((e = g.k1.opmeta.upload(om.data(), om.size() * sizeof(IdxT)))) return e;
+  if ((e = g.k1.table.upload(tab.data(), tab.size() * sizeof(int64_t)))) return e;
+  if ((e = g.k1.edges.upload(ed.data(), ed.size() * sizeof(IdxT)))) return e;
+  if ((e = g.k1.mptr.upload(g.h_mptr.data(), g.h_mptr.size() * sizeof(int32_t)))) return e;
+  if ((e = g.k1.mcons.upload(mc.data(), mc.size() * sizeof(IdxT)))) return e;
+  if ((e = g.k1.msize.upload(g.h_msize.data(), g.h_msize.size() * sizeof(int64_t)))) return e;
+  return cudaSuccess;
+}
+
+template <class V>
+static cudaError_t up(DevBuf& b, const std::vector<V>& v) {
+  return b.upload(v.data(), v.size() * sizeof(V));
+}
+
+}  // namespace roam
+
+using namespace roam;
+
+extern "C" {
+
+const char* rm_last_error(void) { return g_last_error.c_str(); }
+int64_t rm_launch_count(void) { return g_launches.load(); }
+
+int rm_device_count(int* count) {
+  if (!count) return fail(RM_ERR_INVALID_ARG, "count is NULL");
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) {
+    cudaGetLastError();
+    c = 0;
+  }
+  *count = c;
+  return RM_OK;
+}
+
+static bool csr_ok(const int32_t* ptr, int32_t rows, int64_t* total) {
+  if (rows < 0) return false;
+  if (!ptr) return rows == 0 ? (*total = 0, true) : false;
+  if (ptr[0] != 0) return false;
+  for (int32_t i = 0; i < rows; ++i)
+    if (ptr[i + 1] < ptr[i]) return false;
+  *total = ptr[rows];
+  return true;
+}
+
+int rm_graph_create(const RmGraphDesc* d, uint32_t flags, RmGraph** out) {
+  if (!d || !out) return fail(RM_ERR_INVALID_ARG, "desc/out is NULL");
+  *out = nullptr;
+  const int32_t n = d->n_ops, T = d->n_tensors;
+  if (n < 0 || T < 0) return fail(RM_ERR_INVALID_ARG, "negative op/tensor count");
+  if (T > 0 && (!d->size || !d->producer)) return fail(RM_ERR_INVALID_ARG, "size/producer NULL");
+  int64_t E = 0, Ein = 0, Eout = 0;
+  if (!csr_ok(d->cons_ptr, T, &E) || !csr_ok(d->in_ptr, n, &Ein) || !csr_ok(d->out_ptr, n, &Eout))
+    return fail(RM_ERR_INVALID_ARG, "malformed CSR pointer array");
+  if ((E && !d->cons_idx) || (Ein && !d->in_idx) || (Eout && !d->out_idx))
+    return fail(RM_ERR_INVALID_ARG, "CSR index array NULL");
+
+  RmGraph* g = new RmGraph();
+  g->n = n;
+  g->T = T;
+  g->size.assign(d->size, d->size + T);
+  g->producer.assign(d->producer, d->producer + T);
+  g->cons_ptr.assign(d->cons_ptr, d->cons_ptr + T + 1);
+  g->cons_idx.assign(d->cons_idx, d->cons_idx + E);
+  g->in_ptr.assign(d->in_ptr, d->in_ptr + n + 1);
+  g->in_idx.assign(d->in_idx, d->in_idx + Ein);
+  g->out_ptr.assign(d->out_ptr, d->out_ptr + n + 1);
+  g->out_idx.assign(d->out_idx, d->out_idx + Eout);
+  if (T == 0) g->cons_ptr.assign(1, 0);
+  auto bad = [&](const std::string& m) {
+    delete g;
+    return fail(RM_ERR_GRAPH, m);
+  };
+  int64_t total = 0;
+  for (int t = 0; t < T; ++t) {
+    if (g->producer[t] < 0 || g->producer[t] >= n) return bad("producer out of range");
+    int64_t s = g->size[t];
+    uint64_t a = s < 0 ? 0ull - (uint64_t)s : (uint64_t)s;
+    if (a >= (1ull << 62) || (uint64_t)total + a >= (1ull << 62)) {
+      delete g;
+      return fail(RM_ERR_OVERFLOW, "summed tensor sizes exceed 2^62 bytes");
+    }
+    total += (int64_t)a;
+  }
+  for (int64_t k = 0; k < E; ++k)
+    if (g->cons_idx[k] < 0 || g->cons_idx[k] >= n) return bad("consumer out of range");
+  for (int64_t k = 0; k < Ein; ++k)
+    if (g->in_idx[k] < 0 || g->in_idx[k] >= T) return bad("input tensor out of range");
+  for (int64_t k = 0; k < Eout; ++k)
+    if (g->out_idx[k] < 0 || g->out_idx[k] >= T) return bad("output tensor out of range");
+
+  // direct_preds (graph.py:97-104) and its transpose
+  g->pred_ptr.assign(n + 1, 0);
+  std::vector<int32_t> tmp;
+  for (int v = 0; v < n; ++v) {
+    tmp.clear();
+    for (int k = g->in_ptr[v]; k < g->in_ptr[v + 1]; ++k) {
+      int p = g->producer[g->in_idx[k]];
+      if (p != v) tmp.push_back(p);
+    }
+    std::sort(tmp.begin(), tmp.end());
+    tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+    g->pred_idx.insert(g->pred_idx.end(), tmp.begin(), tmp.end());
+    g->pred_ptr[v + 1] = (int32_t)g->pred_idx.size();
+  }
+  g->succ_ptr.assign(n + 1, 0);
+  for (int32_t p : g->pred_idx) g->succ_ptr[p + 1]++;
+  for (int v = 0; v < n; ++v) g->succ_ptr[v + 1] += g->succ_ptr[v];
+  g->succ_idx.resize(g->pred_idx.size());
+  {
+    std::vector<int32_t> cur(g->succ_ptr.begin(), g->succ_ptr.end() - 1);
+    for (int v = 0; v < n; ++v)  // ascending v keeps each succ list sorted
+      for (int k = g->pred_ptr[v]; k < g->pred_ptr[v + 1]; ++k) g->succ_idx[cur[g->pred_idx[k]]++] = v;
+  }
+
+  RmGraphInfo& I = g->info;
+  I.n_ops = n;
+  I.n_tensors = T;
+  I.n_cons = E;
+  I.n_pred_edges = (int64_t)g->pred_idx.size();
+  I.total_bytes = total;
+  int st = build_k1_host(*g, !(flags & RM_NO_REDUCE));
+  if (st != RM_OK) {
+    delete g;
+    return st;
+  }
+
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess) {
+    cudaGetLastError();
+    ndev = 0;
+  }
+  if (ndev > 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    g->device = dev;
+    cudaError_t e = g->info.wide_index ? upload_k1<int32_t>(*g) : upload_k1<uint16_t>(*g);
+    if (!e) e = up(g->d_size, g->size);
+    if (!e) e = up(g->d_producer, g->producer);
+    if (!e) e = up(g->d_cons_ptr, g->cons_ptr);
+    if (!e) e = up(g->d_cons_idx, g->cons_idx);
+    if (!e) e = up(g->d_in_ptr, g->in_ptr);
+    if (!e) e = up(g->d_in_idx, g->in_idx);
+    if (!e) e = up(g->d_out_ptr, g->out_ptr);
+    if (!e) e = up(g->d_out_idx, g->out_idx);
+    if (!e) e = up(g->d_pred_ptr, g->pred_ptr);
+    if (!e) e = up(g->d_pred_idx, g->pred_idx);
+    if (!e) e = up(g->d_succ_ptr, g->succ_ptr);
+    if (!e) e = up(g->d_succ_idx, g->succ_idx);
+    if (e) {
+      delete g;
+      return cuda_fail(e, "rm_graph_create upload");
+    }
+  }
+  *out = g;
+  return RM_OK;
+}
+
+int rm_graph_destroy(RmGraph* g) {
+  delete g;
+  return RM_OK;
+}
+
+int rm_graph_info(const RmGraph* g, RmGraphInfo* info) {
+  if (!g || !info) return fail(RM_ERR_INVALID_ARG, "NULL argument");
+  *info = g->info;
+  return RM_OK;
+}
+
+int rm_graph_k1_export(const RmGraph* g, int32_t* vidx, int32_t* slot, int64_t* out_tab,
+                       int64_t* fs_tab, int32_t* edge_u, int32_t* edge_v, int32_t* mptr,
+                       int32_t* mcons, int64_t* msize) {
+  if (!g) return fail(RM_ERR_INVALID_ARG, "NULL graph");
+  auto cp = [](auto* dst, const auto& src) {
+    if (dst && !src.empty()) std::memcpy(dst, src.data(), src.size() * sizeof(src[0]));
+  };
+  cp(vidx, g->h_vidx);
+  cp(slot, g->h_slot);
+  cp(out_tab, g->h_out);
+  cp(fs_tab, g->h_fs);
+  cp(edge_u, g->h_edge_u);
+  cp(edge_v, g->h_edge_v);
+  cp(mptr, g->h_mptr);
+  cp(mcons, g->h_mcons);
+  cp(msize, g->h_msize);
+  return RM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,107 @@
+// Internal declarations shared by the libroam translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/roam.h"
+
+namespace roam {
+
+// ---- thread-local error reporting ----------------------------------------
+void set_error(const std::string& msg);
+int fail(int status, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+void note_launch(int64_t k = 1);
+
+#define RM_CUDA(call)                                         \
+  do {                                                        \
+    cudaError_t e_ = (call);                                  \
+    if (e_ != cudaSuccess) return ::roam::cuda_fail(e_, #call); \
+  } while (0)
+
+#define RM_LAUNCH_CHECK(what)                                  \
+  do {                                                         \
+    ::roam::note_launch();                                     \
+    cudaError_t e_ = cudaGetLastError();                       \
+    if (e_ != cudaSuccess) return ::roam::cuda_fail(e_, what); \
+  } while (0)
+
+// ---- device buffer owned by a handle --------------------------------------
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~DevBuf();
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  cudaError_t upload(const void* host, size_t nbytes);
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+// Per-call scratch: stream-ordered device allocation freed on scope exit.
+struct Scratch {
+  cudaStream_t s;
+  std::vector<void*> ptrs;
+  explicit Scratch(cudaStream_t st) : s(st) {}
+  ~Scratch();
+  template <class T>
+  cudaError_t alloc(T** out, size_t count) {
+    void* p = nullptr;
+    cudaError_t e = cudaMallocAsync(&p, count ? count * sizeof(T) : 16, s);
+    if (e == cudaSuccess) ptrs.push_back(p);
+    *out = static_cast<T*>(p);
+    return e;
+  }
+};
+
+// K1 metadata: the order evaluator never touches the raw CSR.  For a valid
+// sequential order o (pos = inverse permutation):
+//   live[i] = sum_{j<=i} ( out[o_j] - freed_after[o_{j-1}] )
+//   freed_after[v] = fs[v] + sum{ size_t : t multi, argmax_{c in maxC(t)} pos[c] == v }
+// where maxC(t) = consumers of t that are not transitive predecessors of
+// another consumer (their positions bound every consumer's), fs[v] = summed
+// size of tensors with maxC(t) == {v}; zero-consumer tensors are never freed.
+// Validity: the permutation plus every edge of the transitive reduction of
+// direct_preds (equivalent to all edges for a linear extension).
+struct K1Meta {
+  int wide = 0;              // 0: uint16 ids, 1: int32 ids
+  int64_t n_edges = 0;       // checked edges
+  int64_t n_multi = 0;
+  int64_t n_multi_cons = 0;
+  int64_t n_slots = 0;
+  int64_t n_values = 0;
+  DevBuf opmeta;             // per op {vidx, slot} (IdxT pair)
+  DevBuf table;              // longlong2 {out, fs} [n_values]
+  DevBuf edges;              // IdxT pairs (u, v) [n_edges]
+  DevBuf mptr;               // int32 [n_multi + 1]
+  DevBuf mcons;              // IdxT [n_multi_cons]
+  DevBuf msize;              // int64 [n_multi]
+};
+
+}  // namespace roam
+
+struct RmGraph {
+  int32_t n = 0, T = 0;
+  RmGraphInfo info{};
+  // host CSR
+  std::vector<int64_t> size;
+  std::vector<int32_t> producer, cons_ptr, cons_idx, in_ptr, in_idx, out_ptr, out_idx;
+  std::vector<int32_t> pred_ptr, pred_idx;   // direct_preds (dedup, sorted, no self)
+  std::vector<int32_t> succ_ptr, succ_idx;   // direct_succs
+  // host copies of K1 metadata (kept for tests / introspection)
+  std::vector<int32_t> h_vidx, h_slot;
+  std::vector<int64_t> h_out, h_fs;          // per value class
+  std::vector<int32_t> h_edge_u, h_edge_v;
+  std::vector<int32_t> h_mptr, h_mcons;
+  std::vector<int64_t> h_msize;
+  // device side
+  int device = -1;
+  roam::K1Meta k1;
+  roam::DevBuf d_size, d_producer, d_cons_ptr, d_cons_idx, d_in_ptr, d_in_idx, d_out_ptr,
+      d_out_idx, d_pred_ptr, d_pred_idx, d_succ_ptr, d_succ_idx;
+};

@@ -1,0 +1,138 @@
+"""K1 (batched order evaluator), the device candidate generator, argmin and the
+single-schedule drop-ins, against the reference's golden vectors and the
+CPU oracle.  Bit-exact (integer work)."""
+
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import coracle
+from oracle import memplan_oracle as O
+from paper_2310_19295_b200 import graphgen as gg
+from paper_2310_19295_b200.evaluator import (argmin_orders, evaluate_orders, generate_orders,
+                                             live_bytes_by_timestep, peak_memory, sequential_schedule,
+                                             tensor_lifetimes, validate_schedule)
+from paper_2310_19295_b200.graph import ConfigError, Schedule, ScheduleError, load_graph
+
+pytestmark = pytest.mark.gpu
+
+
+def _check_rows(g, rows):
+    n = len(g.ops)
+    ok_rows = [r for r in rows if len(r["order"]) == n]
+    orders = np.array([r["order"] for r in ok_rows], np.int64).reshape(len(ok_rows), n)
+    peak, arg, val = evaluate_orders(g, orders)
+    for k, r in enumerate(ok_rows):
+        e = r["expect"]
+        if isinstance(e, dict):
+            assert not val[k], r["order"]
+        else:
+            assert val[k] and (int(peak[k]), int(arg[k])) == tuple(e), r["order"]
+
+
+def test_fixture_cases():
+    P = golden("peaks")
+    graphs = {k: load_graph(v) for k, v in P["fixtures"].items()}
+    by: dict[str, list] = {}
+    for c in P["cases"]:
+        by.setdefault(c["graph"], []).append(c)
+    for name, rows in by.items():
+        _check_rows(graphs[name], rows)
+
+
+@pytest.mark.parametrize("corpus", ["small_dags", "random_dags", "training"])
+def test_corpora(corpus):
+    for e in golden("peaks")[corpus]:
+        _check_rows(load_graph(e["doc"]), e["rows"])
+
+
+@pytest.mark.parametrize("name", ["layered", "gpt2-small", "bert-large", "gpt2-xl"])
+def test_config_graphs_generator_and_golden(name):
+    entry = [e for e in golden("peaks")["configs"] if e["graph"] == name][0]
+    g = load_graph(gg.config_doc(name))
+    B = len(entry["rows"])
+    orders = generate_orders(g, 0, 0, B)
+    peak, arg, val = evaluate_orders(g, orders)
+    host = orders.cpu().numpy()
+    for k, r in enumerate(entry["rows"]):
+        assert hashlib.sha256(",".join(map(str, host[k].tolist())).encode()).hexdigest()[:16] == r["order_sha"]
+        assert bool(val[k]) and (int(peak[k]), int(arg[k])) == tuple(r["expect"])
+
+
+@pytest.mark.parametrize("name,B", [("layered", 4096), ("gpt2-small", 2048), ("gpt2-xl", 256)])
+def test_large_batch_vs_c_oracle(name, B):
+    g = load_graph(gg.config_doc(name))
+    orders = generate_orders(g, 12345, 1000, B)
+    host = orders.cpu().numpy()
+    # corrupt a few rows: swap a pred/succ pair, duplicate, out-of-range
+    host[1] = host[1][::-1]
+    host[2, 5] = host[2, 6]
+    host[3, 0] = len(g.ops)
+    cg = coracle.CGraph(g)
+    want = coracle.eval_orders(cg, host)
+    got = evaluate_orders(g, host)
+    assert np.array_equal(got[2], want[2])
+    assert np.array_equal(got[0][want[2]], want[0][want[2]])
+    assert np.array_equal(got[1][want[2]], want[1][want[2]])
+    import torch
+    dev = evaluate_orders(g, torch.from_numpy(host).cuda())
+    assert np.array_equal(dev[2].cpu().numpy(), want[2])
+    assert np.array_equal(dev[0].cpu().numpy()[want[2]], want[0][want[2]])
+    # argmin == first strict minimum, on device and host paths
+    best = O.first_strict_min(want[0].tolist(), want[2].tolist())
+    assert argmin_orders(dev[0], dev[2], id_base=7) == (best[0], best[1] + 7)
+    assert argmin_orders(got[0], got[2]) == best
+
+
+def test_generator_matches_python_restatement():
+    g = load_graph(gg.config_doc("gpt2-small"))
+    preds, succs = O.direct_preds(g), O.direct_succs(g)
+    orders = generate_orders(g, 99, 5, 8).cpu().numpy()
+    for k in range(8):
+        assert orders[k].tolist() == O.kahn_candidate(len(g.ops), preds, succs, 99, 5 + k)
+
+
+def test_argmin_ties_and_none_valid():
+    peak = np.array([7, 3, 3, 1, 3], np.int64)
+    valid = np.array([1, 1, 1, 0, 1], bool)
+    assert argmin_orders(peak, valid) == (3, 1)
+    assert argmin_orders(peak, np.zeros(5, bool)) == (2**63 - 1, -1)
+
+
+def test_single_schedule_dropins():
+    S = golden("schedules")
+    fx = {k: load_graph(v) for k, v in golden("peaks")["fixtures"].items()}
+    for c in S["packed"] + S["random"]:
+        g = fx[c["graph"]] if "graph" in c else load_graph(c["doc"])
+        s = Schedule(tuple(c["order"]), tuple(c["timesteps"]), c["ops_per_step"])
+        assert peak_memory(g, s) == tuple(c["peak"])
+        assert live_bytes_by_timestep(g, s) == c["live"]
+        if "lifetimes" in c:
+            assert [list(x) for x in tensor_lifetimes(g, s)] == c["lifetimes"]
+    g = fx["diamond"]
+    for c in S["errors"]:
+        s = Schedule(tuple(c["order"]), tuple(c["timesteps"]), c["ops_per_step"])
+        if c["error"] is None:
+            validate_schedule(g, s)
+            assert peak_memory(g, s) == tuple(c["peak"])
+            continue
+        exc = ConfigError if c["error"] == "ConfigError" else ScheduleError
+        with pytest.raises(exc) as ei:
+            validate_schedule(g, s)
+        assert str(ei.value) == c["message"]
+
+
+def test_reference_unit_answers_through_gpu():
+    MB = 1 << 20
+    fx = {k: load_graph(v) for k, v in golden("peaks")["fixtures"].items()}
+    d = fx["diamond"]
+    assert peak_memory(d, sequential_schedule(d, (0, 1, 2, 3))) == (120 * MB, 1)
+    assert peak_memory(d, sequential_schedule(d, (0, 2, 1, 3)))[0] == 90 * MB
+    assert peak_memory(fx["single"], sequential_schedule(fx["single"], (0,))) == (8, 0)
+    assert peak_memory(fx["empty"], sequential_schedule(fx["empty"], ())) == (0, 0)
+    with pytest.raises(ScheduleError):
+        sequential_schedule(d, (3, 0, 1, 2))
