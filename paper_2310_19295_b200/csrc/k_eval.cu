@@ -587,7 +587,7 @@ static int eval_impl(RmGraph* g, const int32_t* orders, int64_t B, uint32_t flag
   int st = need_device(g);
   if (st) return st;
   if (B < 0) return fail(RM_ERR_INVALID_ARG, "negative batch");
-  if (B > 0 && (!orders || !peak || !argmax || !valid))
+  if (B > 0 && ((!orders && g->n > 0) || !peak || !argmax || !valid))
     return fail(RM_ERR_INVALID_ARG, "NULL array argument");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (flags & RM_DEVICE_PTRS) {
