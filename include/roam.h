@@ -186,19 +186,29 @@ int rm_layout_violations(int64_t N, const int32_t* start, const int32_t* end,
 /* ---------------------------------------------- K3: batched LLFB packer */
 
 enum {
-  RM_LLFB_PLAIN = 0,        /* llfb_layout (layout.py:100-118) */
-  RM_LLFB_CONSTRAINED = 1,  /* constrained_llfb_layout (layout.py:121-146) */
-  RM_LLFB_COMPONENTS = 2    /* exact_layout's per-component incumbent + bound
-                               (layout.py:165-225), activations_at_bottom */
+  RM_LLFB_PLAIN = 0,          /* llfb_layout (layout.py:100-118) */
+  RM_LLFB_CONSTRAINED = 1,    /* constrained_llfb_layout (layout.py:121-146) */
+  RM_LLFB_COMPONENTS = 2,     /* exact_layout up to its search (layout.py:165-225),
+                                 activations_at_bottom=True */
+  RM_LLFB_COMPONENTS_FREE = 3 /* the same with activations_at_bottom=False */
 };
 
-/* P independent layout problems; problem p owns items [item_ptr[p],
- * item_ptr[p+1]).  Per item: tensor id, inclusive [start, end], size,
- * is_activation.  Outputs: offset[item] (int64), capacity[p]; for
- * RM_LLFB_COMPONENTS also bound[p] = 1 iff every component's incumbent met
- * its lower bound (the reference returns without search), comp[item] = the
- * component root tensor id (-1 for pre-placed activations) and
- * comp_cap[item] = that component's incumbent capacity.  Host pointers. */
+/* P independent layout problems, one CTA each; problem p owns items
+ * [item_ptr[p], item_ptr[p+1]).  Per item: tensor id, inclusive [start, end],
+ * size, is_activation.  Outputs: offset[item] (int64) and capacity[p].
+ * PLAIN / CONSTRAINED reproduce the reference packers bit-exactly (sort keys,
+ * activation stacking and floors, _lowest_fit, capacity).
+ * COMPONENTS / COMPONENTS_FREE reproduce exact_layout up to its search:
+ * activations pre-placed (bottom mode), overlap-connected components of the
+ * rest, each component's long-lived-first incumbent (offset[]) and lower
+ * bound.  bound_met[p] = 1 iff every component's incumbent capacity is <= its
+ * bound -- then the reference returns exactly this layout without search and
+ * capacity[p] is exact_layout's capacity.  comp[item] = the component's
+ * smallest tensor id (-1 for pre-placed activations), comp_cap[item] = that
+ * component's incumbent capacity.  bound_met/comp/comp_cap may be NULL for
+ * PLAIN / CONSTRAINED.  Host pointers; synchronous.  Problems of more than
+ * RM_LLFB_MAX_ITEMS items fail with RM_ERR_CAPACITY. */
+#define RM_LLFB_MAX_ITEMS 16383
 int rm_llfb_batch(int32_t P, const int64_t* item_ptr, const int32_t* tensor,
                   const int32_t* start, const int32_t* end, const int64_t* size,
                   const uint8_t* is_act, int32_t mode, int64_t* offset, int64_t* capacity,

@@ -342,7 +342,7 @@ __global__ void k_sched_check(SchedArgs a, const int32_t* __restrict__ pred_ptr,
     if (a.cnt[v] != 1) a.flags[0] = 1;
     const int t = a.ts[v];
     if (t < 0 || t >= a.steps) {
-      a.flags[0] = 1;  // unreachable when the host validated ranges
+      a.flags[3] = 1;  // padding of a short timesteps vector: reported as such
       continue;
     }
     if (atomicAdd(a.cnt_ts + t, 1) + 1 > a.ops_per_step) a.flags[2] = 1;
@@ -742,7 +742,10 @@ int rm_eval_schedule(RmGraph* g, const int32_t* order, int64_t order_len, const 
   for (int64_t i = n; i < ts_len; ++i) max_ts = std::max(max_ts, timesteps[i]);
   const int steps = ts_len ? max_ts + 1 : 0;  // Schedule.n_steps (graph.py:165-167)
   res->n_steps = steps;
-  if (ts_len < n) return fail(RM_ERR_INVALID_ARG, "timesteps shorter than n_ops");
+  // a short timesteps vector is a validation failure (graph.py:379-380) that
+  // the reference reports only after the permutation check
+  if (ts_len < n && !(flags & RM_SCHED_VALIDATE))
+    return fail(RM_ERR_INVALID_ARG, "timesteps shorter than n_ops");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   Scratch sc(s);
   int32_t *d_ts, *d_order = nullptr, *d_pos, *d_cnt, *d_cnt_ts, *d_flags, *d_birth = nullptr,
@@ -750,7 +753,10 @@ int rm_eval_schedule(RmGraph* g, const int32_t* order, int64_t order_len, const 
   unsigned long long *d_first, *d_delta = nullptr;
   long long *d_live = nullptr, *d_peak;
   RM_CUDA(sc.alloc(&d_ts, size_t(n)));
-  RM_CUDA(cudaMemcpyAsync(d_ts, timesteps, size_t(n) * 4, cudaMemcpyHostToDevice, s));
+  RM_CUDA(cudaMemsetAsync(d_ts, 0, size_t(n) * 4, s));
+  const int64_t ts_copy = std::min<int64_t>(ts_len, n);
+  if (ts_copy)
+    RM_CUDA(cudaMemcpyAsync(d_ts, timesteps, size_t(ts_copy) * 4, cudaMemcpyHostToDevice, s));
   const int TB = 256;
   auto blocks = [&](int64_t work) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(4096, (work + TB - 1) / TB));

@@ -1,8 +1,391 @@
-// K4: batched window greedy (placeholder until the kernel lands).
+// K4: batched window greedy (least-memory-increase list scheduling), one CTA
+// per window -- the greedy solver the planner runs on every window larger
+// than node_limit (planner.py:127-131) and as exact_order's incumbent.
+//
+// Reference (pkg/src/memplan/ordering.py):
+//   _Local          78-123  window-local bookkeeping: ops sorted, tracked
+//                           tensors = produced inside U live_in with their
+//                           local consumer-ENTRY counts (duplicates count),
+//                           held = live_out U produced-and-unconsumed,
+//                           start_live = sum(live_in), local precedence
+//   greedy_order   126-180  each step scores every ready op by
+//                           out_bytes - sum(size of distinct tracked, non-held
+//                           inputs whose count is 1), strict < over ascending
+//                           local index; then live += out, peak = max, each
+//                           distinct tracked input's count -= 1 and frees at 0
+//                           unless held.  (Parity hazard h1: an input listed
+//                           twice by one op is never freed by this solver.)
+//
+// Host (C++, this file): builds every window's local problem from the graph
+// handle's CSR in O(window + its consumer entries).  Device: per step, each
+// thread scores its ready ops, a block (delta, index) argmin picks the op, one
+// warp applies it (counts, frees, successor pred counts).  Mutable state
+// (pred counts, consumer counts, scheduled flags) lives in shared memory when
+// it fits, else in a per-window global scratch.
+#include <algorithm>
+#include <climits>
+
 #include "roam_internal.h"
 
-extern "C" int rm_greedy_windows(RmGraph*, int32_t, const int64_t*, const int32_t*, const int64_t*,
-                                 const int32_t*, const int64_t*, const int32_t*, int32_t*, int64_t*,
-                                 int32_t*, int32_t*, void*) {
-  return roam::fail(RM_ERR_CAPACITY, "rm_greedy_windows: not built yet");
+namespace roam {
+
+struct K4Args {
+  int W;
+  const int64_t* op_base;   // [W] window op base in the flat op arrays
+  const int32_t* nops;      // [W] ops per window (each window owns nops+1 slots)
+  const int64_t* ten_base;  // [W+1] window tensor ranges
+  const int32_t* gop;       // [NO] global op id per local op
+  const int64_t* out;       // [NO] out_bytes
+  const int32_t* npred0;    // [NO] distinct local preds
+  const int64_t* in_ptr;    // [NO+1] into in_idx (window-local tensor index)
+  const int32_t* in_idx;
+  const int64_t* succ_ptr;  // [NO+1] into succ_idx (window-local op index)
+  const int32_t* succ_idx;
+  const int32_t* count0;    // [NT_] tracked consumer-entry counts
+  const int64_t* tsize;     // [NT_]
+  const int64_t* start_live;  // [W]
+  int32_t* order;           // [NO] global op ids in schedule order
+  int64_t* peak;            // [W]
+  int32_t* status;          // [W]
+  unsigned char* gscratch;
+  const int64_t* gscratch_off;  // [W] (-1: shared memory)
+};
+
+__host__ __device__ inline size_t k4_bytes(int64_t n_ops, int64_t n_ten) {
+  auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
+  return al(4 * size_t(n_ops)) + al(size_t(n_ops)) + al(4 * size_t(n_ten));
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k4_greedy(const K4Args a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ long long s_wv[NT / 32];
+  __shared__ int s_wi[NT / 32];
+  __shared__ int s_pick;
+  __shared__ long long s_live, s_peak;
+  constexpr int NW = NT / 32;
+  const int w = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t ob = a.op_base[w], tb = a.ten_base[w];
+  const int n = a.nops[w];
+  const int nt = (int)(a.ten_base[w + 1] - tb);
+  auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
+  unsigned char* ws = a.gscratch_off[w] < 0 ? smem : a.gscratch + a.gscratch_off[w];
+  int* npred = reinterpret_cast<int*>(ws);
+  unsigned char* done = ws + al(4 * size_t(n));
+  int* cnt = reinterpret_cast<int*>(ws + al(4 * size_t(n)) + al(size_t(n)));
+  const int64_t* out = a.out + ob;
+  const int64_t* in_ptr = a.in_ptr + ob;
+  const int64_t* succ_ptr = a.succ_ptr + ob;
+  const int64_t* tsize = a.tsize + tb;
+  for (int i = tid; i < n; i += NT) {
+    npred[i] = a.npred0[ob + i];
+    done[i] = 0;
+  }
+  for (int t = tid; t < nt; t += NT) cnt[t] = a.count0[tb + t];
+  if (tid == 0) {
+    s_live = a.start_live[w];
+    s_peak = a.start_live[w];
+  }
+  __syncthreads();
+
+  for (int step = 0; step < n; ++step) {
+    // ---- score ready ops: delta = out - bytes freed by last uses
+    long long bv = LLONG_MAX;
+    int bi = INT_MAX;
+    for (int i = tid; i < n; i += NT) {
+      if (done[i] || npred[i]) continue;
+      long long freed = 0;
+      for (int64_t k = in_ptr[i]; k < in_ptr[i + 1]; ++k) {
+        const int t = __ldg(a.in_idx + k);
+        if (cnt[t] == 1) freed += tsize[t];
+      }
+      const long long d = out[i] - freed;
+      if (d < bv) {  // ascending i per thread: strict < keeps the smallest
+        bv = d;
+        bi = i;
+      }
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      const long long ov = __shfl_xor_sync(0xffffffffu, bv, d);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, d);
+      if (ov < bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if (lane == 0) {
+      s_wv[warp] = bv;
+      s_wi[warp] = bi;
+    }
+    __syncthreads();
+    // ---- warp 0 applies the pick
+    if (warp == 0) {
+      bv = lane < NW ? s_wv[lane] : LLONG_MAX;
+      bi = lane < NW ? s_wi[lane] : INT_MAX;
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) {
+        const long long ov = __shfl_xor_sync(0xffffffffu, bv, d);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, d);
+        if (ov < bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+      if (bi == INT_MAX) {
+        if (lane == 0) s_pick = -1;
+      } else {
+        long long freed = 0;
+        for (int64_t k = in_ptr[bi] + lane; k < in_ptr[bi + 1]; k += 32) {
+          const int t = __ldg(a.in_idx + k);
+          if (--cnt[t] == 0) freed += tsize[t];  // distinct inputs: no races
+        }
+        for (int64_t k = succ_ptr[bi] + lane; k < succ_ptr[bi + 1]; k += 32)
+          npred[__ldg(a.succ_idx + k)] -= 1;     // distinct successors
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) freed += __shfl_xor_sync(0xffffffffu, freed, d);
+        if (lane == 0) {
+          const long long live = s_live + out[bi];
+          s_peak = max(s_peak, live);
+          s_live = live - freed;
+          done[bi] = 1;
+          a.order[ob + step] = a.gop[ob + bi];
+          s_pick = bi;
+        }
+      }
+    }
+    __syncthreads();
+    if (s_pick < 0) {  // no ready op: the window's precedence has a cycle
+      if (tid == 0) a.status[w] = 2;
+      return;
+    }
+  }
+  if (tid == 0) {
+    a.peak[w] = s_peak;
+    a.status[w] = 0;
+  }
+}
+
+template <int NT>
+static int launch_k4_t(const K4Args& a, size_t smem, cudaStream_t s) {
+  auto kern = k4_greedy<NT>;
+  RM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<a.W, NT, smem, s>>>(a);
+  RM_LAUNCH_CHECK("k4_greedy launch");
+  return RM_OK;
+}
+
+}  // namespace roam
+
+using namespace roam;
+
+extern "C" int rm_greedy_windows(RmGraph* g, int32_t W, const int64_t* win_ptr,
+                                 const int32_t* win_ops, const int64_t* lin_ptr,
+                                 const int32_t* lin_idx, const int64_t* lout_ptr,
+                                 const int32_t* lout_idx, int32_t* order, int64_t* peak,
+                                 int32_t* status, int32_t* bad_tensor, void* stream) {
+  if (!g) return fail(RM_ERR_INVALID_ARG, "graph handle is NULL");
+  if (W < 0 || (W > 0 && (!win_ptr || !lin_ptr || !lout_ptr || !peak || !status || !bad_tensor)))
+    return fail(RM_ERR_INVALID_ARG, "bad rm_greedy_windows arguments");
+  if (W == 0) return RM_OK;
+  if (g->device < 0) return fail(RM_ERR_NO_DEVICE, "no CUDA device: libroam has no CPU path");
+  const int n = g->n, T = g->T;
+  if (win_ptr[0] != 0 || lin_ptr[0] != 0 || lout_ptr[0] != 0)
+    return fail(RM_ERR_INVALID_ARG, "CSR pointers must start at 0");
+  for (int w = 0; w < W; ++w)
+    if (win_ptr[w + 1] < win_ptr[w] || lin_ptr[w + 1] < lin_ptr[w] || lout_ptr[w + 1] < lout_ptr[w])
+      return fail(RM_ERR_INVALID_ARG, "CSR pointers must be non-decreasing");
+  if ((win_ptr[W] && (!win_ops || !order)) || (lin_ptr[W] && !lin_idx) || (lout_ptr[W] && !lout_idx))
+    return fail(RM_ERR_INVALID_ARG, "NULL window array");
+
+  // ---- host: build every window's local problem (_Local, ordering.py:84-123)
+  std::vector<int32_t> loc(n, -1), tloc(T, -1);
+  std::vector<uint8_t> is_lin(T, 0), is_lout(T, 0);
+  std::vector<int64_t> op_base(W + 1, 0), ten_base(W + 1, 0), start_live(W, 0);
+  std::vector<int32_t> gop, npred0, in_idx, succ_idx, count0;
+  std::vector<int64_t> out_b, in_ptr(1, 0), succ_ptr(1, 0), tsize;
+  std::vector<int32_t> ops, rel, tmp;
+  std::vector<std::vector<int32_t>> succ;
+  std::vector<uint8_t> held;
+  for (int w = 0; w < W; ++w) {
+    status[w] = 0;
+    bad_tensor[w] = -1;
+    ops.assign(win_ops + win_ptr[w], win_ops + win_ptr[w + 1]);
+    for (int v : ops)
+      if (v < 0 || v >= n) return fail(RM_ERR_INVALID_ARG, "window op out of range");
+    std::sort(ops.begin(), ops.end());
+    if (std::adjacent_find(ops.begin(), ops.end()) != ops.end())
+      return fail(RM_ERR_INVALID_ARG, "window lists an op twice");
+    const int nw = (int)ops.size();
+    for (int i = 0; i < nw; ++i) loc[ops[i]] = i;
+    for (int64_t k = lin_ptr[w]; k < lin_ptr[w + 1]; ++k) {
+      const int t = lin_idx[k];
+      if (t < 0 || t >= T) return fail(RM_ERR_INVALID_ARG, "live-in tensor out of range");
+      is_lin[t] = 1;
+    }
+    for (int64_t k = lout_ptr[w]; k < lout_ptr[w + 1]; ++k) {
+      const int t = lout_idx[k];
+      if (t < 0 || t >= T) return fail(RM_ERR_INVALID_ARG, "live-out tensor out of range");
+      is_lout[t] = 1;
+    }
+    // relevant = produced inside U live_in, ascending
+    rel.clear();
+    for (int v : ops)
+      for (int k = g->out_ptr[v]; k < g->out_ptr[v + 1]; ++k) rel.push_back(g->out_idx[k]);
+    for (int64_t k = lin_ptr[w]; k < lin_ptr[w + 1]; ++k) rel.push_back(lin_idx[k]);
+    std::sort(rel.begin(), rel.end());
+    rel.erase(std::unique(rel.begin(), rel.end()), rel.end());
+    held.assign(rel.size(), 0);
+    int64_t sl = 0;
+    const int64_t tb = (int64_t)tsize.size();
+    int nt = 0;
+    for (size_t r = 0; r < rel.size(); ++r) {
+      const int t = rel[r];
+      int local = 0;
+      for (int k = g->cons_ptr[t]; k < g->cons_ptr[t + 1]; ++k) local += loc[g->cons_idx[k]] >= 0;
+      const bool produced = loc[g->producer[t]] >= 0;
+      if (is_lout[t] || (produced && local == 0)) {
+        held[r] = 1;
+      } else if (is_lin[t] && local == 0) {
+        if (status[w] == 0) {
+          status[w] = 1;  // ConfigError (ordering.py:107-110); smallest id first
+          bad_tensor[w] = t;
+        }
+      }
+      if (is_lin[t]) sl += g->size[t];
+      if (!held[r]) {  // held tensors never free: the device never needs them
+        tloc[t] = nt++;
+        tsize.push_back(g->size[t]);
+        count0.push_back(local);
+      }
+    }
+    start_live[w] = sl;
+    // per op: out_bytes, distinct tracked non-held inputs, local preds
+    succ.assign(nw, {});
+    for (int i = 0; i < nw; ++i) {
+      const int v = ops[i];
+      int64_t ob = 0;
+      for (int k = g->out_ptr[v]; k < g->out_ptr[v + 1]; ++k) ob += g->size[g->out_idx[k]];
+      gop.push_back(v);
+      out_b.push_back(ob);
+      tmp.clear();
+      for (int k = g->in_ptr[v]; k < g->in_ptr[v + 1]; ++k)
+        if (tloc[g->in_idx[k]] >= 0) tmp.push_back(tloc[g->in_idx[k]]);
+      std::sort(tmp.begin(), tmp.end());
+      tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+      in_idx.insert(in_idx.end(), tmp.begin(), tmp.end());
+      in_ptr.push_back((int64_t)in_idx.size());
+      tmp.clear();
+      for (int k = g->in_ptr[v]; k < g->in_ptr[v + 1]; ++k) {
+        const int pr = g->producer[g->in_idx[k]];
+        if (loc[pr] >= 0 && pr != v) tmp.push_back(loc[pr]);
+      }
+      std::sort(tmp.begin(), tmp.end());
+      tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+      npred0.push_back((int32_t)tmp.size());
+      for (int p : tmp) succ[p].push_back(i);
+    }
+    for (int i = 0; i < nw; ++i) {
+      succ_idx.insert(succ_idx.end(), succ[i].begin(), succ[i].end());
+      succ_ptr.push_back((int64_t)succ_idx.size());
+    }
+    op_base[w + 1] = (int64_t)gop.size();
+    ten_base[w + 1] = tb + nt;
+    // reset the per-window marks
+    for (int v : ops) loc[v] = -1;
+    for (int t : rel) tloc[t] = -1;
+    for (int64_t k = lin_ptr[w]; k < lin_ptr[w + 1]; ++k) is_lin[lin_idx[k]] = 0;
+    for (int64_t k = lout_ptr[w]; k < lout_ptr[w + 1]; ++k) is_lout[lout_idx[k]] = 0;
+  }
+  // device layout: window w owns nops+1 op slots from opb_dev[w] (the extra
+  // slot is the tail entry of its in/succ pointer arrays)
+  const int64_t NO = (int64_t)gop.size();
+  std::vector<int64_t> in_ptr_w(NO + W), succ_ptr_w(NO + W);
+  std::vector<int64_t> opb_dev(W + 1);
+  {
+    int64_t q = 0;
+    for (int w = 0; w < W; ++w) {
+      opb_dev[w] = q;
+      for (int64_t i = op_base[w]; i <= op_base[w + 1]; ++i, ++q) {
+        in_ptr_w[q] = in_ptr[i];
+        succ_ptr_w[q] = succ_ptr[i];
+      }
+    }
+    opb_dev[W] = q;
+  }
+
+  // ---- device
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int dev = 0, max_smem = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const size_t limit = size_t(max_smem) - 1024;
+  std::vector<int64_t> goff(W, -1);
+  size_t gbytes = 0, smem = 16;
+  for (int w = 0; w < W; ++w) {
+    const size_t b = k4_bytes(op_base[w + 1] - op_base[w], ten_base[w + 1] - ten_base[w]);
+    if (b <= limit) {
+      smem = std::max(smem, b);
+    } else {
+      goff[w] = (int64_t)gbytes;
+      gbytes += b;
+    }
+  }
+  // op arrays are indexed op_base[w] + i on the device; the pointer arrays
+  // are indexed opb_dev[w] + i (one extra tail entry per window)
+  std::vector<int32_t> gop_w(opb_dev[W], 0), npred_w(opb_dev[W], 0);
+  std::vector<int64_t> out_w(opb_dev[W], 0);
+  for (int w = 0; w < W; ++w)
+    for (int64_t i = 0; i < op_base[w + 1] - op_base[w]; ++i) {
+      gop_w[opb_dev[w] + i] = gop[op_base[w] + i];
+      npred_w[opb_dev[w] + i] = npred0[op_base[w] + i];
+      out_w[opb_dev[w] + i] = out_b[op_base[w] + i];
+    }
+  Scratch sc(s);
+  int64_t *d_ob, *d_tb, *d_out, *d_inp, *d_sup, *d_tsz, *d_sl, *d_peak, *d_goff;
+  int32_t *d_gop, *d_np, *d_ini, *d_sui, *d_c0, *d_ord, *d_st;
+  unsigned char* d_g = nullptr;
+  auto up = [&](auto** d, const auto& v) -> cudaError_t {
+    cudaError_t e = sc.alloc(d, v.size());
+    if (e == cudaSuccess && !v.empty())
+      e = cudaMemcpyAsync(*d, v.data(), v.size() * sizeof(v[0]), cudaMemcpyHostToDevice, s);
+    return e;
+  };
+  std::vector<int32_t> nops(W);
+  for (int w = 0; w < W; ++w) nops[w] = (int32_t)(op_base[w + 1] - op_base[w]);
+  int32_t* d_nops;
+  RM_CUDA(up(&d_ob, opb_dev));
+  RM_CUDA(up(&d_nops, nops));
+  RM_CUDA(up(&d_tb, ten_base));
+  RM_CUDA(up(&d_gop, gop_w));
+  RM_CUDA(up(&d_out, out_w));
+  RM_CUDA(up(&d_np, npred_w));
+  RM_CUDA(up(&d_inp, in_ptr_w));
+  RM_CUDA(up(&d_ini, in_idx));
+  RM_CUDA(up(&d_sup, succ_ptr_w));
+  RM_CUDA(up(&d_sui, succ_idx));
+  RM_CUDA(up(&d_c0, count0));
+  RM_CUDA(up(&d_tsz, tsize));
+  RM_CUDA(up(&d_sl, start_live));
+  RM_CUDA(up(&d_goff, goff));
+  RM_CUDA(sc.alloc(&d_ord, size_t(std::max<int64_t>(opb_dev[W], 1))));
+  RM_CUDA(sc.alloc(&d_peak, size_t(W)));
+  RM_CUDA(sc.alloc(&d_st, size_t(W)));
+  if (gbytes) RM_CUDA(sc.alloc(&d_g, gbytes));
+  K4Args a{W, d_ob, d_nops, d_tb, d_gop, d_out, d_np, d_inp, d_ini, d_sup, d_sui, d_c0, d_tsz, d_sl,
+           d_ord, d_peak, d_st, d_g, d_goff};
+  int rc = launch_k4_t<256>(a, smem, s);
+  if (rc) return rc;
+  std::vector<int32_t> ord_w(opb_dev[W]), st_dev(W);
+  if (opb_dev[W])
+    RM_CUDA(cudaMemcpyAsync(ord_w.data(), d_ord, size_t(opb_dev[W]) * 4, cudaMemcpyDeviceToHost, s));
+  RM_CUDA(cudaMemcpyAsync(peak, d_peak, size_t(W) * 8, cudaMemcpyDeviceToHost, s));
+  RM_CUDA(cudaMemcpyAsync(st_dev.data(), d_st, size_t(W) * 4, cudaMemcpyDeviceToHost, s));
+  RM_CUDA(cudaStreamSynchronize(s));
+  for (int w = 0; w < W; ++w) {
+    if (status[w] == 0 && st_dev[w] != 0) status[w] = st_dev[w];
+    const int64_t nw = win_ptr[w + 1] - win_ptr[w];
+    for (int64_t i = 0; i < nw; ++i) order[win_ptr[w] + i] = ord_w[opb_dev[w] + i];
+  }
+  return RM_OK;
 }

@@ -173,8 +173,3 @@ extern "C" int rm_layout_violations(int64_t N, const int32_t* start, const int32
   return fail(RM_ERR_CAPACITY, "pair buffer overflow");
 }
 
-extern "C" int rm_llfb_batch(int32_t, const int64_t*, const int32_t*, const int32_t*,
-                             const int32_t*, const int64_t*, const uint8_t*, int32_t, int64_t*,
-                             int64_t*, uint8_t*, int32_t*, int64_t*, void*) {
-  return fail(RM_ERR_CAPACITY, "rm_llfb_batch: not built yet");
-}

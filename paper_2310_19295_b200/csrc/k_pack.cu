@@ -1,0 +1,532 @@
+// K3: batched long-lived-first (LLFB) offset packer, one CTA per layout
+// problem (the independent leaf subtasks the planner's tree decomposition
+// produces, planner.py:239-252).
+//
+// Reference (pkg/src/memplan/layout.py):
+//   _lowest_fit             71-78   lowest offset >= floor missing every placed,
+//                                   time-overlapping span (spans sorted by lo)
+//   _activation_floors      81-97   activations stacked from 0 in (-len, id)
+//                                   order; floor = block top if the item
+//                                   overlaps any activation, else 0
+//   llfb_layout            100-118  sort (-len, -size, id), lowest fit
+//   _constrained_incumbent 121-132  + constrained_llfb_layout 135-146
+//   exact_layout           153-225  union-find components, per-component
+//                                   bound and incumbent (the search itself,
+//                                   226-290, runs only when incumbent > bound)
+//
+// Per problem the CTA: loads the items into shared memory (global scratch
+// when they do not fit), bitonic-sorts the placement order, stacks the
+// activation block with a block scan, derives the floors, then places items
+// one at a time.  _lowest_fit is evaluated in parallel over the placed list
+// kept sorted by offset:  with spans sorted by lo and M_k = max(floor,
+// max_{j<k} hi_j) over the time-overlapping ones, the sweep breaks at the
+// first k with lo_k >= M_k + size and returns M_k (M_last if it never
+// breaks); ties in lo never change the result.  So one pass computes chunk
+// maxima, a block exclusive max-scan gives each chunk its entry M, a second
+// pass finds each chunk's first break, and a block min picks the first one.
+// The new item is then inserted at upper_bound(lo) with a register shift.
+#include <climits>
+
+#include "roam_internal.h"
+
+namespace roam {
+
+struct K3Args {
+  int P;
+  const int64_t* item_ptr;
+  const int32_t* tensor;
+  const int32_t* start;
+  const int32_t* end;
+  const int64_t* size;
+  const uint8_t* is_act;
+  int mode;
+  int64_t* offset;
+  int64_t* capacity;
+  uint8_t* bound_met;
+  int32_t* comp;
+  int64_t* comp_cap;
+  unsigned char* gscratch;     // per-problem working set when it exceeds smem
+  const int64_t* gscratch_off;  // [P] byte offsets (-1: use shared memory)
+};
+
+__host__ __device__ inline int k3_pow2(int n) {
+  int p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+
+// Working-set layout of one problem with N items (all offsets 16-aligned).
+struct K3Layout {
+  size_t o_sz, o_off, o_flo, o_aux, o_s, o_e, o_tid, o_ord, o_sidx, o_act, bytes;
+  __host__ __device__ K3Layout(int N) {
+    auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
+    const size_t n = size_t(N), p2 = size_t(k3_pow2(N));
+    o_sz = 0;
+    o_off = al(o_sz + 8 * n);
+    o_flo = al(o_off + 8 * n);
+    o_aux = al(o_flo + 8 * n);
+    o_s = al(o_aux + 8 * n);
+    o_e = al(o_s + 4 * n);
+    o_tid = al(o_e + 4 * n);
+    o_ord = al(o_tid + 4 * n);
+    o_sidx = al(o_ord + 4 * p2);
+    o_act = al(o_sidx + 4 * (n + 1));
+    bytes = al(o_act + n);
+  }
+};
+
+template <int NT>
+struct K3Block {
+  // block-wide helpers over NT threads (NT multiple of 32, <= 1024)
+  static constexpr int NW = NT / 32;
+  long long* wv;  // [NW]
+  int* wi;        // [NW]
+
+  __device__ long long reduce_max(long long v) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, d));
+    __syncthreads();
+    if (lane == 0) wv[w] = v;
+    __syncthreads();
+    long long r = wv[0];
+    for (int k = 1; k < NW; ++k) r = max(r, wv[k]);
+    return r;
+  }
+  __device__ long long reduce_sum(long long v) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    __syncthreads();
+    if (lane == 0) wv[w] = v;
+    __syncthreads();
+    long long r = 0;
+    for (int k = 0; k < NW; ++k) r += wv[k];
+    return r;
+  }
+  // exclusive max-scan over thread order; *total = inclusive max of all
+  __device__ long long excl_max(long long v, long long* total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    long long inc = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const long long t = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc = max(inc, t);
+    }
+    long long ex = __shfl_up_sync(0xffffffffu, inc, 1);
+    if (lane == 0) ex = LLONG_MIN;
+    __syncthreads();
+    if (lane == 31) wv[w] = inc;
+    __syncthreads();
+    long long before = LLONG_MIN, all = LLONG_MIN;
+    for (int k = 0; k < NW; ++k) {
+      if (k < w) before = max(before, wv[k]);
+      all = max(all, wv[k]);
+    }
+    *total = all;
+    return max(before, ex);
+  }
+  // exclusive sum-scan over thread order; *total = sum of all
+  __device__ long long excl_sum(long long v, long long* total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    long long inc = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const long long t = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc += t;
+    }
+    __syncthreads();
+    if (lane == 31) wv[w] = inc;
+    __syncthreads();
+    long long before = 0, all = 0;
+    for (int k = 0; k < NW; ++k) {
+      if (k < w) before += wv[k];
+      all += wv[k];
+    }
+    *total = all;
+    return before + inc - v;
+  }
+  // (min key, its value) over the block; key INT_MAX = none
+  __device__ int min_key(int key, long long val, long long* out_val) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      const int ok = __shfl_xor_sync(0xffffffffu, key, d);
+      const long long ov = __shfl_xor_sync(0xffffffffu, val, d);
+      if (ok < key) {
+        key = ok;
+        val = ov;
+      }
+    }
+    __syncthreads();
+    if (lane == 0) {
+      wi[w] = key;
+      wv[w] = val;
+    }
+    __syncthreads();
+    int k = wi[0];
+    long long v = wv[0];
+    for (int q = 1; q < NW; ++q)
+      if (wi[q] < k) {
+        k = wi[q];
+        v = wv[q];
+      }
+    *out_val = v;
+    return k;
+  }
+};
+
+template <int NT, int MAXC>
+__global__ void __launch_bounds__(NT) k3_llfb(const K3Args a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ long long s_wv[NT / 32];
+  __shared__ int s_wi[NT / 32];
+  K3Block<NT> blk{s_wv, s_wi};
+  const int p = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int64_t base = a.item_ptr[p];
+  const int N = (int)(a.item_ptr[p + 1] - base);
+  const bool bottom = a.mode == RM_LLFB_CONSTRAINED || a.mode == RM_LLFB_COMPONENTS;
+  const bool comps = a.mode == RM_LLFB_COMPONENTS || a.mode == RM_LLFB_COMPONENTS_FREE;
+  if (N == 0) {
+    if (tid == 0) {
+      a.capacity[p] = 0;
+      if (a.bound_met) a.bound_met[p] = 1;
+    }
+    return;
+  }
+  const K3Layout L(N);
+  unsigned char* ws = a.gscratch_off[p] < 0 ? smem : a.gscratch + a.gscratch_off[p];
+  long long* sz = reinterpret_cast<long long*>(ws + L.o_sz);
+  long long* off = reinterpret_cast<long long*>(ws + L.o_off);
+  long long* flo = reinterpret_cast<long long*>(ws + L.o_flo);
+  int* st = reinterpret_cast<int*>(ws + L.o_s);
+  int* en = reinterpret_cast<int*>(ws + L.o_e);
+  int* tn = reinterpret_cast<int*>(ws + L.o_tid);
+  int* ord = reinterpret_cast<int*>(ws + L.o_ord);
+  int* sidx = reinterpret_cast<int*>(ws + L.o_sidx);
+  unsigned char* act = ws + L.o_act;
+  const int P2 = k3_pow2(N);
+
+  for (int i = tid; i < N; i += NT) {
+    sz[i] = a.size[base + i];
+    st[i] = a.start[base + i];
+    en[i] = a.end[base + i];
+    tn[i] = a.tensor[base + i];
+    act[i] = (bottom && a.is_act[base + i]) ? 1 : 0;  // group 0 = stacked activations
+    off[i] = 0;
+    flo[i] = 0;
+  }
+  for (int i = tid; i < P2; i += NT) ord[i] = i < N ? i : -1;
+  __syncthreads();
+
+  // ---- placement order: activations by (-len, id); the rest by (-len, -size, id)
+  auto less = [&](int x, int y) -> bool {
+    if (x < 0) return false;
+    if (y < 0) return true;
+    const int gx = act[x] ? 0 : 1, gy = act[y] ? 0 : 1;
+    if (gx != gy) return gx < gy;
+    const long long lx = (long long)en[x] - st[x], ly = (long long)en[y] - st[y];
+    if (lx != ly) return lx > ly;
+    if (gx == 1 && sz[x] != sz[y]) return sz[x] > sz[y];
+    if (tn[x] != tn[y]) return tn[x] < tn[y];
+    return x < y;
+  };
+  for (int k = 2; k <= P2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = tid; t < (P2 >> 1); t += NT) {
+        const int i = ((t & ~(j - 1)) << 1) | (t & (j - 1));  // lower index of the pair
+        const int l = i | j;
+        const bool up = (i & k) == 0;
+        const int x = ord[i], y = ord[l];
+        if (up ? less(y, x) : less(x, y)) {
+          ord[i] = y;
+          ord[l] = x;
+        }
+      }
+      __syncthreads();
+    }
+  }
+
+  // ---- activation block: stacked from 0 in sorted order (block scan)
+  int A = 0;
+  {
+    long long cnt = 0;
+    for (int i = tid; i < N; i += NT) cnt += act[i];
+    A = (int)blk.reduce_sum(cnt);
+  }
+  long long block_top = 0;
+  {
+    const int C = (A + NT - 1) / NT;
+    const int k0 = min(A, tid * C), k1 = min(A, k0 + C);
+    long long run = 0;
+    for (int k = k0; k < k1; ++k) run += sz[ord[k]];
+    long long total;
+    long long pre = blk.excl_sum(run, &total);
+    for (int k = k0; k < k1; ++k) {
+      off[ord[k]] = pre;
+      pre += sz[ord[k]];
+    }
+    block_top = total;
+  }
+  // floors: block top if the item overlaps any activation (layout.py:95)
+  if (A > 0) {
+    for (int i = tid; i < N; i += NT) {
+      if (act[i]) continue;
+      bool hit = false;
+      for (int k = 0; k < A && !hit; ++k) {
+        const int q = ord[k];
+        hit = st[q] <= en[i] && st[i] <= en[q];
+      }
+      flo[i] = hit ? block_top : 0;
+    }
+  }
+  // placed list sorted by offset: activations first when they are obstacles
+  int P = (a.mode == RM_LLFB_CONSTRAINED) ? A : 0;
+  for (int k = tid; k < P; k += NT) sidx[k] = ord[k];
+  __syncthreads();
+
+  // ---- sequential placement, parallel _lowest_fit
+  long long cap_rest = LLONG_MIN;
+  for (int k = A; k < N; ++k) {
+    const int i = ord[k];
+    const int si = st[i], ei = en[i];
+    const long long szi = sz[i], fl = flo[i];
+    const int C = (P + NT) / NT;  // chunk covers [0, P] so index P has an owner
+    const int j0 = tid * C, j1 = min(P, j0 + C);
+    long long mx = LLONG_MIN;
+    for (int j = j0; j < j1; ++j) {
+      const int q = sidx[j];
+      if (st[q] <= ei && si <= en[q]) mx = max(mx, off[q] + sz[q]);
+    }
+    long long all_mx;
+    long long M = max(fl, blk.excl_max(mx, &all_mx));
+    int brk = INT_MAX;
+    long long at = 0;
+    for (int j = j0; j < j1; ++j) {
+      const int q = sidx[j];
+      if (st[q] <= ei && si <= en[q]) {
+        const long long lo = off[q];
+        if (M + szi <= lo) {
+          brk = j;
+          at = M;
+          break;
+        }
+        M = max(M, lo + sz[q]);
+      }
+    }
+    long long res;
+    if (blk.min_key(brk, at, &res) == INT_MAX) res = max(fl, all_mx);
+    // insert at upper_bound(lo = res): the elements with lo > res are a
+    // suffix of the sorted list and each shifts right by one
+    int jm = j1;
+    for (int j = j0; j < j1; ++j)
+      if (off[sidx[j]] > res) {
+        jm = j;
+        break;
+      }
+    const bool owner = jm < j1 && (jm == 0 || off[sidx[jm - 1]] <= res);
+    int kv[MAXC];
+#pragma unroll
+    for (int m = 0; m < MAXC; ++m)
+      if (jm + m < j1) kv[m] = sidx[jm + m];
+    const bool tail_owner = (P >= j0 && P < j0 + C) && (P == 0 || off[sidx[P - 1]] <= res);
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < MAXC; ++m)
+      if (jm + m < j1) sidx[jm + m + 1] = kv[m];
+    if (owner) sidx[jm] = i;
+    if (tail_owner) sidx[P] = i;
+    if (tid == 0) off[i] = res;
+    cap_rest = max(cap_rest, res + szi);
+    ++P;
+    __syncthreads();
+  }
+  if (tid == 0) {
+    // capacity starts at the activation block (layout.py:127, 199)
+    long long cap = max(block_top, cap_rest == LLONG_MIN ? 0 : cap_rest);
+    a.capacity[p] = cap;
+  }
+  for (int i = tid; i < N; i += NT) a.offset[base + i] = off[i];
+  if (!comps) return;
+
+  // ---- exact_layout components (layout.py:176-225), O(N^2) per problem.
+  // Components of the interval overlap graph are the maximal runs in start
+  // order: item i opens a run iff no j has start_j < start_i <= end_j; its
+  // label is the largest run-opening start <= start_i.
+  int* lab = sidx;  // placement is done: reuse
+  __syncthreads();
+  for (int i = tid; i < N; i += NT) {
+    if (act[i]) continue;
+    bool inner = false;
+    for (int j = 0; j < N && !inner; ++j)
+      inner = !act[j] && st[j] < st[i] && st[i] <= en[j];
+    lab[i] = inner ? INT_MIN : st[i];
+  }
+  __syncthreads();
+  for (int i = tid; i < N; i += NT) {
+    if (act[i] || lab[i] != INT_MIN) continue;
+    int best = INT_MIN;
+    for (int j = 0; j < N; ++j)
+      if (!act[j] && lab[j] != INT_MIN && st[j] <= st[i] && st[j] > best) best = st[j];
+    ord[i] = best;  // stash (ord is free now); label of a non-opening item
+  }
+  __syncthreads();
+  for (int i = tid; i < N; i += NT)
+    if (!act[i] && lab[i] == INT_MIN) lab[i] = ord[i];
+  __syncthreads();
+  // probe value at each item's start: live bytes of its component, and
+  // block top + the floored ones (layout.py:209-217)
+  long long* probe = reinterpret_cast<long long*>(ws + L.o_aux);
+  for (int j = tid; j < N; j += NT) {
+    if (act[j]) continue;
+    const int lj = lab[j], t = st[j];
+    long long total = 0, above = 0;
+    for (int q = 0; q < N; ++q) {
+      if (act[q] || lab[q] != lj || !(st[q] <= t && t <= en[q])) continue;
+      total += sz[q];
+      if (flo[q]) above += sz[q];
+    }
+    probe[j] = max(total, above ? block_top + above : 0LL);
+  }
+  __syncthreads();
+  // per item: root (min id), incumbent capacity and bound of its component
+  bool met = true;
+  for (int i = tid; i < N; i += NT) {
+    if (act[i]) {
+      a.comp[base + i] = -1;
+      a.comp_cap[base + i] = 0;
+      continue;
+    }
+    const int li = lab[i];
+    int root = INT_MAX;
+    long long ccap = 0, bound = 0;
+    for (int j = 0; j < N; ++j) {
+      if (act[j] || lab[j] != li) continue;
+      root = min(root, tn[j]);
+      ccap = max(ccap, off[j] + sz[j]);
+      bound = max(bound, probe[j]);
+    }
+    a.comp[base + i] = root;
+    a.comp_cap[base + i] = ccap;
+    if (ccap > bound) met = false;
+  }
+  const int all_met = __syncthreads_and(met ? 1 : 0);
+  if (tid == 0) a.bound_met[p] = all_met ? 1 : 0;
+}
+
+static int sm_max_smem(int dev) {
+  int v = 0;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  return v;
+}
+
+template <int NT, int MAXC>
+static int launch_k3_t(const K3Args& a, int grid, size_t smem, cudaStream_t s) {
+  auto kern = k3_llfb<NT, MAXC>;
+  RM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<grid, NT, smem, s>>>(a);
+  RM_LAUNCH_CHECK("k3_llfb launch");
+  return RM_OK;
+}
+
+}  // namespace roam
+
+using namespace roam;
+
+extern "C" int rm_llfb_batch(int32_t P, const int64_t* item_ptr, const int32_t* tensor,
+                             const int32_t* start, const int32_t* end, const int64_t* size,
+                             const uint8_t* is_act, int32_t mode, int64_t* offset,
+                             int64_t* capacity, uint8_t* bound_met, int32_t* comp,
+                             int64_t* comp_cap, void* stream) {
+  if (P < 0 || !item_ptr || !capacity || mode < 0 || mode > 3)
+    return fail(RM_ERR_INVALID_ARG, "bad rm_llfb_batch arguments");
+  if (P == 0) return RM_OK;
+  if (item_ptr[0] != 0) return fail(RM_ERR_INVALID_ARG, "item_ptr[0] must be 0");
+  int maxN = 0;
+  for (int p = 0; p < P; ++p) {
+    const int64_t n = item_ptr[p + 1] - item_ptr[p];
+    if (n < 0) return fail(RM_ERR_INVALID_ARG, "item_ptr must be non-decreasing");
+    if (n > RM_LLFB_MAX_ITEMS) return fail(RM_ERR_CAPACITY, "layout problem exceeds RM_LLFB_MAX_ITEMS");
+    maxN = std::max<int>(maxN, (int)n);
+  }
+  const int64_t NI = item_ptr[P];
+  if (NI > 0 && (!tensor || !start || !end || !size || !is_act || !offset))
+    return fail(RM_ERR_INVALID_ARG, "NULL item array");
+  const bool comps = mode >= RM_LLFB_COMPONENTS;
+  if (comps && (!bound_met || !comp || !comp_cap))
+    return fail(RM_ERR_INVALID_ARG, "component outputs are required for COMPONENTS modes");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(RM_ERR_NO_DEVICE, "no CUDA device: libroam has no CPU path");
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // shared memory holds any problem up to the opt-in limit; larger ones work
+  // out of a global scratch region (L1/L2 cached)
+  const size_t limit = (size_t)sm_max_smem(dev) - 1024;
+  std::vector<int64_t> goff(P, -1);
+  size_t gbytes = 0, smem = 0;
+  for (int p = 0; p < P; ++p) {
+    const int n = (int)(item_ptr[p + 1] - item_ptr[p]);
+    if (n == 0) continue;
+    const size_t b = K3Layout(n).bytes;
+    if (b <= limit) {
+      smem = std::max(smem, b);
+    } else {
+      goff[p] = (int64_t)gbytes;
+      gbytes += b;
+    }
+  }
+  Scratch sc(s);
+  int64_t *d_ptr, *d_sz, *d_off, *d_cap, *d_goff, *d_ccap = nullptr;
+  int32_t *d_t, *d_s, *d_e, *d_comp = nullptr;
+  uint8_t *d_act, *d_met = nullptr;
+  unsigned char* d_g = nullptr;
+  const size_t ni = size_t(std::max<int64_t>(NI, 1));
+  RM_CUDA(sc.alloc(&d_ptr, size_t(P) + 1));
+  RM_CUDA(sc.alloc(&d_t, ni));
+  RM_CUDA(sc.alloc(&d_s, ni));
+  RM_CUDA(sc.alloc(&d_e, ni));
+  RM_CUDA(sc.alloc(&d_sz, ni));
+  RM_CUDA(sc.alloc(&d_act, ni));
+  RM_CUDA(sc.alloc(&d_off, ni));
+  RM_CUDA(sc.alloc(&d_cap, size_t(P)));
+  RM_CUDA(sc.alloc(&d_goff, size_t(P)));
+  if (comps) {
+    RM_CUDA(sc.alloc(&d_met, size_t(P)));
+    RM_CUDA(sc.alloc(&d_comp, ni));
+    RM_CUDA(sc.alloc(&d_ccap, ni));
+  }
+  if (gbytes) RM_CUDA(sc.alloc(&d_g, gbytes));
+  RM_CUDA(cudaMemcpyAsync(d_ptr, item_ptr, (size_t(P) + 1) * 8, cudaMemcpyHostToDevice, s));
+  RM_CUDA(cudaMemcpyAsync(d_goff, goff.data(), size_t(P) * 8, cudaMemcpyHostToDevice, s));
+  if (NI > 0) {
+    RM_CUDA(cudaMemcpyAsync(d_t, tensor, size_t(NI) * 4, cudaMemcpyHostToDevice, s));
+    RM_CUDA(cudaMemcpyAsync(d_s, start, size_t(NI) * 4, cudaMemcpyHostToDevice, s));
+    RM_CUDA(cudaMemcpyAsync(d_e, end, size_t(NI) * 4, cudaMemcpyHostToDevice, s));
+    RM_CUDA(cudaMemcpyAsync(d_sz, size, size_t(NI) * 8, cudaMemcpyHostToDevice, s));
+    RM_CUDA(cudaMemcpyAsync(d_act, is_act, size_t(NI), cudaMemcpyHostToDevice, s));
+  }
+  K3Args a{P, d_ptr, d_t, d_s, d_e, d_sz, d_act, mode, d_off, d_cap, d_met, d_comp, d_ccap, d_g,
+           d_goff};
+  int rc;
+  if (maxN <= 255 * 16 + 15 && maxN < 4096)
+    rc = launch_k3_t<256, 16>(a, P, smem, s);
+  else
+    rc = launch_k3_t<1024, 16>(a, P, smem, s);
+  if (rc) return rc;
+  RM_CUDA(cudaMemcpyAsync(capacity, d_cap, size_t(P) * 8, cudaMemcpyDeviceToHost, s));
+  if (NI > 0) RM_CUDA(cudaMemcpyAsync(offset, d_off, size_t(NI) * 8, cudaMemcpyDeviceToHost, s));
+  if (comps) {
+    RM_CUDA(cudaMemcpyAsync(bound_met, d_met, size_t(P), cudaMemcpyDeviceToHost, s));
+    if (NI > 0) {
+      RM_CUDA(cudaMemcpyAsync(comp, d_comp, size_t(NI) * 4, cudaMemcpyDeviceToHost, s));
+      RM_CUDA(cudaMemcpyAsync(comp_cap, d_ccap, size_t(NI) * 8, cudaMemcpyDeviceToHost, s));
+    }
+  }
+  RM_CUDA(cudaStreamSynchronize(s));
+  return RM_OK;
+}

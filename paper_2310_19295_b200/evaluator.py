@@ -118,7 +118,7 @@ def _run_schedule(g, s: Schedule, flags: int, want_spans: bool = False, want_liv
     dg = device_graph(g)
     order = _as_i32(s.order)
     ts = _as_i32(s.timesteps)
-    if len(ts) < dg.n_ops:
+    if len(ts) < dg.n_ops and not (flags & _lib.RM_SCHED_VALIDATE):
         raise IndexError("tuple index out of range")  # reference indexes s.timesteps[op]
     if ts.size and ts.min() < 0:
         raise ValueError("negative timesteps are not supported")

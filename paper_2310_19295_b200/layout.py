@@ -9,12 +9,15 @@ reference's ``memplan.layout`` / ``memplan.simulator`` hot-path functions.
   conflict_pairs         layout.py:420-429   -> K2 (repair_conflicts' detector)
   llfb_layout            layout.py:100-118   -> rm_llfb_batch PLAIN (K3)
   constrained_llfb_layout layout.py:121-146  -> rm_llfb_batch CONSTRAINED (K3)
-  solve_layouts          planner.py:134-138 batch dispatch (_pool_map of _solve_layout)
+  exact_layout           layout.py:153-302   -> rm_llfb_batch COMPONENTS (K3; the
+                                              search only if incumbent > bound)
+  pack_batch             planner.py:250-252 batch dispatch (_pool_map of _solve_layout)
 """
 
 from __future__ import annotations
 
 import ctypes as C
+import time
 from dataclasses import dataclass, field
 from typing import Mapping, Sequence
 
@@ -142,3 +145,204 @@ def replay_static(g, s: Schedule, m) -> tuple[int, list[str]]:
     items = items_from_schedule(g, s)
     flags, off, pairs, mx = _k2(items, m.offsets, m.capacity, 1024)
     return int(mx), _messages(items, m.capacity, flags, off, pairs)
+
+
+# ------------------------------------------------------ K3: batched packer
+
+PLAIN, CONSTRAINED, COMPONENTS, COMPONENTS_FREE = (_lib.RM_LLFB_PLAIN, _lib.RM_LLFB_CONSTRAINED,
+                                                   _lib.RM_LLFB_COMPONENTS, 3)
+
+
+@dataclass(frozen=True)
+class PackResult:
+    """One problem's K3 output: offsets by tensor id, capacity, and for the
+    component modes whether every component's incumbent met its bound."""
+    offsets: dict[int, int]
+    capacity: int
+    bound_met: bool = True
+    comp_cap: dict[int, int] = field(default_factory=dict)  # component root -> incumbent cap
+
+
+def pack_batch(problems: Sequence[Sequence], mode: int) -> list[PackResult]:
+    """Run K3 over many independent item lists in ONE launch (one CTA per
+    problem): the batch form of the planner's ``_pool_map(_solve_layout)``
+    (planner.py:250-252)."""
+    _lib.require_device()
+    P = len(problems)
+    if P == 0:
+        return []
+    counts = np.fromiter((len(p) for p in problems), np.int64, P)
+    item_ptr = np.zeros(P + 1, np.int64)
+    np.cumsum(counts, out=item_ptr[1:])
+    flat = [it for p in problems for it in p]
+    NI = len(flat)
+    start, end, size = _item_arrays(flat)
+    tensor = np.fromiter((i.tensor for i in flat), np.int64, NI)
+    if NI and (tensor.min() < 0 or tensor.max() >= 2**31):
+        raise ValueError("tensor ids must fit int32")
+    tensor = tensor.astype(np.int32)
+    is_act = np.fromiter((bool(i.is_activation) for i in flat), np.uint8, NI)
+    offset = np.empty(max(NI, 1), np.int64)
+    cap = np.empty(P, np.int64)
+    comps = mode in (COMPONENTS, COMPONENTS_FREE)
+    met = np.ones(P, np.uint8) if comps else None
+    comp = np.empty(max(NI, 1), np.int32) if comps else None
+    ccap = np.empty(max(NI, 1), np.int64) if comps else None
+    check(lib().rm_llfb_batch(P, ptr(item_ptr), ptr(tensor), ptr(start), ptr(end), ptr(size),
+                              ptr(is_act), int(mode), ptr(offset), ptr(cap), ptr(met), ptr(comp),
+                              ptr(ccap), None), "rm_llfb_batch")
+    out = []
+    off_l, ten_l = offset[:NI].tolist(), tensor.tolist()
+    for p in range(P):
+        a, b = int(item_ptr[p]), int(item_ptr[p + 1])
+        offs = dict(zip(ten_l[a:b], off_l[a:b]))
+        if comps:
+            cc = {int(r): int(c) for r, c in zip(comp[a:b].tolist(), ccap[a:b].tolist()) if r >= 0}
+            out.append(PackResult(offs, int(cap[p]), bool(met[p]), cc))
+        else:
+            out.append(PackResult(offs, int(cap[p])))
+    return out
+
+
+def _act_block(items) -> int:
+    return sum(i.size for i in items if i.is_activation)
+
+
+def llfb_layout(p) -> MemoryLayout:
+    """Long-lived-first best fit (layout.py:100-118) on the GPU (K3 PLAIN)."""
+    t0 = time.monotonic()
+    r = pack_batch([p.items], PLAIN)[0]
+    return MemoryLayout(offsets=r.offsets, capacity=r.capacity, activation_block=_act_block(p.items),
+                        optimal=False, stats=LayoutStats(len(p.items), time.monotonic() - t0))
+
+
+def constrained_llfb_layout(p) -> MemoryLayout:
+    """Long-lived-first fallback keeping the activation block at the bottom
+    (layout.py:121-146) on the GPU (K3 CONSTRAINED)."""
+    t0 = time.monotonic()
+    r = pack_batch([p.items], CONSTRAINED)[0]
+    return MemoryLayout(offsets=r.offsets, capacity=r.capacity, activation_block=_act_block(p.items),
+                        optimal=False, stats=LayoutStats(len(p.items), time.monotonic() - t0))
+
+
+class SearchRequired(RuntimeError):
+    """exact_layout's incumbent missed its lower bound: the branch-and-bound
+    (layout.py:226-290) must run; pass ``search=`` to delegate it."""
+
+
+def exact_layout(p, search=None) -> MemoryLayout:
+    """exact_layout (layout.py:153-302) decided on the GPU whenever every
+    overlap component's long-lived-first incumbent meets its lower bound --
+    then the reference returns that incumbent without search, and so does
+    this.  Otherwise ``search(p)`` is called (e.g. the reference's own
+    exact_layout) or SearchRequired is raised."""
+    t0 = time.monotonic()
+    if p.time_budget <= 0:
+        from .graph import ConfigError
+        raise ConfigError("time budget must be positive")
+    if not p.items:
+        return MemoryLayout(offsets={}, capacity=0, stats=LayoutStats(0, 0.0))
+    r = exact_layout_batch([p])[0]
+    if r is not None:
+        return r
+    if search is None:
+        raise SearchRequired("layout incumbent above its bound: branch-and-bound needed")
+    return search(p)
+
+
+def exact_layout_batch(problems: Sequence) -> list[MemoryLayout | None]:
+    """K3 component pass over many exact_layout problems in one launch; None
+    where the search would run (incumbent above bound)."""
+    t0 = time.monotonic()
+    out: list[MemoryLayout | None] = [None] * len(problems)
+    for bottom in (True, False):
+        idx = [k for k, p in enumerate(problems) if bool(p.activations_at_bottom) == bottom]
+        if not idx:
+            continue
+        res = pack_batch([problems[k].items for k in idx], COMPONENTS if bottom else COMPONENTS_FREE)
+        for k, r in zip(idx, res):
+            p = problems[k]
+            if not p.items:
+                out[k] = MemoryLayout(offsets={}, capacity=0, stats=LayoutStats(0, 0.0))
+            elif r.bound_met:
+                out[k] = MemoryLayout(offsets=r.offsets, capacity=r.capacity,
+                                      activation_block=_act_block(p.items), optimal=True,
+                                      stats=LayoutStats(0, time.monotonic() - t0))
+    return out
+
+
+# --------------------------------------------------------- conflict repair
+
+def repair_conflicts(m, p):
+    """Re-place the smaller, shorter-lived member of every conflicting pair
+    (layout.py:409-470).  Conflict detection -- the O(N^2) part, 91.5 s of
+    279 s at 10.8k ops in the reference -- is K2; mover placement (best-fit
+    gap, strict < on gap size so the lowest-addressed smallest gap wins) is a
+    vectorised host sweep per mover.  Returns ``dataclasses.replace(m, ...)``
+    so the caller's layout type is preserved."""
+    from dataclasses import replace
+
+    from .graph import StructuralError
+    items = sorted(p.items, key=lambda i: i.tensor)
+    by_id = {i.tensor: i for i in p.items}
+    offsets = dict(m.offsets)
+    capacity = m.capacity
+    N = len(items)
+    tid = np.fromiter((i.tensor for i in items), np.int64, N)
+    st, en, sz = _item_arrays(items)
+    st64, en64 = st.astype(np.int64), en.astype(np.int64)
+
+    def conflicts():
+        return conflict_pairs(items, offsets) if N > 1 else []
+
+    def mover(a, b):
+        if a.is_activation != b.is_activation:
+            return b if a.is_activation else a
+        ka = (a.size, a.end - a.start, -a.tensor)
+        kb = (b.size, b.end - b.start, -b.tensor)
+        return a if ka < kb else b
+
+    # offsets keyed by items' tensors (every item of p has one after concat)
+    has = np.fromiter((t in offsets for t in tid.tolist()), bool, N)
+    for _ in range(N + 1):
+        pairs = conflicts()
+        if not pairs:
+            break
+        movers = sorted({mover(items[a], items[b]).tensor for a, b in pairs},
+                        key=lambda t: (by_id[t].size, by_id[t].end - by_id[t].start, t))
+        off = np.fromiter((offsets.get(t, 0) for t in tid.tolist()), np.int64, N)
+        pos = {t: k for k, t in enumerate(tid.tolist())}
+        for t in movers:
+            k = pos[t]
+            it = by_id[t]
+            sel = has & (st64 <= it.end) & (it.start <= en64)
+            sel[k] = False
+            lo = off[sel]
+            hi = lo + sz[sel]
+            o = np.argsort(lo, kind="stable")
+            lo, hi = lo[o], hi[o]
+            if lo.size:
+                edge_before = np.maximum.accumulate(np.concatenate(([0], hi[:-1])))
+                edge_before = np.maximum(edge_before, 0)
+                gap = lo > edge_before
+                g_lo, g_hi = edge_before[gap], lo[gap]
+                edge = int(max(0, hi.max()))
+            else:
+                g_lo = g_hi = np.zeros(0, np.int64)
+                edge = 0
+            if capacity > edge:
+                g_lo = np.append(g_lo, edge)
+                g_hi = np.append(g_hi, capacity)
+            width = g_hi - g_lo
+            fit = np.flatnonzero(width >= it.size)
+            if fit.size:
+                best = fit[np.argmin(width[fit])]   # first of the smallest
+                new = int(g_lo[best])
+            else:
+                new = edge
+            offsets[t] = new
+            off[k] = new
+            capacity = max(capacity, new + it.size)
+    if conflicts():
+        raise StructuralError("conflict repair did not converge")
+    return replace(m, offsets=offsets, capacity=capacity)

@@ -1,0 +1,171 @@
+"""Drop-in of the B200 hot path into the reference planner (``memplan``).
+
+The reference has no plugin registry: its planner resolves the hot-path
+functions as module globals at call time (planner.py:16-51, simulator.py:15-16,
+cli.py:14-40).  ``install()`` rebinds exactly those globals to the GPU
+implementations in this package, so the reference's own ``plan(g, cfg)`` /
+``compare_baselines`` / ``replay_static`` / CLI run unchanged on top of
+libroam; ``uninstall()`` restores the originals.
+
+Dispatch points rebound (reference file:line of the call site):
+  planner.peak_memory            planner.py:212    weight-update candidate argmin
+  planner.tensor_lifetimes       planner.py:227    layout item lifetimes
+  planner.live_bytes_by_timestep planner.py:264    boundary peaks
+  planner._pool_map              planner.py:155-157, 250-252  the batch dispatch:
+        _solve_window jobs -> every greedy window in ONE K4 launch, exact
+                              windows stay on the reference's exact_order
+        _solve_layout jobs -> every leaf in ONE K3 launch per mode
+                              (constrained LLFB for big leaves, exact_layout's
+                              incumbent+bound for small ones; the reference's
+                              branch-and-bound only where incumbent > bound)
+  planner.repair_conflicts       planner.py:259    K2 detection + mover placement
+  planner.validate_layout        planner.py:260    K2
+  layout.layout_violations / simulator.layout_violations / simulator.peak_memory
+  graph.peak_memory / tensor_lifetimes / live_bytes_by_timestep (module-level users)
+
+Results are bit-identical to the unpatched reference: the plan document bytes
+(``plan_doc_bytes``) are the parity artefact (tests/test_gpu_plan.py).
+"""
+
+from __future__ import annotations
+
+import functools
+import importlib
+import sys
+import time
+from pathlib import Path
+
+from . import evaluator as _ev
+from . import layout as _lay
+from . import ordering as _ord
+from .graph import GraphError
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def load_memplan():
+    """Import the reference package: an installed ``memplan`` or the copy the
+    driver installs under baseline/_ref (pip --target)."""
+    try:
+        return importlib.import_module("memplan")
+    except ImportError:
+        ref = ROOT / "baseline" / "_ref"
+        if (ref / "memplan").is_dir() and str(ref) not in sys.path:
+            sys.path.insert(0, str(ref))
+        return importlib.import_module("memplan")
+
+
+def _translate(mp, fn):
+    """Re-raise this package's errors as the reference's classes (same names,
+    same messages), so callers' except clauses keep working."""
+
+    @functools.wraps(fn)
+    def wrapper(*a, **k):
+        try:
+            return fn(*a, **k)
+        except GraphError as e:
+            cls = getattr(mp.graph, type(e).__name__, None)
+            if cls is None:
+                raise
+            raise cls(str(e)) from None
+    return wrapper
+
+
+class _State:
+    installed = None  # (memplan module, {(module, name): original})
+
+
+def install(mp=None):
+    """Rebind the reference's hot-path globals to libroam; idempotent."""
+    mp = mp or load_memplan()
+    if _State.installed is not None:
+        return mp
+    pl, lay, sim, gr, ordm = mp.planner, mp.layout, mp.simulator, mp.graph, mp.ordering
+    orig_solve_window = pl._solve_window
+    orig_solve_layout = pl._solve_layout
+    orig_pool_map = pl._pool_map
+    ref_exact_layout = lay.exact_layout
+    ref_exact_order = ordm.exact_order
+
+    def to_layout(m):
+        return lay.MemoryLayout(offsets=m.offsets, capacity=m.capacity,
+                                activation_block=m.activation_block, optimal=m.optimal,
+                                stats=lay.LayoutStats(m.stats.nodes, m.stats.wall_time))
+
+    def solve_windows(jobs):
+        out = [None] * len(jobs)
+        greedy = [k for k, (p, limit) in enumerate(jobs) if len(p.ops) > limit]
+        sols = _ord.greedy_orders([jobs[k][0] for k in greedy], solution_type=ordm.OrderingSolution,
+                                  stats_type=ordm.SolverStats)
+        for k, s in zip(greedy, sols):
+            out[k] = s
+        for k, (p, limit) in enumerate(jobs):
+            if out[k] is None:
+                out[k] = ref_exact_order(p)   # exact DFS stays the reference's
+        return out
+
+    def solve_layouts(jobs):
+        out = [None] * len(jobs)
+        big = [k for k, (p, limit) in enumerate(jobs) if len(p.items) > limit]
+        small = [k for k, (p, limit) in enumerate(jobs) if len(p.items) <= limit]
+        t0 = time.monotonic()
+        if big:
+            res = _lay.pack_batch([jobs[k][0].items for k in big], _lay.CONSTRAINED)
+            wall = time.monotonic() - t0
+            for k, r in zip(big, res):
+                p = jobs[k][0]
+                out[k] = lay.MemoryLayout(offsets=r.offsets, capacity=r.capacity,
+                                          activation_block=_lay._act_block(p.items), optimal=False,
+                                          stats=lay.LayoutStats(len(p.items), wall))
+        if small:
+            for p in (jobs[k][0] for k in small):
+                if p.time_budget <= 0:
+                    raise gr.ConfigError("time budget must be positive")
+            res = _lay.exact_layout_batch([jobs[k][0] for k in small])
+            for k, r in zip(small, res):
+                # incumbent above bound: the reference's branch-and-bound decides
+                out[k] = to_layout(r) if r is not None else ref_exact_layout(jobs[k][0])
+        return out
+
+    def pool_map(fn, jobs, workers):
+        jobs = list(jobs)
+        if fn is orig_solve_window:
+            return solve_windows(jobs)
+        if fn is orig_solve_layout:
+            return solve_layouts(jobs)
+        return orig_pool_map(fn, jobs, workers)
+
+    T = functools.partial(_translate, mp)
+    patches = {
+        (pl, "peak_memory"): T(_ev.peak_memory),
+        (pl, "tensor_lifetimes"): T(_ev.tensor_lifetimes),
+        (pl, "live_bytes_by_timestep"): T(_ev.live_bytes_by_timestep),
+        (pl, "_pool_map"): pool_map,
+        (pl, "repair_conflicts"): T(_lay.repair_conflicts),
+        (pl, "validate_layout"): T(_lay.validate_layout),
+        (lay, "layout_violations"): T(_lay.layout_violations),
+        (sim, "layout_violations"): T(_lay.layout_violations),
+        (sim, "peak_memory"): T(_ev.peak_memory),
+    }
+    saved = {}
+    for (mod, name), fn in patches.items():
+        saved[(mod, name)] = getattr(mod, name)
+        setattr(mod, name, fn)
+    _State.installed = (mp, saved)
+    return mp
+
+
+def uninstall() -> None:
+    if _State.installed is None:
+        return
+    _, saved = _State.installed
+    for (mod, name), fn in saved.items():
+        setattr(mod, name, fn)
+    _State.installed = None
+
+
+def plan(g, cfg=None):
+    """The reference's ``plan(g, cfg)`` (planner.py:180) with the B200 hot path
+    installed; returns the reference's ExecutionPlan."""
+    mp = install()
+    return mp.planner.plan(g, cfg)

@@ -1,0 +1,120 @@
+"""K3 (batched long-lived-first packer) against the reference's golden layout
+vectors (tests/golden/layouts.json, produced by the reference itself) and the
+oracle restatement; offsets and capacities bit-exact."""
+
+from __future__ import annotations
+
+import random
+
+import pytest
+
+from conftest import golden
+from oracle import memplan_oracle as O
+from paper_2310_19295_b200.layout import (COMPONENTS, CONSTRAINED, PLAIN, LayoutItem, LayoutProblem,
+                                          SearchRequired, constrained_llfb_layout, exact_layout,
+                                          exact_layout_batch, llfb_layout, pack_batch)
+
+pytestmark = pytest.mark.gpu
+MB = 1 << 20
+
+
+def _items(rows):
+    return tuple(LayoutItem(*r) for r in rows)
+
+
+def _offs(d):
+    return {int(k): v for k, v in d.items()}
+
+
+def test_spec_llfb_example():
+    # x(8,[0,10]), y(4,[0,3]), z(4,[4,10]) -> x@0, y@8, z@8, cap 12
+    spec = golden("layouts")["spec"][0]
+    m = llfb_layout(LayoutProblem(items=_items(spec["items"])))
+    assert m.offsets == _offs(spec["offsets"]) and m.capacity == spec["capacity"] == 12
+    assert not m.optimal
+
+
+def test_llfb_and_constrained_golden():
+    cases = golden("layouts")["llfb"]
+    for c in cases:
+        p = LayoutProblem(items=_items(c["items"]), activations_at_bottom=True)
+        a = llfb_layout(p)
+        b = constrained_llfb_layout(p)
+        assert (a.offsets, a.capacity) == (_offs(c["llfb"]["offsets"]), c["llfb"]["capacity"])
+        assert (b.offsets, b.capacity) == (_offs(c["constrained"]["offsets"]), c["constrained"]["capacity"])
+        assert a.activation_block == sum(i.size for i in p.items if i.is_activation)
+    # the whole corpus as ONE batched launch per mode gives the same answers
+    plain = pack_batch([_items(c["items"]) for c in cases], PLAIN)
+    cons = pack_batch([_items(c["items"]) for c in cases], CONSTRAINED)
+    for c, a, b in zip(cases, plain, cons):
+        assert a.offsets == _offs(c["llfb"]["offsets"]) and a.capacity == c["llfb"]["capacity"]
+        assert b.offsets == _offs(c["constrained"]["offsets"]) and b.capacity == c["constrained"]["capacity"]
+
+
+def test_exact_golden_decided_without_search():
+    """Every golden exact_layout case the reference closed at 0 nodes is decided
+    by K3 alone (same offsets and capacity); the others report the search."""
+    cases = golden("layouts")["exact"]
+    probs = [LayoutProblem(items=_items(c["items"]), activations_at_bottom=True, node_cap=200_000)
+             for c in cases]
+    res = exact_layout_batch(probs)
+    for c, p, r in zip(cases, probs, res):
+        if c["nodes"] == 0:
+            assert r is not None, c
+            assert r.offsets == _offs(c["offsets"]) and r.capacity == c["capacity"] and r.optimal
+        else:
+            assert r is None, c
+            with pytest.raises(SearchRequired):
+                exact_layout(p)
+            assert exact_layout(p, search=lambda q: "searched") == "searched"
+
+
+def test_exact_spec_examples():
+    # disjoint 16 MB / 20 MB -> both @0, cap 20 MB; a 3-clique stacks
+    m = exact_layout(LayoutProblem(items=(LayoutItem(0, 16 * MB, 0, 1), LayoutItem(1, 20 * MB, 2, 3))))
+    assert m.offsets == {0: 0, 1: 0} and m.capacity == 20 * MB and m.optimal
+    m = exact_layout(LayoutProblem(items=(LayoutItem(0, 4, 0, 5), LayoutItem(1, 2, 1, 5), LayoutItem(2, 1, 2, 5))))
+    assert m.capacity == 7
+    assert exact_layout(LayoutProblem(items=())).capacity == 0
+
+
+def _rand_rows(rng, n, horizon, act_p):
+    rows = []
+    for t in rng.sample(range(4 * n), n):
+        s = rng.randint(0, horizon - 1)
+        e = min(horizon - 1, s + rng.randint(0, max(1, horizon // 3)))
+        rows.append((t, rng.choice([0, 1, 3, 8, 64, 100]) * rng.choice([1, MB]), s, e, rng.random() < act_p))
+    return rows
+
+
+@pytest.mark.parametrize("n", [1, 2, 31, 255, 256, 257, 1000, 3000])
+def test_random_vs_oracle(n):
+    rng = random.Random(1000 + n)
+    rows = _rand_rows(rng, n, max(4, n // 3), 0.3)
+    items = _items(rows)
+    a, b = pack_batch([items], PLAIN)[0], pack_batch([items], CONSTRAINED)[0]
+    wa = O.llfb_layout(rows)
+    wb = O.constrained_llfb_layout(rows)
+    assert (a.offsets, a.capacity) == wa
+    assert (b.offsets, b.capacity) == wb
+
+
+def test_large_problem_global_scratch():
+    """> shared-memory working set: the CTA works out of global scratch."""
+    rng = random.Random(7)
+    rows = _rand_rows(rng, 6000, 2000, 0.2)
+    items = _items(rows)
+    b = pack_batch([items], CONSTRAINED)[0]
+    assert (b.offsets, b.capacity) == O.constrained_llfb_layout(rows)
+
+
+def test_components_vs_oracle():
+    rng = random.Random(3)
+    probs = []
+    for k in range(200):
+        probs.append(_rand_rows(rng, rng.randint(1, 24), rng.randint(3, 30), 0.3))
+    res = pack_batch([_items(r) for r in probs], COMPONENTS)
+    for rows, r in zip(probs, res):
+        offs, cap, met, comps = O.component_incumbents(rows)
+        assert r.offsets == offs and r.capacity == cap and r.bound_met == met
+        assert r.comp_cap == {root: c[1] for root, c in comps.items()}

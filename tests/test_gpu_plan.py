@@ -1,0 +1,64 @@
+"""End-to-end drop-in: the reference's own ``plan(g, cfg)`` with the B200 hot
+path installed (memplan_plugin) must emit byte-identical plan documents
+(planner.py:398-399) -- against the golden plans the reference produced in the
+build container, and against the unpatched reference run live on the same box
+(baseline/_ref) for the BASELINE config graphs."""
+
+from __future__ import annotations
+
+import pytest
+
+from conftest import golden
+from paper_2310_19295_b200 import graphgen as gg
+from paper_2310_19295_b200 import memplan_plugin as plug
+from paper_2310_19295_b200.evaluator import launch_count
+
+pytestmark = pytest.mark.gpu
+
+try:
+    mp = plug.load_memplan()
+except ImportError:  # pragma: no cover - baseline/_ref missing
+    mp = None
+needs_ref = pytest.mark.skipif(mp is None, reason="reference memplan not installed (baseline/_ref)")
+
+
+@needs_ref
+@pytest.mark.parametrize("name", sorted(golden("plans")))
+def test_golden_plan_bytes(name):
+    c = golden("plans")[name]
+    g = mp.graph.load_graph(c["doc"])
+    plug.install(mp)
+    try:
+        before = launch_count()
+        got = mp.planner.plan_doc_bytes(mp.planner.plan(g)).decode()
+        assert launch_count() > before          # the GPU path really ran
+    finally:
+        plug.uninstall()
+    assert got == c["plan"]
+
+
+@needs_ref
+@pytest.mark.parametrize("name", ["layered", "gpt2-small"])
+def test_config_plan_matches_live_reference(name):
+    g = mp.graph.load_graph(gg.config_doc(name))
+    want = mp.planner.plan_doc_bytes(mp.planner.plan(g))
+    plug.install(mp)
+    try:
+        got = mp.planner.plan_doc_bytes(mp.planner.plan(g))
+    finally:
+        plug.uninstall()
+    assert got == want
+
+
+@needs_ref
+def test_replay_and_compare_through_plugin():
+    c = golden("plans")["diamond"]
+    g = mp.graph.load_graph(c["doc"])
+    plug.install(mp)
+    try:
+        p = mp.planner.plan(g)
+        assert mp.simulator.replay_static(g, p.schedule, p.layout) == (94371840, [])
+        rows = mp.planner.compare_baselines(g)
+        assert rows
+    finally:
+        plug.uninstall()

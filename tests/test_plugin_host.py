@@ -1,0 +1,75 @@
+"""Host-side drop-in plumbing (no GPU): the plugin rebinds exactly the
+reference's hot-path module globals and restores them."""
+
+from __future__ import annotations
+
+import pytest
+
+from paper_2310_19295_b200 import memplan_plugin as plug
+
+try:
+    mp = plug.load_memplan()
+except ImportError:  # pragma: no cover
+    mp = None
+
+
+@pytest.mark.skipif(mp is None, reason="reference memplan not importable")
+def test_install_uninstall_roundtrip():
+    names = [(mp.planner, n) for n in ("peak_memory", "tensor_lifetimes", "live_bytes_by_timestep",
+                                       "_pool_map", "repair_conflicts", "validate_layout")]
+    names += [(mp.layout, "layout_violations"), (mp.simulator, "layout_violations"),
+              (mp.simulator, "peak_memory")]
+    before = {k: getattr(*k) for k in names}
+    plug.install(mp)
+    try:
+        for k in names:
+            assert getattr(*k) is not before[k], k
+        plug.install(mp)  # idempotent
+    finally:
+        plug.uninstall()
+    for k in names:
+        assert getattr(*k) is before[k], k
+
+
+@pytest.mark.skipif(mp is None, reason="reference memplan not importable")
+def test_errors_translate_to_reference_classes():
+    from paper_2310_19295_b200.graph import ScheduleError
+    def boom():
+        raise ScheduleError("schedule must contain every op exactly once")
+    w = plug._translate(mp, boom)
+    with pytest.raises(mp.graph.ScheduleError, match="exactly once"):
+        w()
+
+
+@pytest.mark.skipif(mp is None, reason="reference memplan not importable")
+def test_repair_mover_placement_matches_reference(monkeypatch):
+    """repair_conflicts' host mover placement (the part that is not K2) against
+    the reference, with K2's pair detection stood in by the oracle's pair
+    predicate so this runs without a GPU."""
+    import random
+
+    from oracle import memplan_oracle as O
+    from paper_2310_19295_b200 import layout as L
+
+    def cpu_pairs(items, offsets):
+        rows = [(i.tensor, i.size, i.start, i.end, i.is_activation) for i in items]
+        return [(a, b) for a in range(len(rows)) for b in range(a + 1, len(rows))
+                if O.overlaps(rows[a], rows[b]) and offsets[rows[a][0]] < offsets[rows[b][0]] + rows[b][1]
+                and offsets[rows[b][0]] < offsets[rows[a][0]] + rows[a][1]]
+
+    monkeypatch.setattr(L, "conflict_pairs", cpu_pairs)
+    rng = random.Random(11)
+    for trial in range(150):
+        n = rng.randint(1, 40)
+        items = []
+        for t in rng.sample(range(100), n):
+            s = rng.randint(0, 15)
+            items.append(mp.layout.LayoutItem(t, rng.choice([0, 1, 2, 4, 8, 16]), s,
+                                              s + rng.randint(0, 6), rng.random() < 0.3))
+        offs = {i.tensor: rng.choice([0, 1, 2, 4, 8, 12, 16, 24]) for i in items}
+        cap = max(offs[i.tensor] + i.size for i in items) + rng.choice([0, 0, 5])
+        m = mp.layout.MemoryLayout(offsets=offs, capacity=cap)
+        p = mp.layout.LayoutProblem(items=tuple(items))
+        want = mp.layout.repair_conflicts(m, p)
+        got = L.repair_conflicts(m, p)
+        assert got == want
