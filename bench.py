@@ -264,8 +264,11 @@ def main() -> None:
     best_host = [int(x) for x in best.cpu().tolist()]
 
     # roofline of K1: algorithmic bytes per launch / average K1 duration
-    meta_bytes = (2 * n * (2 if not info["wide_index"] else 4) + 16 * info["n_values"]
-                  + 4 * info["n_check_edges"] + 8 * info["n_multi"] + 2 * info["n_multi_cons"])
+    if info["k1_variant"] == 2:   # opv 8n + mref 4n + packed edges + partner words + sizes
+        meta_bytes = 12 * n + 4 * info["n_check_edges"] + 8 * info["n_multi_cons"] + 8 * info["n_multi"]
+    else:
+        meta_bytes = (2 * n * (2 if not info["wide_index"] else 4) + 16 * info["n_values"]
+                      + 4 * info["n_check_edges"] + 8 * info["n_multi"] + 2 * info["n_multi_cons"])
     alg_bytes = B * (4 * n + 16) + meta_bytes
     k1_avg = sum(k1_ms) / K
     peaks = measured_peaks()
@@ -338,7 +341,8 @@ def main() -> None:
                        "generation_ms": gen_ms},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
-                         "kernel": "k1_eval_orders", "k1_ms": k1_avg,
+                         "kernel": "k1v2_eval_orders" if info["k1_variant"] == 2 else "k1_eval_orders",
+                         "k1_ms": k1_avg,
                          "alg_bytes_per_launch": alg_bytes,
                          "alg_bytes_formula": "B*(4n+16) + graph metadata",
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst)" if "_fallback" not in peaks

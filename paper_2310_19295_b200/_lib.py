@@ -90,7 +90,7 @@ class RmGraphInfo(C.Structure):
                 ("n_pred_edges", C.c_int64), ("n_check_edges", C.c_int64),
                 ("n_multi", C.c_int64), ("n_multi_cons", C.c_int64), ("n_slots", C.c_int64),
                 ("n_values", C.c_int64), ("reduced", C.c_int32), ("wide_index", C.c_int32),
-                ("total_bytes", C.c_int64)]
+                ("total_bytes", C.c_int64), ("k1_variant", C.c_int32), ("unit_shift", C.c_int32)]
 
 
 class RmScheduleResult(C.Structure):
@@ -126,6 +126,7 @@ SIGNATURES = {
     "rm_device_count": (C.c_int, [C.POINTER(C.c_int)]),
     "rm_launch_count": (C.c_int64, []),
     "rm_set_timing": (C.c_int, [C.c_int]),
+    "rm_set_k1_variant": (C.c_int, [C.c_int]),
     "rm_last_kernel_ms": (C.c_double, []),
 }
 

@@ -241,6 +241,228 @@ __global__ void __launch_bounds__(1024, 1) k1_eval_orders(const K1Args a) {
   }
 }
 
+// ------------------------------------------------------------- K1 v2
+// Unit-packed, interleaved evaluator (the default when the graph qualifies,
+// see K1V2Meta).  One persistent CTA per SM holds the graph metadata in
+// shared memory; G groups of NT threads each evaluate one candidate at a time.
+// Candidate rows are near-topological, so ops at consecutive positions have
+// nearby ids: every per-op gather is done with consecutive positions on
+// consecutive lanes (position k = t + j*NT), which keeps the shared-memory
+// gathers close to conflict-free.
+//   P1  pos[o_k] = k (u16) from the row held in registers; range check
+//   P2  checked edges pos[u] < pos[v]; per position: readback pos[o_k] == k
+//       (permutation), out/fs units of o_k, multi-consumer frees decided
+//       in place (o_k frees tensor m iff every other maximal consumer of m
+//       sits earlier), xs[k] = (out_k, free_k) packed int32 pair; then the
+//       NEXT candidate's row is loaded into registers (hidden behind P3)
+//   P3  blocked scan over xs (padded, LDS.128): live[k] = sum_{j<k}(out-free)
+//       + out_k, running max / first argmax, group scan of chunk totals
+struct K1V2Args {
+  const int32_t* orders;
+  int64_t B;
+  int n, NT, G, C3, C3L;  // C3 = positions per thread in P3 (power of two), C3L = log2
+  int shift;
+  const int2* opv;
+  const uint32_t* mref;
+  const uint32_t* edges;
+  int64_t n_edges;
+  const uint32_t* mw;
+  int64_t n_words;
+  const long long* msz;
+  int n_msz;
+  int64_t* peak;
+  int32_t* argmax;
+  uint8_t* valid;
+  size_t off_mref, off_edges, off_mw, off_msz, off_groups, group_bytes, off_xs, off_red;
+  int xs_stride;  // int64 words per P3 chunk (C3 + pad)
+};
+
+template <int MAXC>
+__global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = a.n;
+  // ---- stage the graph metadata once per CTA
+  {
+    const uint4* src;
+    uint4* dst;
+    auto cp16 = [&](const void* g, size_t off, size_t bytes) {
+      src = static_cast<const uint4*>(g);
+      dst = reinterpret_cast<uint4*>(smem + off);
+      for (size_t i = threadIdx.x; i < bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+    };
+    cp16(a.opv, 0, align16(8 * size_t(n)));
+    cp16(a.mref, a.off_mref, align16(4 * size_t(n)));
+    cp16(a.edges, a.off_edges, align16(4 * size_t(a.n_edges)));
+    cp16(a.mw, a.off_mw, align16(4 * size_t(a.n_words)));
+    cp16(a.msz, a.off_msz, align16(8 * size_t(a.n_msz)));
+  }
+  __syncthreads();
+  const int2* opv = reinterpret_cast<const int2*>(smem);
+  const uint32_t* mref = reinterpret_cast<const uint32_t*>(smem + a.off_mref);
+  const uint32_t* edges = reinterpret_cast<const uint32_t*>(smem + a.off_edges);
+  const uint32_t* mw = reinterpret_cast<const uint32_t*>(smem + a.off_mw);
+  const long long* msz = reinterpret_cast<const long long*>(smem + a.off_msz);
+
+  const int NT = a.NT;
+  const int gid = threadIdx.x / NT;
+  const int tid = threadIdx.x - gid * NT;
+  if (gid >= a.G) return;
+  const int bar_id = 1 + gid;
+  unsigned char* gbase = smem + a.off_groups + size_t(gid) * a.group_bytes;
+  uint16_t* pos = reinterpret_cast<uint16_t*>(gbase);
+  long long* xs = reinterpret_cast<long long*>(gbase + a.off_xs);
+  long long* red_v = reinterpret_cast<long long*>(gbase + a.off_red);  // [32]
+  int* red_i = reinterpret_cast<int*>(red_v + 32);                      // [32]
+  const int lane = tid & 31, warp = tid >> 5, nwarps = NT >> 5;
+  const int64_t cstride = int64_t(gridDim.x) * a.G;
+
+  int32_t v[MAXC];
+  int64_t c = int64_t(blockIdx.x) * a.G + gid;
+  if (c < a.B) {
+    const int32_t* row = a.orders + c * int64_t(n);
+#pragma unroll
+    for (int j = 0; j < MAXC; ++j) {
+      const int k = tid + j * NT;
+      v[j] = k < n ? __ldcs(row + k) : 0;
+    }
+  }
+  for (; c < a.B; c += cstride) {
+    int bad = 0;
+    // ---- P1: scatter positions
+#pragma unroll
+    for (int j = 0; j < MAXC; ++j) {
+      const int k = tid + j * NT;
+      if (k < n) {
+        int o = v[j];
+        if ((unsigned)o >= (unsigned)n) {
+          bad = 1;
+          o = 0;
+          v[j] = 0;
+        }
+        pos[o] = (uint16_t)k;
+      }
+    }
+    gbar(bar_id, NT);
+    // ---- P2: edges, per-position values, multi-consumer frees
+    for (int64_t e = tid; e < a.n_edges; e += NT) {
+      const uint32_t w = edges[e];
+      bad |= pos[w & 0xffffu] >= pos[w >> 16];
+    }
+#pragma unroll
+    for (int j = 0; j < MAXC; ++j) {
+      const int k = tid + j * NT;
+      if (k < n) {
+        const int o = v[j];
+        bad |= pos[o] != k;
+        const int2 ov = opv[o];
+        long long fr = ov.y;
+        const uint32_t r = mref[o];
+        if (r) {
+          const uint32_t* wp = mw + (r >> 8);
+          const int cnt = r & 0xffu;
+          bool all = true;
+          for (int q = 0; q < cnt; ++q) {
+            const uint32_t w = wp[q];
+            all &= (int)pos[w & 0xffffu] < k;
+            if (!(w >> 31)) {  // end of this tensor's partner run
+              if (all) fr += msz[(w >> 16) & 0x7fffu];
+              all = true;
+            }
+          }
+        }
+        const int t3 = k >> a.C3L;
+        xs[t3 * a.xs_stride + (k & (a.C3 - 1))] =
+            (long long)(((unsigned long long)(unsigned)ov.x << 32) | (unsigned long long)(unsigned)fr);
+        // fr fits 32 bits: out/fs units are < 2^31 and a tensor is freed at
+        // one position only, so the frees at k are at most the bytes alive
+      }
+    }
+    // prefetch the next candidate's row; it lands while P3 runs
+    const int64_t cn = c + cstride;
+    if (cn < a.B) {
+      const int32_t* row = a.orders + cn * int64_t(n);
+#pragma unroll
+      for (int j = 0; j < MAXC; ++j) {
+        const int k = tid + j * NT;
+        v[j] = k < n ? __ldcs(row + k) : 0;
+      }
+    }
+    gbar(bar_id, NT);
+    // ---- P3: blocked scan over this thread's chunk of xs
+    const int k0 = tid << a.C3L;
+    const int k1 = min(n, k0 + a.C3);
+    const long long* xr = xs + size_t(tid) * a.xs_stride;
+    long long run = 0, best = LLONG_MIN;
+    int bestk = INT_MAX;
+    for (int k = k0; k < k1; k += 2) {
+      const longlong2 pr = *reinterpret_cast<const longlong2*>(xr + (k - k0));
+      {
+        const long long out_u = (long long)((unsigned long long)pr.x >> 32);
+        const long long fr_u = (long long)(unsigned)(pr.x & 0xffffffffll);
+        const long long live = run + out_u;
+        if (live > best) {
+          best = live;
+          bestk = k;
+        }
+        run = live - fr_u;
+      }
+      if (k + 1 < k1) {
+        const long long out_u = (long long)((unsigned long long)pr.y >> 32);
+        const long long fr_u = (long long)(unsigned)(pr.y & 0xffffffffll);
+        const long long live = run + out_u;
+        if (live > best) {
+          best = live;
+          bestk = k + 1;
+        }
+        run = live - fr_u;
+      }
+    }
+    long long incl = run;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const long long t = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += t;
+    }
+    if (lane == 31) red_v[warp] = incl;
+    bad = gbar_or(bar_id, NT, bad);
+    long long off = incl - run;
+    for (int w = 0; w < warp; ++w) off += red_v[w];
+    long long cand = bestk == INT_MAX ? LLONG_MIN : off + best;
+    int ck = bestk;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      const long long ov = __shfl_down_sync(0xffffffffu, cand, d);
+      const int oi = __shfl_down_sync(0xffffffffu, ck, d);
+      if (ov > cand || (ov == cand && oi < ck)) {
+        cand = ov;
+        ck = oi;
+      }
+    }
+    gbar(bar_id, NT);
+    if (lane == 0) {
+      red_v[warp] = cand;
+      red_i[warp] = ck;
+    }
+    gbar(bar_id, NT);
+    if (tid == 0) {
+      long long bv = red_v[0];
+      int bi = red_i[0];
+      for (int w = 1; w < nwarps; ++w)
+        if (red_v[w] > bv || (red_v[w] == bv && red_i[w] < bi)) {
+          bv = red_v[w];
+          bi = red_i[w];
+        }
+      if (n == 0) {
+        bv = 0;
+        bi = 0;
+      }
+      a.peak[c] = (int64_t)bv << a.shift;
+      a.argmax[c] = bi;
+      a.valid[c] = bad ? 0 : 1;
+    }
+  }
+}
+
 // ---------------------------------------------------------------- argmin
 // Lexicographic min of (peak, id) over valid rows; last-block-done finish.
 __global__ void k_argmin(const int64_t* __restrict__ peak, const uint8_t* __restrict__ valid,
@@ -492,11 +714,104 @@ static int launch_k1_idx(K1Args& a, int maxc, int grid, size_t smem, cudaStream_
   return fail(RM_ERR_CAPACITY, "K1: positions per thread exceed 64");
 }
 
+template <int MAXC>
+static int launch_k1v2_t(K1V2Args& a, int grid, size_t smem, cudaStream_t s) {
+  auto kern = k1v2_eval_orders<MAXC>;
+  RM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (t_timing) {
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, s);
+  }
+  kern<<<grid, a.NT * a.G, smem, s>>>(a);
+  RM_LAUNCH_CHECK("k1v2_eval_orders launch");
+  if (t_timing) {
+    cudaEventRecord(e1, s);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    t_last_ms = ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+  return RM_OK;
+}
+
+// K1 v2 geometry: NT threads per group (positions per thread <= 16 in P1/P2),
+// as many groups per CTA as shared memory allows (<= 15 named barriers).
+// Returns 1 when the graph does not fit the v2 layout (caller falls back).
+static int launch_k1v2(RmGraph* g, const int32_t* orders_dev, int64_t B, int64_t* peak,
+                       int32_t* argmax, uint8_t* valid, cudaStream_t s) {
+  const int n = g->n;
+  K1V2Args a{};
+  a.orders = orders_dev;
+  a.B = B;
+  a.n = n;
+  a.shift = g->k2v.shift;
+  a.opv = g->k2v.opv.as<int2>();
+  a.mref = g->k2v.mref.as<uint32_t>();
+  a.edges = g->k2v.edges.as<uint32_t>();
+  a.n_edges = g->info.n_check_edges;
+  a.mw = g->k2v.mw.as<uint32_t>();
+  a.n_words = g->k2v.n_words;
+  a.msz = g->k2v.msz.as<long long>();
+  a.n_msz = (int)g->k2v.n_msz;
+  a.peak = peak;
+  a.argmax = argmax;
+  a.valid = valid;
+  int NT = n <= 1024 ? 64 : n <= 2048 ? 128 : n <= 4096 ? 256 : n <= 8192 ? 512 : 1024;
+  const int C = std::max(1, (n + NT - 1) / NT);
+  const int maxc = C <= 4 ? 4 : C <= 8 ? 8 : 16;
+  if (C > 16) return 1;  // > 16384 ops: the generic evaluator
+  int C3L = 0;
+  while ((1 << C3L) < C) ++C3L;
+  if (C3L < 1) C3L = 1;  // pairs for the 16-byte reads
+  a.C3 = 1 << C3L;
+  a.C3L = C3L;
+  // (C3 + pad) / 2 odd keeps 8 consecutive threads' 16-byte reads on
+  // distinct bank groups
+  a.xs_stride = ((a.C3 / 2) % 2 == 1) ? a.C3 : a.C3 + 2;
+  a.NT = NT;
+  a.off_mref = align16(8 * size_t(n));
+  a.off_edges = align16(a.off_mref + 4 * size_t(n));
+  a.off_mw = align16(a.off_edges + 4 * size_t(a.n_edges));
+  a.off_msz = align16(a.off_mw + 4 * size_t(a.n_words));
+  a.off_groups = align16(a.off_msz + 8 * size_t(a.n_msz));
+  a.off_xs = align16(2 * size_t(n));
+  a.off_red = align16(a.off_xs + 8 * size_t(NT) * a.xs_stride);
+  a.group_bytes = align16(a.off_red + 32 * 8 + 32 * 4);
+  int dev = g->device;
+  int max_smem = 0;
+  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const size_t avail = max_smem > (int)a.off_groups ? size_t(max_smem) - a.off_groups : 0;
+  int G = (int)(avail / a.group_bytes);
+  G = std::min(G, 1024 / NT);
+  G = std::min(G, 15);
+  if (G < 1) return 1;
+  const int64_t sms = sm_count(dev);
+  if (int64_t(G) * sms > B) G = (int)std::max<int64_t>(1, (B + sms - 1) / sms);
+  a.G = G;
+  const size_t smem = a.off_groups + size_t(G) * a.group_bytes;
+  const int grid = (int)std::min<int64_t>(sms, (B + G - 1) / G);
+  switch (maxc) {
+    case 4: return launch_k1v2_t<4>(a, grid, smem, s);
+    case 8: return launch_k1v2_t<8>(a, grid, smem, s);
+    default: return launch_k1v2_t<16>(a, grid, smem, s);
+  }
+}
+
+static thread_local int t_force_variant = 0;  // 0 auto, 1 generic, 2 v2
+
 // Launch geometry: NT threads per candidate group, G groups per CTA, one
 // CTA per SM.  Shared memory bounds G; NT keeps ~8-16 positions per thread.
 int launch_k1(RmGraph* g, const int32_t* orders_dev, int64_t B, int64_t* peak, int32_t* argmax,
               uint8_t* valid, cudaStream_t s) {
   if (B <= 0) return RM_OK;
+  if (g->k2v.ok && t_force_variant != 1) {
+    const int rc = launch_k1v2(g, orders_dev, B, peak, argmax, valid, s);
+    if (rc != 1) return rc;
+  }
   const int n = g->n;
   const bool wide = g->info.wide_index != 0;
   const size_t isz = wide ? 4 : 2;
@@ -577,6 +892,11 @@ extern "C" {
 
 int rm_set_timing(int enable) {
   t_timing = enable != 0;
+  return RM_OK;
+}
+int rm_set_k1_variant(int variant) {
+  if (variant < 0 || variant > 2) return fail(RM_ERR_INVALID_ARG, "variant must be 0, 1 or 2");
+  t_force_variant = variant;
   return RM_OK;
 }
 double rm_last_kernel_ms(void) { return t_last_ms; }

@@ -9,6 +9,7 @@
 //   validate_schedule 375-398 permutation + preds-before
 #include <algorithm>
 #include <atomic>
+#include <climits>
 #include <cstring>
 #include <map>
 #include <unordered_map>
@@ -76,6 +77,78 @@ static bool descendants(const RmGraph& g, std::vector<uint64_t>& desc, size_t& w
     }
   }
   return true;
+}
+
+// K1 v2 metadata (see roam_internal.h).  Leaves g.k2v.ok = 0 when the graph
+// does not qualify; the generic evaluator then runs.
+static void build_k1v2_host(RmGraph& g, const std::vector<int64_t>& out,
+                            const std::vector<int64_t>& fs) {
+  const int n = g.n, T = g.T;
+  g.k2v.ok = 0;
+  if (n > 65535) return;
+  int shift = 62;
+  for (int t = 0; t < T; ++t) {
+    if (g.size[t] < 0) return;
+    if (g.size[t] > 0) shift = std::min(shift, __builtin_ctzll((unsigned long long)g.size[t]));
+  }
+  if (shift == 62) shift = 0;
+  const int64_t lim = INT32_MAX;
+  g.h2_opv.assign(2 * size_t(n), 0);
+  for (int v = 0; v < n; ++v) {
+    if ((out[v] >> shift) > lim || (fs[v] >> shift) > lim) return;
+    g.h2_opv[2 * v] = (int32_t)(out[v] >> shift);
+    g.h2_opv[2 * v + 1] = (int32_t)(fs[v] >> shift);
+  }
+  g.h2_edges.resize(g.h_edge_u.size());
+  for (size_t e = 0; e < g.h_edge_u.size(); ++e)
+    g.h2_edges[e] = (uint32_t)g.h_edge_u[e] | ((uint32_t)g.h_edge_v[e] << 16);
+  // size classes of multi-consumer tensors
+  std::map<int64_t, int32_t> scls;
+  g.h2_msz.clear();
+  std::vector<int32_t> mcls(g.h_msize.size());
+  for (size_t m = 0; m < g.h_msize.size(); ++m) {
+    auto it = scls.find(g.h_msize[m]);
+    if (it == scls.end()) {
+      it = scls.emplace(g.h_msize[m], (int32_t)g.h2_msz.size()).first;
+      g.h2_msz.push_back(g.h_msize[m] >> shift);
+    }
+    mcls[m] = it->second;
+  }
+  if (g.h2_msz.size() >= 32768) return;
+  // per closing op: its tensor groups (partners = the other maximal consumers)
+  std::vector<std::vector<uint32_t>> words(n);
+  for (size_t m = 0; m + 1 < g.h_mptr.size(); ++m) {
+    const int b0 = g.h_mptr[m], b1 = g.h_mptr[m + 1];
+    for (int q = b0; q < b1; ++q) {
+      const int v = g.h_mcons[q];
+      std::vector<uint32_t>& w = words[v];
+      int left = b1 - b0 - 1;
+      for (int r = b0; r < b1; ++r) {
+        if (r == q) continue;
+        --left;
+        w.push_back((uint32_t)g.h_mcons[r] | ((uint32_t)mcls[m] << 16) | (left ? 0x80000000u : 0u));
+      }
+    }
+  }
+  // the frees decided at one position are packed into 32 bits: bound them
+  for (int v = 0; v < n; ++v) {
+    int64_t mx = fs[v] >> shift;
+    for (uint32_t w : words[v])
+      if (!(w >> 31)) mx += g.h2_msz[(w >> 16) & 0x7fffu];
+    if (mx > (int64_t)UINT32_MAX) return;
+  }
+  g.h2_mref.assign(n, 0);
+  g.h2_mw.assign(1, 0);  // word 0 unused so that mref == 0 means "none"
+  for (int v = 0; v < n; ++v) {
+    if (words[v].empty()) continue;
+    if (words[v].size() > 255 || g.h2_mw.size() >= (1u << 24)) return;
+    g.h2_mref[v] = ((uint32_t)g.h2_mw.size() << 8) | (uint32_t)words[v].size();
+    g.h2_mw.insert(g.h2_mw.end(), words[v].begin(), words[v].end());
+  }
+  g.k2v.shift = shift;
+  g.k2v.n_words = (int64_t)g.h2_mw.size();
+  g.k2v.n_msz = (int64_t)g.h2_msz.size();
+  g.k2v.ok = 1;
 }
 
 static int build_k1_host(RmGraph& g, bool allow_reduce) {
@@ -157,7 +230,11 @@ static int build_k1_host(RmGraph& g, bool allow_reduce) {
   for (int32_t c : g.h_mcons)
     if (g.h_slot[c] < 0) g.h_slot[c] = K++;
 
+  build_k1v2_host(g, out, fs);
+
   RmGraphInfo& I = g.info;
+  I.k1_variant = g.k2v.ok ? 2 : 1;
+  I.unit_shift = g.k2v.shift;
   I.n_check_edges = (int64_t)g.h_edge_u.size();
   I.n_multi = (int64_t)g.h_msize.size();
   I.n_multi_cons = (int64_t)g.h_mcons.size();
@@ -325,6 +402,11 @@ int rm_graph_create(const RmGraphDesc* d, uint32_t flags, RmGraph** out) {
     cudaGetDevice(&dev);
     g->device = dev;
     cudaError_t e = g->info.wide_index ? upload_k1<int32_t>(*g) : upload_k1<uint16_t>(*g);
+    if (!e && g->k2v.ok) e = up(g->k2v.opv, g->h2_opv);
+    if (!e && g->k2v.ok) e = up(g->k2v.mref, g->h2_mref);
+    if (!e && g->k2v.ok) e = up(g->k2v.edges, g->h2_edges);
+    if (!e && g->k2v.ok) e = up(g->k2v.mw, g->h2_mw);
+    if (!e && g->k2v.ok) e = up(g->k2v.msz, g->h2_msz);
     if (!e) e = up(g->d_size, g->size);
     if (!e) e = up(g->d_producer, g->producer);
     if (!e) e = up(g->d_cons_ptr, g->cons_ptr);

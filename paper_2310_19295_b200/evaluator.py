@@ -307,6 +307,11 @@ def set_kernel_timing(enable: bool) -> None:
     lib().rm_set_timing(1 if enable else 0)
 
 
+def set_k1_variant(variant: int) -> None:
+    """0 auto, 1 generic evaluator, 2 unit-packed interleaved (v2); per thread."""
+    check(lib().rm_set_k1_variant(int(variant)), "rm_set_k1_variant")
+
+
 def last_kernel_ms() -> float:
     return float(lib().rm_last_kernel_ms())
 

@@ -136,3 +136,55 @@ def test_reference_unit_answers_through_gpu():
     assert peak_memory(fx["empty"], sequential_schedule(fx["empty"], ())) == (0, 0)
     with pytest.raises(ScheduleError):
         sequential_schedule(d, (3, 0, 1, 2))
+
+
+@pytest.mark.parametrize("variant", [1, 2])
+@pytest.mark.parametrize("name", ["layered", "gpt2-small", "bert-large", "gpt2-xl"])
+def test_both_k1_variants_vs_c_oracle(name, variant):
+    """The unit-packed interleaved evaluator (v2, default) and the generic one
+    (v1, the fallback for graphs v2 cannot pack) agree with the oracle,
+    including on corrupted rows (invalid -> valid=False)."""
+    from paper_2310_19295_b200.evaluator import device_graph, set_k1_variant
+    g = load_graph(gg.config_doc(name))
+    assert device_graph(g).info()["k1_variant"] == 2
+    B = 1500
+    host = generate_orders(g, 7, 0, B).cpu().numpy()
+    rng = np.random.default_rng(0)
+    n = len(g.ops)
+    for r in range(0, B, 50):                   # swaps: mostly invalid
+        i, j = rng.integers(0, n, 2)
+        host[r, [i, j]] = host[r, [j, i]]
+    for r in range(1, B, 97):                   # duplicates
+        host[r, rng.integers(0, n)] = host[r, rng.integers(0, n)]
+    for r in range(2, B, 131):                  # out of range
+        host[r, rng.integers(0, n)] = n + 3
+    want = coracle.eval_orders(coracle.CGraph(g), host)
+    set_k1_variant(variant)
+    try:
+        got = evaluate_orders(g, host)
+    finally:
+        set_k1_variant(0)
+    assert np.array_equal(got[2], want[2])
+    v = want[2]
+    assert np.array_equal(got[0][v], want[0][v]) and np.array_equal(got[1][v], want[1][v])
+
+
+def test_unit_shift_and_v2_eligibility():
+    from paper_2310_19295_b200.evaluator import device_graph
+    MB = 1 << 20
+    info = device_graph(load_graph(gg.config_doc("layered"))).info()
+    assert info["k1_variant"] == 2 and info["unit_shift"] >= 20   # MB-rounded sizes
+    # an odd byte count forces unit 1; a 2^33-byte output forces the generic path
+    doc = {"ops": [{"id": 0, "name": "a", "kind": "forward", "inputs": [], "outputs": [0]},
+                   {"id": 1, "name": "b", "kind": "forward", "inputs": [0], "outputs": [1]}],
+           "tensors": [{"id": 0, "size_bytes": 3}, {"id": 1, "size_bytes": 2**33 + 1}]}
+    g = load_graph(doc)
+    assert device_graph(g).info()["k1_variant"] == 1
+    peak, arg, val = evaluate_orders(g, np.array([[0, 1]]))
+    assert bool(val[0]) and (int(peak[0]), int(arg[0])) == O.peak_memory(g, (0, 1))
+    doc["tensors"][1]["size_bytes"] = 5 * MB + 1
+    g = load_graph(doc)
+    assert device_graph(g).info()["k1_variant"] == 2
+    peak, arg, val = evaluate_orders(g, np.array([[0, 1], [1, 0]]))
+    assert val.tolist() == [True, False]
+    assert (int(peak[0]), int(arg[0])) == O.peak_memory(g, (0, 1))
