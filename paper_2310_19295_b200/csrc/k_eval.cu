@@ -260,14 +260,14 @@ __global__ void __launch_bounds__(1024, 1) k1_eval_orders(const K1Args a) {
 struct K1V2Args {
   const int32_t* orders;
   int64_t B;
-  int n, NT, G, C3, C3L;  // C3 = positions per thread in P3 (power of two), C3L = log2
+  int n, G, C3, C3L;  // C3 = positions per thread in P3 (power of two), C3L = log2
   int shift;
   const int2* opv;
-  const uint32_t* mref;
+  const unsigned long long* mref;
   const uint32_t* edges;
-  int64_t n_edges;
+  int n_edges;
   const uint32_t* mw;
-  int64_t n_words;
+  int n_words;
   const long long* msz;
   int n_msz;
   int64_t* peak;
@@ -277,33 +277,32 @@ struct K1V2Args {
   int xs_stride;  // int64 words per P3 chunk (C3 + pad)
 };
 
-template <int MAXC>
+__device__ __forceinline__ unsigned pos_at(const uint16_t* pos, unsigned i) { return pos[i]; }
+
+template <int NT, int MAXC>
 __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int n = a.n;
   // ---- stage the graph metadata once per CTA
   {
-    const uint4* src;
-    uint4* dst;
     auto cp16 = [&](const void* g, size_t off, size_t bytes) {
-      src = static_cast<const uint4*>(g);
-      dst = reinterpret_cast<uint4*>(smem + off);
+      const uint4* src = static_cast<const uint4*>(g);
+      uint4* dst = reinterpret_cast<uint4*>(smem + off);
       for (size_t i = threadIdx.x; i < bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
     };
     cp16(a.opv, 0, align16(8 * size_t(n)));
-    cp16(a.mref, a.off_mref, align16(4 * size_t(n)));
+    cp16(a.mref, a.off_mref, align16(8 * size_t(n)));
     cp16(a.edges, a.off_edges, align16(4 * size_t(a.n_edges)));
     cp16(a.mw, a.off_mw, align16(4 * size_t(a.n_words)));
     cp16(a.msz, a.off_msz, align16(8 * size_t(a.n_msz)));
   }
   __syncthreads();
   const int2* opv = reinterpret_cast<const int2*>(smem);
-  const uint32_t* mref = reinterpret_cast<const uint32_t*>(smem + a.off_mref);
+  const unsigned long long* mref = reinterpret_cast<const unsigned long long*>(smem + a.off_mref);
   const uint32_t* edges = reinterpret_cast<const uint32_t*>(smem + a.off_edges);
   const uint32_t* mw = reinterpret_cast<const uint32_t*>(smem + a.off_mw);
   const long long* msz = reinterpret_cast<const long long*>(smem + a.off_msz);
 
-  const int NT = a.NT;
   const int gid = threadIdx.x / NT;
   const int tid = threadIdx.x - gid * NT;
   if (gid >= a.G) return;
@@ -313,8 +312,14 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
   long long* xs = reinterpret_cast<long long*>(gbase + a.off_xs);
   long long* red_v = reinterpret_cast<long long*>(gbase + a.off_red);  // [32]
   int* red_i = reinterpret_cast<int*>(red_v + 32);                      // [32]
-  const int lane = tid & 31, warp = tid >> 5, nwarps = NT >> 5;
+  const int lane = tid & 31, warp = tid >> 5;
+  constexpr int NWARPS = NT / 32;
   const int64_t cstride = int64_t(gridDim.x) * a.G;
+  // P2 writes position k = tid + j*NT to xs[(k >> C3L) * stride + (k & (C3-1))];
+  // NT is a multiple of C3, so that is xs_base + j * xs_step
+  long long* xs_w = xs + (tid >> a.C3L) * a.xs_stride + (tid & (a.C3 - 1));
+  const int xs_step = (NT >> a.C3L) * a.xs_stride;
+  const int n_edges = a.n_edges;
 
   int32_t v[MAXC];
   int64_t c = int64_t(blockIdx.x) * a.G + gid;
@@ -333,48 +338,61 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
     for (int j = 0; j < MAXC; ++j) {
       const int k = tid + j * NT;
       if (k < n) {
-        int o = v[j];
-        if ((unsigned)o >= (unsigned)n) {
-          bad = 1;
-          o = 0;
-          v[j] = 0;
-        }
-        pos[o] = (uint16_t)k;
+        const bool oor = (unsigned)v[j] >= (unsigned)n;
+        bad |= oor;
+        if (oor) v[j] = 0;
+        pos[v[j]] = (uint16_t)k;
       }
     }
     gbar(bar_id, NT);
-    // ---- P2: edges, per-position values, multi-consumer frees
-    for (int64_t e = tid; e < a.n_edges; e += NT) {
-      const uint32_t w = edges[e];
-      bad |= pos[w & 0xffffu] >= pos[w >> 16];
+    // ---- P2: checked edges
+    int e = tid;
+    for (; e + NT < n_edges; e += 2 * NT) {
+      const uint32_t w0 = edges[e], w1 = edges[e + NT];
+      bad |= (pos_at(pos, w0 & 0xffffu) >= pos_at(pos, w0 >> 16)) |
+             (pos_at(pos, w1 & 0xffffu) >= pos_at(pos, w1 >> 16));
     }
+    if (e < n_edges) {
+      const uint32_t w0 = edges[e];
+      bad |= pos_at(pos, w0 & 0xffffu) >= pos_at(pos, w0 >> 16);
+    }
+    // ---- P2: per position: readback, out/free units, multi-consumer frees
 #pragma unroll
     for (int j = 0; j < MAXC; ++j) {
       const int k = tid + j * NT;
       if (k < n) {
         const int o = v[j];
-        bad |= pos[o] != k;
+        bad |= (int)pos_at(pos, o) != k;
         const int2 ov = opv[o];
-        long long fr = ov.y;
-        const uint32_t r = mref[o];
+        unsigned fr = (unsigned)ov.y;
+        const unsigned long long r = mref[o];
         if (r) {
-          const uint32_t* wp = mw + (r >> 8);
-          const int cnt = r & 0xffu;
-          bool all = true;
-          for (int q = 0; q < cnt; ++q) {
-            const uint32_t w = wp[q];
-            all &= (int)pos[w & 0xffffu] < k;
-            if (!(w >> 31)) {  // end of this tensor's partner run
-              if (all) fr += msz[(w >> 16) & 0x7fffu];
-              all = true;
+          const unsigned mode = (unsigned)(r >> 62);
+          const unsigned pa = (unsigned)r & 0xffffu, pb = ((unsigned)r >> 16) & 0xffffu;
+          const bool oka = (int)pos_at(pos, pa) < k;
+          const bool okb = pb == 0xffffu || (int)pos_at(pos, pb) < k;
+          const unsigned ca = (unsigned)(r >> 32) & 0x7fffu, cb = (unsigned)(r >> 47) & 0x7fffu;
+          if (mode == 1) {
+            if (oka && okb) fr += (unsigned)msz[ca];
+          } else if (mode == 2) {
+            if (oka) fr += (unsigned)msz[ca];
+            if (okb) fr += (unsigned)msz[cb];
+          } else {
+            const uint32_t* wp = mw + (((unsigned)r) >> 8);
+            const int cnt = (unsigned)r & 0xffu;
+            bool all = true;
+            for (int q = 0; q < cnt; ++q) {
+              const uint32_t w = wp[q];
+              all &= (int)pos_at(pos, w & 0xffffu) < k;
+              if (!(w >> 31)) {  // end of this tensor's partner run
+                if (all) fr += (unsigned)msz[(w >> 16) & 0x7fffu];
+                all = true;
+              }
             }
           }
         }
-        const int t3 = k >> a.C3L;
-        xs[t3 * a.xs_stride + (k & (a.C3 - 1))] =
-            (long long)(((unsigned long long)(unsigned)ov.x << 32) | (unsigned long long)(unsigned)fr);
-        // fr fits 32 bits: out/fs units are < 2^31 and a tensor is freed at
-        // one position only, so the frees at k are at most the bytes alive
+        // the frees decided at one position fit 32 bits (checked on the host)
+        xs_w[j * xs_step] = (long long)(((unsigned long long)(unsigned)ov.x << 32) | fr);
       }
     }
     // prefetch the next candidate's row; it lands while P3 runs
@@ -390,33 +408,28 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
     gbar(bar_id, NT);
     // ---- P3: blocked scan over this thread's chunk of xs
     const int k0 = tid << a.C3L;
-    const int k1 = min(n, k0 + a.C3);
+    const int m = min(n - k0, a.C3);  // may be <= 0
     const long long* xr = xs + size_t(tid) * a.xs_stride;
     long long run = 0, best = LLONG_MIN;
-    int bestk = INT_MAX;
-    for (int k = k0; k < k1; k += 2) {
-      const longlong2 pr = *reinterpret_cast<const longlong2*>(xr + (k - k0));
-      {
-        const long long out_u = (long long)((unsigned long long)pr.x >> 32);
-        const long long fr_u = (long long)(unsigned)(pr.x & 0xffffffffll);
-        const long long live = run + out_u;
-        if (live > best) {
-          best = live;
-          bestk = k;
-        }
-        run = live - fr_u;
+    int bi = INT_MAX;
+    for (int i = 0; i < m; i += 2) {
+      const longlong2 pr = *reinterpret_cast<const longlong2*>(xr + i);
+      long long live = run + (long long)((unsigned long long)pr.x >> 32);
+      if (live > best) {
+        best = live;
+        bi = i;
       }
-      if (k + 1 < k1) {
-        const long long out_u = (long long)((unsigned long long)pr.y >> 32);
-        const long long fr_u = (long long)(unsigned)(pr.y & 0xffffffffll);
-        const long long live = run + out_u;
+      run = live - (long long)(unsigned)pr.x;
+      if (i + 1 < m) {
+        live = run + (long long)((unsigned long long)pr.y >> 32);
         if (live > best) {
           best = live;
-          bestk = k + 1;
+          bi = i + 1;
         }
-        run = live - fr_u;
+        run = live - (long long)(unsigned)pr.y;
       }
     }
+    const int bestk = bi == INT_MAX ? INT_MAX : k0 + bi;
     long long incl = run;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -426,7 +439,9 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
     if (lane == 31) red_v[warp] = incl;
     bad = gbar_or(bar_id, NT, bad);
     long long off = incl - run;
-    for (int w = 0; w < warp; ++w) off += red_v[w];
+#pragma unroll
+    for (int w = 0; w < NWARPS - 1; ++w)
+      if (w < warp) off += red_v[w];
     long long cand = bestk == INT_MAX ? LLONG_MIN : off + best;
     int ck = bestk;
 #pragma unroll
@@ -438,6 +453,14 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
         ck = oi;
       }
     }
+    if (NWARPS == 1) {
+      if (tid == 0) {
+        a.peak[c] = n == 0 ? 0 : (int64_t)cand << a.shift;
+        a.argmax[c] = n == 0 ? 0 : ck;
+        a.valid[c] = bad ? 0 : 1;
+      }
+      continue;
+    }
     gbar(bar_id, NT);
     if (lane == 0) {
       red_v[warp] = cand;
@@ -446,18 +469,19 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
     gbar(bar_id, NT);
     if (tid == 0) {
       long long bv = red_v[0];
-      int bi = red_i[0];
-      for (int w = 1; w < nwarps; ++w)
-        if (red_v[w] > bv || (red_v[w] == bv && red_i[w] < bi)) {
+      int bk = red_i[0];
+#pragma unroll
+      for (int w = 1; w < NWARPS; ++w)
+        if (red_v[w] > bv || (red_v[w] == bv && red_i[w] < bk)) {
           bv = red_v[w];
-          bi = red_i[w];
+          bk = red_i[w];
         }
       if (n == 0) {
         bv = 0;
-        bi = 0;
+        bk = 0;
       }
       a.peak[c] = (int64_t)bv << a.shift;
-      a.argmax[c] = bi;
+      a.argmax[c] = bk;
       a.valid[c] = bad ? 0 : 1;
     }
   }
@@ -714,9 +738,9 @@ static int launch_k1_idx(K1Args& a, int maxc, int grid, size_t smem, cudaStream_
   return fail(RM_ERR_CAPACITY, "K1: positions per thread exceed 64");
 }
 
-template <int MAXC>
+template <int NT, int MAXC>
 static int launch_k1v2_t(K1V2Args& a, int grid, size_t smem, cudaStream_t s) {
-  auto kern = k1v2_eval_orders<MAXC>;
+  auto kern = k1v2_eval_orders<NT, MAXC>;
   RM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (t_timing) {
@@ -724,7 +748,7 @@ static int launch_k1v2_t(K1V2Args& a, int grid, size_t smem, cudaStream_t s) {
     cudaEventCreate(&e1);
     cudaEventRecord(e0, s);
   }
-  kern<<<grid, a.NT * a.G, smem, s>>>(a);
+  kern<<<grid, NT * a.G, smem, s>>>(a);
   RM_LAUNCH_CHECK("k1v2_eval_orders launch");
   if (t_timing) {
     cudaEventRecord(e1, s);
@@ -738,7 +762,7 @@ static int launch_k1v2_t(K1V2Args& a, int grid, size_t smem, cudaStream_t s) {
   return RM_OK;
 }
 
-// K1 v2 geometry: NT threads per group (positions per thread <= 16 in P1/P2),
+// K1 v2 geometry: NT threads per group (<= 16 positions per thread in P1/P2),
 // as many groups per CTA as shared memory allows (<= 15 named barriers).
 // Returns 1 when the graph does not fit the v2 layout (caller falls back).
 static int launch_k1v2(RmGraph* g, const int32_t* orders_dev, int64_t B, int64_t* peak,
@@ -750,36 +774,33 @@ static int launch_k1v2(RmGraph* g, const int32_t* orders_dev, int64_t B, int64_t
   a.n = n;
   a.shift = g->k2v.shift;
   a.opv = g->k2v.opv.as<int2>();
-  a.mref = g->k2v.mref.as<uint32_t>();
+  a.mref = g->k2v.mref.as<unsigned long long>();
   a.edges = g->k2v.edges.as<uint32_t>();
-  a.n_edges = g->info.n_check_edges;
+  a.n_edges = (int)g->info.n_check_edges;
   a.mw = g->k2v.mw.as<uint32_t>();
-  a.n_words = g->k2v.n_words;
+  a.n_words = (int)g->k2v.n_words;
   a.msz = g->k2v.msz.as<long long>();
   a.n_msz = (int)g->k2v.n_msz;
   a.peak = peak;
   a.argmax = argmax;
   a.valid = valid;
-  int NT = n <= 1024 ? 64 : n <= 2048 ? 128 : n <= 4096 ? 256 : n <= 8192 ? 512 : 1024;
+  const int NT = n <= 1024 ? 64 : n <= 2048 ? 128 : n <= 4096 ? 256 : n <= 8192 ? 512 : 1024;
   const int C = std::max(1, (n + NT - 1) / NT);
-  const int maxc = C <= 4 ? 4 : C <= 8 ? 8 : 16;
   if (C > 16) return 1;  // > 16384 ops: the generic evaluator
-  int C3L = 0;
+  int C3L = 1;           // pairs for the 16-byte reads
   while ((1 << C3L) < C) ++C3L;
-  if (C3L < 1) C3L = 1;  // pairs for the 16-byte reads
   a.C3 = 1 << C3L;
   a.C3L = C3L;
   // (C3 + pad) / 2 odd keeps 8 consecutive threads' 16-byte reads on
   // distinct bank groups
   a.xs_stride = ((a.C3 / 2) % 2 == 1) ? a.C3 : a.C3 + 2;
-  a.NT = NT;
   a.off_mref = align16(8 * size_t(n));
-  a.off_edges = align16(a.off_mref + 4 * size_t(n));
+  a.off_edges = align16(a.off_mref + 8 * size_t(n));
   a.off_mw = align16(a.off_edges + 4 * size_t(a.n_edges));
   a.off_msz = align16(a.off_mw + 4 * size_t(a.n_words));
   a.off_groups = align16(a.off_msz + 8 * size_t(a.n_msz));
   a.off_xs = align16(2 * size_t(n));
-  a.off_red = align16(a.off_xs + 8 * size_t(NT) * a.xs_stride);
+  a.off_red = align16(a.off_xs + 8 * size_t((n + a.C3 - 1) / a.C3) * a.xs_stride);
   a.group_bytes = align16(a.off_red + 32 * 8 + 32 * 4);
   int dev = g->device;
   int max_smem = 0;
@@ -794,10 +815,14 @@ static int launch_k1v2(RmGraph* g, const int32_t* orders_dev, int64_t B, int64_t
   a.G = G;
   const size_t smem = a.off_groups + size_t(G) * a.group_bytes;
   const int grid = (int)std::min<int64_t>(sms, (B + G - 1) / G);
-  switch (maxc) {
-    case 4: return launch_k1v2_t<4>(a, grid, smem, s);
-    case 8: return launch_k1v2_t<8>(a, grid, smem, s);
-    default: return launch_k1v2_t<16>(a, grid, smem, s);
+  switch (NT) {
+    case 64: return C <= 4 ? launch_k1v2_t<64, 4>(a, grid, smem, s)
+                   : C <= 8 ? launch_k1v2_t<64, 8>(a, grid, smem, s)
+                            : launch_k1v2_t<64, 16>(a, grid, smem, s);
+    case 128: return launch_k1v2_t<128, 16>(a, grid, smem, s);
+    case 256: return launch_k1v2_t<256, 16>(a, grid, smem, s);
+    case 512: return launch_k1v2_t<512, 16>(a, grid, smem, s);
+    default: return launch_k1v2_t<1024, 16>(a, grid, smem, s);
   }
 }
 

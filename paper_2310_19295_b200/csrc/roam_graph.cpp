@@ -137,13 +137,31 @@ static void build_k1v2_host(RmGraph& g, const std::vector<int64_t>& out,
       if (!(w >> 31)) mx += g.h2_msz[(w >> 16) & 0x7fffu];
     if (mx > (int64_t)UINT32_MAX) return;
   }
+  // mref[v] (64 bits): mode in bits 62-63.
+  //   1: one tensor group, partners pA (bits 0-15) and pB (16-31, 0xffff =
+  //      none), size class bits 32-46
+  //   2: two single-partner groups: pA with class bits 32-46, pB with 47-61
+  //   3: generic list: bits 0-31 = (start << 8) | count over mw[]
   g.h2_mref.assign(n, 0);
-  g.h2_mw.assign(1, 0);  // word 0 unused so that mref == 0 means "none"
+  g.h2_mw.assign(1, 0);
   for (int v = 0; v < n; ++v) {
-    if (words[v].empty()) continue;
-    if (words[v].size() > 255 || g.h2_mw.size() >= (1u << 24)) return;
-    g.h2_mref[v] = ((uint32_t)g.h2_mw.size() << 8) | (uint32_t)words[v].size();
-    g.h2_mw.insert(g.h2_mw.end(), words[v].begin(), words[v].end());
+    const std::vector<uint32_t>& w = words[v];
+    if (w.empty()) continue;
+    auto part = [](uint32_t x) { return (uint64_t)(x & 0xffffu); };
+    auto cls = [](uint32_t x) { return (uint64_t)((x >> 16) & 0x7fffu); };
+    auto last = [](uint32_t x) { return !(x >> 31); };
+    if (w.size() == 1) {
+      g.h2_mref[v] = (1ull << 62) | part(w[0]) | (0xffffull << 16) | (cls(w[0]) << 32);
+    } else if (w.size() == 2 && !last(w[0])) {  // one group, two partners
+      g.h2_mref[v] = (1ull << 62) | part(w[0]) | (part(w[1]) << 16) | (cls(w[1]) << 32);
+    } else if (w.size() == 2) {                  // two single-partner groups
+      g.h2_mref[v] = (2ull << 62) | part(w[0]) | (part(w[1]) << 16) | (cls(w[0]) << 32) |
+                     (cls(w[1]) << 47);
+    } else {
+      if (w.size() > 255 || g.h2_mw.size() >= (1u << 24)) return;
+      g.h2_mref[v] = (3ull << 62) | ((uint64_t)g.h2_mw.size() << 8) | (uint64_t)w.size();
+      g.h2_mw.insert(g.h2_mw.end(), w.begin(), w.end());
+    }
   }
   g.k2v.shift = shift;
   g.k2v.n_words = (int64_t)g.h2_mw.size();

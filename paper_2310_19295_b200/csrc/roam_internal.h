@@ -86,10 +86,11 @@ struct K1Meta {
 // K1 v2 metadata (the default order evaluator when the graph qualifies:
 // n <= 65535, sizes >= 0, every per-op byte count < 2^31 units of 2^shift).
 //   opv[v]  = {out[v] >> shift, fs[v] >> shift}  (int2)
-//   mref[v] = (start << 8) | count over mw[] (0 = v closes no multi-consumer
-//             lifetime).  mw words: partner | sizecls << 16 | cont << 31; a
-//             tensor group is a run of words ending with cont = 0: v frees
-//             msz[sizecls] iff every partner sits earlier in the order.
+//   mref[v] = the multi-consumer lifetimes v may close (0 = none): inline
+//             for up to two partners (see build_k1v2_host), else a run of
+//             mw words: partner | sizecls << 16 | cont << 31; a tensor group
+//             ends with cont = 0 and v frees msz[sizecls] iff every partner
+//             sits earlier in the order.
 //   edges   = checked pred edges packed u | v << 16.
 struct K1V2Meta {
   int ok = 0;
@@ -119,7 +120,8 @@ struct RmGraph {
   roam::K1Meta k1;
   roam::K1V2Meta k2v;
   std::vector<int32_t> h2_opv;     // 2n
-  std::vector<uint32_t> h2_mref, h2_edges, h2_mw;
+  std::vector<uint64_t> h2_mref;
+  std::vector<uint32_t> h2_edges, h2_mw;
   std::vector<int64_t> h2_msz;
   roam::DevBuf d_size, d_producer, d_cons_ptr, d_cons_idx, d_in_ptr, d_in_idx, d_out_ptr,
       d_out_idx, d_pred_ptr, d_pred_idx, d_succ_ptr, d_succ_idx;
