@@ -36,10 +36,13 @@ DevBuf::~DevBuf() {
   if (p) cudaFree(p);
 }
 cudaError_t DevBuf::upload(const void* host, size_t nbytes) {
+  // padded to 16 bytes (zeroed) so kernels may stage it with 16-byte loads
   bytes = nbytes;
-  cudaError_t e = cudaMalloc(&p, nbytes ? nbytes : 16);
+  const size_t padded = (nbytes + 15) & ~size_t(15);
+  cudaError_t e = cudaMalloc(&p, padded ? padded : 16);
   if (e != cudaSuccess) return e;
-  if (nbytes) e = cudaMemcpy(p, host, nbytes, cudaMemcpyHostToDevice);
+  if (padded != nbytes || !nbytes) e = cudaMemset(p, 0, padded ? padded : 16);
+  if (e == cudaSuccess && nbytes) e = cudaMemcpy(p, host, nbytes, cudaMemcpyHostToDevice);
   return e;
 }
 
