@@ -368,15 +368,17 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
         const unsigned long long r = mref[o];
         if (r) {
           const unsigned mode = (unsigned)(r >> 62);
-          const unsigned pa = (unsigned)r & 0xffffu, pb = ((unsigned)r >> 16) & 0xffffu;
-          const bool oka = (int)pos_at(pos, pa) < k;
-          const bool okb = pb == 0xffffu || (int)pos_at(pos, pb) < k;
-          const unsigned ca = (unsigned)(r >> 32) & 0x7fffu, cb = (unsigned)(r >> 47) & 0x7fffu;
-          if (mode == 1) {
-            if (oka && okb) fr += (unsigned)msz[ca];
-          } else if (mode == 2) {
-            if (oka) fr += (unsigned)msz[ca];
-            if (okb) fr += (unsigned)msz[cb];
+          if (mode != 3) {  // inline: one group with <= 2 partners, or two single-partner groups
+            const unsigned pa = (unsigned)r & 0xffffu, pb = ((unsigned)r >> 16) & 0xffffu;
+            const bool oka = (int)pos_at(pos, pa) < k;
+            const bool okb = pb == 0xffffu || (int)pos_at(pos, pb) < k;
+            const unsigned ca = (unsigned)(r >> 32) & 0x7fffu, cb = (unsigned)(r >> 47) & 0x7fffu;
+            if (mode == 1) {
+              if (oka && okb) fr += (unsigned)msz[ca];
+            } else {
+              if (oka) fr += (unsigned)msz[ca];
+              if (okb) fr += (unsigned)msz[cb];
+            }
           } else {
             const uint32_t* wp = mw + (((unsigned)r) >> 8);
             const int cnt = (unsigned)r & 0xffu;
