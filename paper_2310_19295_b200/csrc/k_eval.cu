@@ -279,6 +279,26 @@ struct K1V2Args {
 
 __device__ __forceinline__ unsigned pos_at(const uint16_t* pos, unsigned i) { return pos[i]; }
 
+// Rare path of K1 v2 (an op closing several multi-consumer lifetimes):
+// out of line so the 16x-unrolled position loop stays small in the I-cache.
+__device__ __noinline__ unsigned k1v2_list_frees(const uint16_t* pos, const uint32_t* mw,
+                                                 const long long* msz, unsigned r, int k) {
+  const uint32_t* wp = mw + (r >> 8);
+  const int cnt = r & 0xffu;
+  unsigned fr = 0;
+  bool all = true;
+#pragma unroll 1
+  for (int q = 0; q < cnt; ++q) {
+    const uint32_t w = wp[q];
+    all &= (int)pos[w & 0xffffu] < k;
+    if (!(w >> 31)) {  // end of this tensor's partner run
+      if (all) fr += (unsigned)msz[(w >> 16) & 0x7fffu];
+      all = true;
+    }
+  }
+  return fr;
+}
+
 template <int NT, int MAXC>
 __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -290,8 +310,8 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
       uint4* dst = reinterpret_cast<uint4*>(smem + off);
       for (size_t i = threadIdx.x; i < bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
     };
-    cp16(a.opv, 0, align16(8 * size_t(n)));
-    cp16(a.mref, a.off_mref, align16(8 * size_t(n)));
+    cp16(a.opv, 0, align16(8 * size_t(n + 3)));
+    cp16(a.mref, a.off_mref, align16(8 * size_t(n + 3)));
     cp16(a.edges, a.off_edges, align16(4 * size_t(a.n_edges)));
     cp16(a.mw, a.off_mw, align16(4 * size_t(a.n_words)));
     cp16(a.msz, a.off_msz, align16(8 * size_t(a.n_msz)));
@@ -304,6 +324,7 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
   const long long* msz = reinterpret_cast<const long long*>(smem + a.off_msz);
 
   const int gid = threadIdx.x / NT;
+  const int D = n;  // padding op; D+1 / D+2 have pinned positions
   const int tid = threadIdx.x - gid * NT;
   if (gid >= a.G) return;
   const int bar_id = 1 + gid;
@@ -321,6 +342,10 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
   const int xs_step = (NT >> a.C3L) * a.xs_stride;
   const int n_edges = a.n_edges;
 
+  if (tid == 0) {
+    pos[D + 1] = 0xffffu;  // "never earlier"
+    pos[D + 2] = 0;        // "always earlier" (k >= 1)
+  }
   int32_t v[MAXC];
   int64_t c = int64_t(blockIdx.x) * a.G + gid;
   if (c < a.B) {
@@ -328,21 +353,19 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
 #pragma unroll
     for (int j = 0; j < MAXC; ++j) {
       const int k = tid + j * NT;
-      v[j] = k < n ? __ldcs(row + k) : 0;
+      v[j] = k < n ? __ldcs(row + k) : D;
     }
   }
   for (; c < a.B; c += cstride) {
     int bad = 0;
-    // ---- P1: scatter positions
+    // ---- P1: scatter positions (padding slots write the dummy D)
 #pragma unroll
     for (int j = 0; j < MAXC; ++j) {
       const int k = tid + j * NT;
-      if (k < n) {
-        const bool oor = (unsigned)v[j] >= (unsigned)n;
-        bad |= oor;
-        if (oor) v[j] = 0;
-        pos[v[j]] = (uint16_t)k;
-      }
+      const bool oor = (unsigned)v[j] > (unsigned)D || (v[j] == D && k < n);
+      bad |= oor;
+      v[j] = oor ? D : v[j];
+      pos[v[j]] = (uint16_t)k;
     }
     gbar(bar_id, NT);
     // ---- P2: checked edges
@@ -360,42 +383,21 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
 #pragma unroll
     for (int j = 0; j < MAXC; ++j) {
       const int k = tid + j * NT;
-      if (k < n) {
-        const int o = v[j];
-        bad |= (int)pos_at(pos, o) != k;
-        const int2 ov = opv[o];
-        unsigned fr = (unsigned)ov.y;
-        const unsigned long long r = mref[o];
-        if (r) {
-          const unsigned mode = (unsigned)(r >> 62);
-          if (mode != 3) {  // inline: one group with <= 2 partners, or two single-partner groups
-            const unsigned pa = (unsigned)r & 0xffffu, pb = ((unsigned)r >> 16) & 0xffffu;
-            const bool oka = (int)pos_at(pos, pa) < k;
-            const bool okb = pb == 0xffffu || (int)pos_at(pos, pb) < k;
-            const unsigned ca = (unsigned)(r >> 32) & 0x7fffu, cb = (unsigned)(r >> 47) & 0x7fffu;
-            if (mode == 1) {
-              if (oka && okb) fr += (unsigned)msz[ca];
-            } else {
-              if (oka) fr += (unsigned)msz[ca];
-              if (okb) fr += (unsigned)msz[cb];
-            }
-          } else {
-            const uint32_t* wp = mw + (((unsigned)r) >> 8);
-            const int cnt = (unsigned)r & 0xffu;
-            bool all = true;
-            for (int q = 0; q < cnt; ++q) {
-              const uint32_t w = wp[q];
-              all &= (int)pos_at(pos, w & 0xffffu) < k;
-              if (!(w >> 31)) {  // end of this tensor's partner run
-                if (all) fr += (unsigned)msz[(w >> 16) & 0x7fffu];
-                all = true;
-              }
-            }
-          }
-        }
-        // the frees decided at one position fit 32 bits (checked on the host)
-        xs_w[j * xs_step] = (long long)(((unsigned long long)(unsigned)ov.x << 32) | fr);
+      const int o = v[j];
+      bad |= ((int)pos_at(pos, o) != k) & (k < n);
+      const int2 ov = opv[o];
+      const unsigned long long r = mref[o];
+      unsigned fr = (unsigned)ov.y;
+      if (!(r >> 63)) {  // inline: one tensor group, <= 2 partners (branch-free)
+        const unsigned a1 = (unsigned)r & 0xffffu, a2 = ((unsigned)r >> 16) & 0xffffu;
+        const bool ok = ((int)pos_at(pos, a1) < k) & ((int)pos_at(pos, a2) < k);
+        const unsigned add = (unsigned)msz[(unsigned)(r >> 32) & 0x7fffu];
+        fr += ok ? add : 0u;
+      } else {
+        fr += k1v2_list_frees(pos, mw, msz, (unsigned)r, k);
       }
+      // the frees decided at one position fit 32 bits (checked on the host)
+      if (k < n) xs_w[j * xs_step] = (long long)(((unsigned long long)(unsigned)ov.x << 32) | fr);
     }
     // prefetch the next candidate's row; it lands while P3 runs
     const int64_t cn = c + cstride;
@@ -404,7 +406,7 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
 #pragma unroll
       for (int j = 0; j < MAXC; ++j) {
         const int k = tid + j * NT;
-        v[j] = k < n ? __ldcs(row + k) : 0;
+        v[j] = k < n ? __ldcs(row + k) : D;
       }
     }
     gbar(bar_id, NT);
@@ -796,12 +798,12 @@ static int launch_k1v2(RmGraph* g, const int32_t* orders_dev, int64_t B, int64_t
   // (C3 + pad) / 2 odd keeps 8 consecutive threads' 16-byte reads on
   // distinct bank groups
   a.xs_stride = ((a.C3 / 2) % 2 == 1) ? a.C3 : a.C3 + 2;
-  a.off_mref = align16(8 * size_t(n));
-  a.off_edges = align16(a.off_mref + 8 * size_t(n));
+  a.off_mref = align16(8 * size_t(n + 3));
+  a.off_edges = align16(a.off_mref + 8 * size_t(n + 3));
   a.off_mw = align16(a.off_edges + 4 * size_t(a.n_edges));
   a.off_msz = align16(a.off_mw + 4 * size_t(a.n_words));
   a.off_groups = align16(a.off_msz + 8 * size_t(a.n_msz));
-  a.off_xs = align16(2 * size_t(n));
+  a.off_xs = align16(2 * size_t(n + 3));
   a.off_red = align16(a.off_xs + 8 * size_t((n + a.C3 - 1) / a.C3) * a.xs_stride);
   a.group_bytes = align16(a.off_red + 32 * 8 + 32 * 4);
   int dev = g->device;

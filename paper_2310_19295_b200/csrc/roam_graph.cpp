@@ -88,7 +88,7 @@ static void build_k1v2_host(RmGraph& g, const std::vector<int64_t>& out,
                             const std::vector<int64_t>& fs) {
   const int n = g.n, T = g.T;
   g.k2v.ok = 0;
-  if (n > 65535) return;
+  if (n > 65532) return;  // ids and three dummy ops fit 16 bits
   int shift = 62;
   for (int t = 0; t < T; ++t) {
     if (g.size[t] < 0) return;
@@ -107,7 +107,7 @@ static void build_k1v2_host(RmGraph& g, const std::vector<int64_t>& out,
     g.h2_edges[e] = (uint32_t)g.h_edge_u[e] | ((uint32_t)g.h_edge_v[e] << 16);
   // size classes of multi-consumer tensors
   std::map<int64_t, int32_t> scls;
-  g.h2_msz.clear();
+  g.h2_msz.assign(1, 0);  // class 0 = "frees nothing"
   std::vector<int32_t> mcls(g.h_msize.size());
   for (size_t m = 0; m < g.h_msize.size(); ++m) {
     auto it = scls.find(g.h_msize[m]);
@@ -118,6 +118,8 @@ static void build_k1v2_host(RmGraph& g, const std::vector<int64_t>& out,
     mcls[m] = it->second;
   }
   if (g.h2_msz.size() >= 32768) return;
+  for (int64_t x : g.h2_msz)
+    if (x > (int64_t)UINT32_MAX) return;
   // per closing op: its tensor groups (partners = the other maximal consumers)
   std::vector<std::vector<uint32_t>> words(n);
   for (size_t m = 0; m + 1 < g.h_mptr.size(); ++m) {
@@ -140,32 +142,33 @@ static void build_k1v2_host(RmGraph& g, const std::vector<int64_t>& out,
       if (!(w >> 31)) mx += g.h2_msz[(w >> 16) & 0x7fffu];
     if (mx > (int64_t)UINT32_MAX) return;
   }
-  // mref[v] (64 bits): mode in bits 62-63.
-  //   1: one tensor group, partners pA (bits 0-15) and pB (16-31, 0xffff =
-  //      none), size class bits 32-46
-  //   2: two single-partner groups: pA with class bits 32-46, pB with 47-61
-  //   3: generic list: bits 0-31 = (start << 8) | count over mw[]
-  g.h2_mref.assign(n, 0);
+  // mref[v] (64 bits), for v < n plus three dummy ops D = n (row padding),
+  // D+1 (position pinned to 0xffff: never earlier) and D+2 (position pinned
+  // to 0: always earlier for k >= 1):
+  //   inline (bit 63 = 0): partners a1 (bits 0-15), a2 (16-31), size class
+  //     (32-46).  v frees msz[cls] iff pos[a1] < k and pos[a2] < k; unused
+  //     slots point at D+2, "no group" is a1 = D+1 with class 0.
+  //   list (bit 63 = 1): bits 0-31 = (start << 8) | count over mw[].
+  const uint64_t D = (uint64_t)n;
+  const uint64_t none = (D + 1) | ((D + 2) << 16);
+  g.h2_mref.assign(size_t(n) + 3, none);
   g.h2_mw.assign(1, 0);
   for (int v = 0; v < n; ++v) {
     const std::vector<uint32_t>& w = words[v];
     if (w.empty()) continue;
     auto part = [](uint32_t x) { return (uint64_t)(x & 0xffffu); };
     auto cls = [](uint32_t x) { return (uint64_t)((x >> 16) & 0x7fffu); };
-    auto last = [](uint32_t x) { return !(x >> 31); };
-    if (w.size() == 1) {
-      g.h2_mref[v] = (1ull << 62) | part(w[0]) | (0xffffull << 16) | (cls(w[0]) << 32);
-    } else if (w.size() == 2 && !last(w[0])) {  // one group, two partners
-      g.h2_mref[v] = (1ull << 62) | part(w[0]) | (part(w[1]) << 16) | (cls(w[1]) << 32);
-    } else if (w.size() == 2) {                  // two single-partner groups
-      g.h2_mref[v] = (2ull << 62) | part(w[0]) | (part(w[1]) << 16) | (cls(w[0]) << 32) |
-                     (cls(w[1]) << 47);
+    const bool one_group = w.size() == 1 || (w.size() == 2 && (w[0] >> 31));
+    if (one_group) {
+      const uint64_t a2 = w.size() == 2 ? part(w[1]) : D + 2;
+      g.h2_mref[v] = part(w[0]) | (a2 << 16) | (cls(w.back()) << 32);
     } else {
       if (w.size() > 255 || g.h2_mw.size() >= (1u << 24)) return;
-      g.h2_mref[v] = (3ull << 62) | ((uint64_t)g.h2_mw.size() << 8) | (uint64_t)w.size();
+      g.h2_mref[v] = (1ull << 63) | ((uint64_t)g.h2_mw.size() << 8) | (uint64_t)w.size();
       g.h2_mw.insert(g.h2_mw.end(), w.begin(), w.end());
     }
   }
+  g.h2_opv.resize(2 * (size_t(n) + 3), 0);
   g.k2v.shift = shift;
   g.k2v.n_words = (int64_t)g.h2_mw.size();
   g.k2v.n_msz = (int64_t)g.h2_msz.size();

@@ -172,7 +172,8 @@ def test_both_k1_variants_vs_c_oracle(name, variant):
 def test_unit_shift_and_v2_eligibility():
     from paper_2310_19295_b200.evaluator import device_graph
     MB = 1 << 20
-    info = device_graph(load_graph(gg.config_doc("layered"))).info()
+    lay = load_graph(gg.config_doc("layered"))   # keep the graph alive: the handle is cached on it
+    info = device_graph(lay).info()
     assert info["k1_variant"] == 2 and info["unit_shift"] >= 20   # MB-rounded sizes
     # an odd byte count forces unit 1; a 2^33-byte output forces the generic path
     doc = {"ops": [{"id": 0, "name": "a", "kind": "forward", "inputs": [], "outputs": [0]},
