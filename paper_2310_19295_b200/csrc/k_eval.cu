@@ -246,15 +246,16 @@ __global__ void __launch_bounds__(1024, 1) k1_eval_orders(const K1Args a) {
 // see K1V2Meta).  One persistent CTA per SM holds the graph metadata in
 // shared memory; G groups of NT threads each evaluate one candidate at a time.
 // Candidate rows are near-topological, so ops at consecutive positions have
-// nearby ids: every per-op gather is done with consecutive positions on
-// consecutive lanes (position k = t + j*NT), which keeps the shared-memory
-// gathers close to conflict-free.
+// nearby ids: per-op gathers run with consecutive positions on consecutive
+// lanes (position k = t + j*NT), which keeps them close to conflict-free.
 //   P1  pos[o_k] = k (u16) from the row held in registers; range check
-//   P2  checked edges pos[u] < pos[v]; per position: readback pos[o_k] == k
-//       (permutation), out/fs units of o_k, multi-consumer frees decided
-//       in place (o_k frees tensor m iff every other maximal consumer of m
-//       sits earlier), xs[k] = (out_k, free_k) packed int32 pair; then the
-//       NEXT candidate's row is loaded into registers (hidden behind P3)
+//   P2a checked edges pos[u] < pos[v]; per position: readback pos[o_k] == k
+//       (permutation), xs[k] = (out units of o_k) << 32 | (single-consumer
+//       free units of o_k); then the NEXT candidate's row is loaded into
+//       registers (it lands while P2b/P3 run)
+//   P2b per multi-consumer tensor: k* = latest position among its maximal
+//       consumers; 32-bit shared atomicAdd of its size units into the free
+//       field of xs[k*] (the host bounds every position's frees below 2^32)
 //   P3  blocked scan over xs (padded, LDS.128): live[k] = sum_{j<k}(out-free)
 //       + out_k, running max / first argmax, group scan of chunk totals
 struct K1V2Args {
@@ -263,41 +264,20 @@ struct K1V2Args {
   int n, G, C3, C3L;  // C3 = positions per thread in P3 (power of two), C3L = log2
   int shift;
   const int2* opv;
-  const unsigned long long* mref;
   const uint32_t* edges;
   int n_edges;
-  const uint32_t* mw;
-  int n_words;
-  const long long* msz;
-  int n_msz;
+  const uint32_t* mptr;
+  const uint16_t* mcons;
+  const uint32_t* msz;
+  int n_multi, n_mcons;
   int64_t* peak;
   int32_t* argmax;
   uint8_t* valid;
-  size_t off_mref, off_edges, off_mw, off_msz, off_groups, group_bytes, off_xs, off_red;
+  size_t off_edges, off_mptr, off_mcons, off_msz, off_groups, group_bytes, off_xs, off_red;
   int xs_stride;  // int64 words per P3 chunk (C3 + pad)
 };
 
 __device__ __forceinline__ unsigned pos_at(const uint16_t* pos, unsigned i) { return pos[i]; }
-
-// Rare path of K1 v2 (an op closing several multi-consumer lifetimes):
-// out of line so the 16x-unrolled position loop stays small in the I-cache.
-__device__ __noinline__ unsigned k1v2_list_frees(const uint16_t* pos, const uint32_t* mw,
-                                                 const long long* msz, unsigned r, int k) {
-  const uint32_t* wp = mw + (r >> 8);
-  const int cnt = r & 0xffu;
-  unsigned fr = 0;
-  bool all = true;
-#pragma unroll 1
-  for (int q = 0; q < cnt; ++q) {
-    const uint32_t w = wp[q];
-    all &= (int)pos[w & 0xffffu] < k;
-    if (!(w >> 31)) {  // end of this tensor's partner run
-      if (all) fr += (unsigned)msz[(w >> 16) & 0x7fffu];
-      all = true;
-    }
-  }
-  return fr;
-}
 
 template <int NT, int MAXC>
 __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
@@ -310,23 +290,23 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
       uint4* dst = reinterpret_cast<uint4*>(smem + off);
       for (size_t i = threadIdx.x; i < bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
     };
-    cp16(a.opv, 0, align16(8 * size_t(n + 3)));
-    cp16(a.mref, a.off_mref, align16(8 * size_t(n + 3)));
+    cp16(a.opv, 0, align16(8 * size_t(n + 1)));
     cp16(a.edges, a.off_edges, align16(4 * size_t(a.n_edges)));
-    cp16(a.mw, a.off_mw, align16(4 * size_t(a.n_words)));
-    cp16(a.msz, a.off_msz, align16(8 * size_t(a.n_msz)));
+    cp16(a.mptr, a.off_mptr, align16(4 * size_t(a.n_multi + 1)));
+    cp16(a.mcons, a.off_mcons, align16(2 * size_t(a.n_mcons)));
+    cp16(a.msz, a.off_msz, align16(4 * size_t(a.n_multi)));
   }
   __syncthreads();
   const int2* opv = reinterpret_cast<const int2*>(smem);
-  const unsigned long long* mref = reinterpret_cast<const unsigned long long*>(smem + a.off_mref);
   const uint32_t* edges = reinterpret_cast<const uint32_t*>(smem + a.off_edges);
-  const uint32_t* mw = reinterpret_cast<const uint32_t*>(smem + a.off_mw);
-  const long long* msz = reinterpret_cast<const long long*>(smem + a.off_msz);
+  const uint32_t* mptr = reinterpret_cast<const uint32_t*>(smem + a.off_mptr);
+  const uint16_t* mcons = reinterpret_cast<const uint16_t*>(smem + a.off_mcons);
+  const uint32_t* msz = reinterpret_cast<const uint32_t*>(smem + a.off_msz);
 
   const int gid = threadIdx.x / NT;
-  const int D = n;  // padding op; D+1 / D+2 have pinned positions
   const int tid = threadIdx.x - gid * NT;
   if (gid >= a.G) return;
+  const int D = n;  // padding op (zero bytes)
   const int bar_id = 1 + gid;
   unsigned char* gbase = smem + a.off_groups + size_t(gid) * a.group_bytes;
   uint16_t* pos = reinterpret_cast<uint16_t*>(gbase);
@@ -336,16 +316,14 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
   const int lane = tid & 31, warp = tid >> 5;
   constexpr int NWARPS = NT / 32;
   const int64_t cstride = int64_t(gridDim.x) * a.G;
-  // P2 writes position k = tid + j*NT to xs[(k >> C3L) * stride + (k & (C3-1))];
-  // NT is a multiple of C3, so that is xs_base + j * xs_step
+  // position k lives at xs[(k >> C3L) * stride + (k & (C3-1))]; NT is a
+  // multiple of C3, so P2a's slot j is xs_w + j * xs_step
   long long* xs_w = xs + (tid >> a.C3L) * a.xs_stride + (tid & (a.C3 - 1));
   const int xs_step = (NT >> a.C3L) * a.xs_stride;
-  const int n_edges = a.n_edges;
+  const int n_edges = a.n_edges, n_multi = a.n_multi;
+  for (int i = tid; i < n; i += NT) pos[i] = 0;  // no stale garbage for P2b
+  gbar(bar_id, NT);
 
-  if (tid == 0) {
-    pos[D + 1] = 0xffffu;  // "never earlier"
-    pos[D + 2] = 0;        // "always earlier" (k >= 1)
-  }
   int32_t v[MAXC];
   int64_t c = int64_t(blockIdx.x) * a.G + gid;
   if (c < a.B) {
@@ -358,17 +336,17 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
   }
   for (; c < a.B; c += cstride) {
     int bad = 0;
-    // ---- P1: scatter positions (padding slots write the dummy D)
+    // ---- P1: scatter positions (padding slots hold the op D)
 #pragma unroll
     for (int j = 0; j < MAXC; ++j) {
       const int k = tid + j * NT;
-      const bool oor = (unsigned)v[j] > (unsigned)D || (v[j] == D && k < n);
+      const bool oor = (unsigned)v[j] >= (unsigned)(k < n ? n : n + 1);
       bad |= oor;
       v[j] = oor ? D : v[j];
       pos[v[j]] = (uint16_t)k;
     }
     gbar(bar_id, NT);
-    // ---- P2: checked edges
+    // ---- P2a: checked edges
     int e = tid;
     for (; e + NT < n_edges; e += 2 * NT) {
       const uint32_t w0 = edges[e], w1 = edges[e + NT];
@@ -379,27 +357,18 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
       const uint32_t w0 = edges[e];
       bad |= pos_at(pos, w0 & 0xffffu) >= pos_at(pos, w0 >> 16);
     }
-    // ---- P2: per position: readback, out/free units, multi-consumer frees
+    // ---- P2a: per position: permutation readback, (out, single frees)
 #pragma unroll
     for (int j = 0; j < MAXC; ++j) {
       const int k = tid + j * NT;
       const int o = v[j];
       bad |= ((int)pos_at(pos, o) != k) & (k < n);
       const int2 ov = opv[o];
-      const unsigned long long r = mref[o];
-      unsigned fr = (unsigned)ov.y;
-      if (!(r >> 63)) {  // inline: one tensor group, <= 2 partners (branch-free)
-        const unsigned a1 = (unsigned)r & 0xffffu, a2 = ((unsigned)r >> 16) & 0xffffu;
-        const bool ok = ((int)pos_at(pos, a1) < k) & ((int)pos_at(pos, a2) < k);
-        const unsigned add = (unsigned)msz[(unsigned)(r >> 32) & 0x7fffu];
-        fr += ok ? add : 0u;
-      } else {
-        fr += k1v2_list_frees(pos, mw, msz, (unsigned)r, k);
-      }
-      // the frees decided at one position fit 32 bits (checked on the host)
-      if (k < n) xs_w[j * xs_step] = (long long)(((unsigned long long)(unsigned)ov.x << 32) | fr);
+      if (k < n)
+        xs_w[j * xs_step] =
+            (long long)(((unsigned long long)(unsigned)ov.x << 32) | (unsigned)ov.y);
     }
-    // prefetch the next candidate's row; it lands while P3 runs
+    // prefetch the next candidate's row; it lands while P2b / P3 run
     const int64_t cn = c + cstride;
     if (cn < a.B) {
       const int32_t* row = a.orders + cn * int64_t(n);
@@ -410,13 +379,23 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
       }
     }
     gbar(bar_id, NT);
+    // ---- P2b: multi-consumer tensors free after their latest maximal consumer
+    for (int m = tid; m < n_multi; m += NT) {
+      const int q0 = mptr[m], q1 = mptr[m + 1];
+      int kmax = 0;
+      for (int q = q0; q < q1; ++q) kmax = max(kmax, (int)pos_at(pos, mcons[q]));
+      if (kmax < n)  // (an invalid row may leave stale positions behind)
+        atomicAdd(reinterpret_cast<unsigned*>(xs + (kmax >> a.C3L) * a.xs_stride + (kmax & (a.C3 - 1))),
+                  msz[m]);
+    }
+    gbar(bar_id, NT);
     // ---- P3: blocked scan over this thread's chunk of xs
     const int k0 = tid << a.C3L;
-    const int m = min(n - k0, a.C3);  // may be <= 0
+    const int mc = min(n - k0, a.C3);  // may be <= 0
     const long long* xr = xs + size_t(tid) * a.xs_stride;
     long long run = 0, best = LLONG_MIN;
     int bi = INT_MAX;
-    for (int i = 0; i < m; i += 2) {
+    for (int i = 0; i < mc; i += 2) {
       const longlong2 pr = *reinterpret_cast<const longlong2*>(xr + i);
       long long live = run + (long long)((unsigned long long)pr.x >> 32);
       if (live > best) {
@@ -424,7 +403,7 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
         bi = i;
       }
       run = live - (long long)(unsigned)pr.x;
-      if (i + 1 < m) {
+      if (i + 1 < mc) {
         live = run + (long long)((unsigned long long)pr.y >> 32);
         if (live > best) {
           best = live;
@@ -456,14 +435,6 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
         cand = ov;
         ck = oi;
       }
-    }
-    if (NWARPS == 1) {
-      if (tid == 0) {
-        a.peak[c] = n == 0 ? 0 : (int64_t)cand << a.shift;
-        a.argmax[c] = n == 0 ? 0 : ck;
-        a.valid[c] = bad ? 0 : 1;
-      }
-      continue;
     }
     gbar(bar_id, NT);
     if (lane == 0) {
@@ -778,13 +749,13 @@ static int launch_k1v2(RmGraph* g, const int32_t* orders_dev, int64_t B, int64_t
   a.n = n;
   a.shift = g->k2v.shift;
   a.opv = g->k2v.opv.as<int2>();
-  a.mref = g->k2v.mref.as<unsigned long long>();
   a.edges = g->k2v.edges.as<uint32_t>();
   a.n_edges = (int)g->info.n_check_edges;
-  a.mw = g->k2v.mw.as<uint32_t>();
-  a.n_words = (int)g->k2v.n_words;
-  a.msz = g->k2v.msz.as<long long>();
-  a.n_msz = (int)g->k2v.n_msz;
+  a.mptr = g->k2v.mptr.as<uint32_t>();
+  a.mcons = g->k2v.mcons.as<uint16_t>();
+  a.msz = g->k2v.msz.as<uint32_t>();
+  a.n_multi = (int)g->k2v.n_multi;
+  a.n_mcons = (int)g->k2v.n_mcons;
   a.peak = peak;
   a.argmax = argmax;
   a.valid = valid;
@@ -798,12 +769,12 @@ static int launch_k1v2(RmGraph* g, const int32_t* orders_dev, int64_t B, int64_t
   // (C3 + pad) / 2 odd keeps 8 consecutive threads' 16-byte reads on
   // distinct bank groups
   a.xs_stride = ((a.C3 / 2) % 2 == 1) ? a.C3 : a.C3 + 2;
-  a.off_mref = align16(8 * size_t(n + 3));
-  a.off_edges = align16(a.off_mref + 8 * size_t(n + 3));
-  a.off_mw = align16(a.off_edges + 4 * size_t(a.n_edges));
-  a.off_msz = align16(a.off_mw + 4 * size_t(a.n_words));
-  a.off_groups = align16(a.off_msz + 8 * size_t(a.n_msz));
-  a.off_xs = align16(2 * size_t(n + 3));
+  a.off_edges = align16(8 * size_t(n + 1));
+  a.off_mptr = align16(a.off_edges + 4 * size_t(a.n_edges));
+  a.off_mcons = align16(a.off_mptr + 4 * size_t(a.n_multi + 1));
+  a.off_msz = align16(a.off_mcons + 2 * size_t(a.n_mcons));
+  a.off_groups = align16(a.off_msz + 4 * size_t(a.n_multi));
+  a.off_xs = align16(2 * size_t(n + 1));
   a.off_red = align16(a.off_xs + 8 * size_t((n + a.C3 - 1) / a.C3) * a.xs_stride);
   a.group_bytes = align16(a.off_red + 32 * 8 + 32 * 4);
   int dev = g->device;

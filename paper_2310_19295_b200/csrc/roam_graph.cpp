@@ -88,7 +88,7 @@ static void build_k1v2_host(RmGraph& g, const std::vector<int64_t>& out,
                             const std::vector<int64_t>& fs) {
   const int n = g.n, T = g.T;
   g.k2v.ok = 0;
-  if (n > 65532) return;  // ids and three dummy ops fit 16 bits
+  if (n > 65534) return;  // ids and the padding op fit 16 bits
   int shift = 62;
   for (int t = 0; t < T; ++t) {
     if (g.size[t] < 0) return;
@@ -96,7 +96,7 @@ static void build_k1v2_host(RmGraph& g, const std::vector<int64_t>& out,
   }
   if (shift == 62) shift = 0;
   const int64_t lim = INT32_MAX;
-  g.h2_opv.assign(2 * size_t(n), 0);
+  g.h2_opv.assign(2 * (size_t(n) + 1), 0);  // + padding op D = n with zero bytes
   for (int v = 0; v < n; ++v) {
     if ((out[v] >> shift) > lim || (fs[v] >> shift) > lim) return;
     g.h2_opv[2 * v] = (int32_t)(out[v] >> shift);
@@ -105,73 +105,27 @@ static void build_k1v2_host(RmGraph& g, const std::vector<int64_t>& out,
   g.h2_edges.resize(g.h_edge_u.size());
   for (size_t e = 0; e < g.h_edge_u.size(); ++e)
     g.h2_edges[e] = (uint32_t)g.h_edge_u[e] | ((uint32_t)g.h_edge_v[e] << 16);
-  // size classes of multi-consumer tensors
-  std::map<int64_t, int32_t> scls;
-  g.h2_msz.assign(1, 0);  // class 0 = "frees nothing"
-  std::vector<int32_t> mcls(g.h_msize.size());
-  for (size_t m = 0; m < g.h_msize.size(); ++m) {
-    auto it = scls.find(g.h_msize[m]);
-    if (it == scls.end()) {
-      it = scls.emplace(g.h_msize[m], (int32_t)g.h2_msz.size()).first;
-      g.h2_msz.push_back(g.h_msize[m] >> shift);
-    }
-    mcls[m] = it->second;
+  // multi-consumer tensors: maximal-consumer CSR (u16 ids) and size units
+  const size_t M = g.h_msize.size();
+  g.h2_mptr.assign(g.h_mptr.begin(), g.h_mptr.end());
+  g.h2_mcons.assign(g.h_mcons.begin(), g.h_mcons.end());
+  g.h2_msz.resize(M);
+  // the frees that land on one position are added into a 32-bit field:
+  // bound each op's worst case (its single-consumer frees plus every
+  // multi-consumer tensor it may close)
+  std::vector<int64_t> worst(n);
+  for (int v = 0; v < n; ++v) worst[v] = fs[v] >> shift;
+  for (size_t m = 0; m < M; ++m) {
+    const int64_t u = g.h_msize[m] >> shift;
+    if (u > (int64_t)UINT32_MAX) return;
+    g.h2_msz[m] = (uint32_t)u;
+    for (int q = g.h_mptr[m]; q < g.h_mptr[m + 1]; ++q) worst[g.h_mcons[q]] += u;
   }
-  if (g.h2_msz.size() >= 32768) return;
-  for (int64_t x : g.h2_msz)
-    if (x > (int64_t)UINT32_MAX) return;
-  // per closing op: its tensor groups (partners = the other maximal consumers)
-  std::vector<std::vector<uint32_t>> words(n);
-  for (size_t m = 0; m + 1 < g.h_mptr.size(); ++m) {
-    const int b0 = g.h_mptr[m], b1 = g.h_mptr[m + 1];
-    for (int q = b0; q < b1; ++q) {
-      const int v = g.h_mcons[q];
-      std::vector<uint32_t>& w = words[v];
-      int left = b1 - b0 - 1;
-      for (int r = b0; r < b1; ++r) {
-        if (r == q) continue;
-        --left;
-        w.push_back((uint32_t)g.h_mcons[r] | ((uint32_t)mcls[m] << 16) | (left ? 0x80000000u : 0u));
-      }
-    }
-  }
-  // the frees decided at one position are packed into 32 bits: bound them
-  for (int v = 0; v < n; ++v) {
-    int64_t mx = fs[v] >> shift;
-    for (uint32_t w : words[v])
-      if (!(w >> 31)) mx += g.h2_msz[(w >> 16) & 0x7fffu];
-    if (mx > (int64_t)UINT32_MAX) return;
-  }
-  // mref[v] (64 bits), for v < n plus three dummy ops D = n (row padding),
-  // D+1 (position pinned to 0xffff: never earlier) and D+2 (position pinned
-  // to 0: always earlier for k >= 1):
-  //   inline (bit 63 = 0): partners a1 (bits 0-15), a2 (16-31), size class
-  //     (32-46).  v frees msz[cls] iff pos[a1] < k and pos[a2] < k; unused
-  //     slots point at D+2, "no group" is a1 = D+1 with class 0.
-  //   list (bit 63 = 1): bits 0-31 = (start << 8) | count over mw[].
-  const uint64_t D = (uint64_t)n;
-  const uint64_t none = (D + 1) | ((D + 2) << 16);
-  g.h2_mref.assign(size_t(n) + 3, none);
-  g.h2_mw.assign(1, 0);
-  for (int v = 0; v < n; ++v) {
-    const std::vector<uint32_t>& w = words[v];
-    if (w.empty()) continue;
-    auto part = [](uint32_t x) { return (uint64_t)(x & 0xffffu); };
-    auto cls = [](uint32_t x) { return (uint64_t)((x >> 16) & 0x7fffu); };
-    const bool one_group = w.size() == 1 || (w.size() == 2 && (w[0] >> 31));
-    if (one_group) {
-      const uint64_t a2 = w.size() == 2 ? part(w[1]) : D + 2;
-      g.h2_mref[v] = part(w[0]) | (a2 << 16) | (cls(w.back()) << 32);
-    } else {
-      if (w.size() > 255 || g.h2_mw.size() >= (1u << 24)) return;
-      g.h2_mref[v] = (1ull << 63) | ((uint64_t)g.h2_mw.size() << 8) | (uint64_t)w.size();
-      g.h2_mw.insert(g.h2_mw.end(), w.begin(), w.end());
-    }
-  }
-  g.h2_opv.resize(2 * (size_t(n) + 3), 0);
+  for (int v = 0; v < n; ++v)
+    if (worst[v] > (int64_t)UINT32_MAX) return;
   g.k2v.shift = shift;
-  g.k2v.n_words = (int64_t)g.h2_mw.size();
-  g.k2v.n_msz = (int64_t)g.h2_msz.size();
+  g.k2v.n_multi = (int64_t)M;
+  g.k2v.n_mcons = (int64_t)g.h2_mcons.size();
   g.k2v.ok = 1;
 }
 
@@ -427,9 +381,9 @@ int rm_graph_create(const RmGraphDesc* d, uint32_t flags, RmGraph** out) {
     g->device = dev;
     cudaError_t e = g->info.wide_index ? upload_k1<int32_t>(*g) : upload_k1<uint16_t>(*g);
     if (!e && g->k2v.ok) e = up(g->k2v.opv, g->h2_opv);
-    if (!e && g->k2v.ok) e = up(g->k2v.mref, g->h2_mref);
     if (!e && g->k2v.ok) e = up(g->k2v.edges, g->h2_edges);
-    if (!e && g->k2v.ok) e = up(g->k2v.mw, g->h2_mw);
+    if (!e && g->k2v.ok) e = up(g->k2v.mptr, g->h2_mptr);
+    if (!e && g->k2v.ok) e = up(g->k2v.mcons, g->h2_mcons);
     if (!e && g->k2v.ok) e = up(g->k2v.msz, g->h2_msz);
     if (!e) e = up(g->d_size, g->size);
     if (!e) e = up(g->d_producer, g->producer);

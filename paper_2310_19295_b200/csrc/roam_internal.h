@@ -84,19 +84,18 @@ struct K1Meta {
 };
 
 // K1 v2 metadata (the default order evaluator when the graph qualifies:
-// n <= 65535, sizes >= 0, every per-op byte count < 2^31 units of 2^shift).
-//   opv[v]  = {out[v] >> shift, fs[v] >> shift}  (int2)
-//   mref[v] = the multi-consumer lifetimes v may close (0 = none): inline
-//             for up to two partners (see build_k1v2_host), else a run of
-//             mw words: partner | sizecls << 16 | cont << 31; a tensor group
-//             ends with cont = 0 and v frees msz[sizecls] iff every partner
-//             sits earlier in the order.
-//   edges   = checked pred edges packed u | v << 16.
+// n < 65535, sizes >= 0, per-op byte counts < 2^31 units of 2^shift and the
+// frees that can land on one position < 2^32 units).
+//   opv[v]  = {out[v] >> shift, fs[v] >> shift} (int2), plus a zero padding op
+//   edges   = checked pred edges packed u | v << 16
+//   mptr/mcons/msz = the multi-consumer tensors: maximal consumers (u16) and
+//             size units (u32); a tensor is freed after its latest maximal
+//             consumer.
 struct K1V2Meta {
   int ok = 0;
   int shift = 0;
-  int64_t n_words = 0, n_msz = 0;
-  DevBuf opv, mref, edges, mw, msz;
+  int64_t n_multi = 0, n_mcons = 0;
+  DevBuf opv, edges, mptr, mcons, msz;
 };
 
 }  // namespace roam
@@ -120,9 +119,8 @@ struct RmGraph {
   roam::K1Meta k1;
   roam::K1V2Meta k2v;
   std::vector<int32_t> h2_opv;     // 2n
-  std::vector<uint64_t> h2_mref;
-  std::vector<uint32_t> h2_edges, h2_mw;
-  std::vector<int64_t> h2_msz;
+  std::vector<uint32_t> h2_edges, h2_mptr, h2_msz;
+  std::vector<uint16_t> h2_mcons;
   roam::DevBuf d_size, d_producer, d_cons_ptr, d_cons_idx, d_in_ptr, d_in_idx, d_out_ptr,
       d_out_idx, d_pred_ptr, d_pred_idx, d_succ_ptr, d_succ_idx;
 };
