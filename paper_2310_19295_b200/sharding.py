@@ -1,0 +1,88 @@
+"""Candidate sharding across GPUs and the global (peak, id) argmin.
+
+Candidates are independent units: rank r of W evaluates the
+contiguous id range [r*B/W, (r+1)*B/W) of a candidate batch, with no data-path
+collective; the only exchange is one all_gather of each rank's 16-byte best
+{peak:int64, id:int64}.  The lexicographic min of (peak, id) over the gathered
+pairs equals the reference's first strict minimum over the global id order
+(tests/oracles.py:46-56 ``peak < best``; planner.py:209-216), because ids are
+globally unique and ranks own disjoint ranges.
+
+One process per GPU; ``torch.distributed`` carries the exchange (NCCL over
+NVLink on the GPU box, gloo in the CPU tests).  Graph metadata is replicated:
+every rank builds the same graph and its own device handle.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+NONE_PEAK = 2**63 - 1
+
+
+def shard_range(total: int, world: int, rank: int) -> tuple[int, int]:
+    """[lo, hi) candidate ids of ``rank``: contiguous, sizes differ by <= 1."""
+    if world < 1 or not 0 <= rank < world or total < 0:
+        raise ValueError("bad shard arguments")
+    base, extra = divmod(total, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def lex_min(pairs) -> tuple[int, int]:
+    """Lexicographic min of (peak, id) pairs, ignoring id == -1 (no valid
+    candidate on that rank); (INT64_MAX, -1) when none is valid."""
+    best = (NONE_PEAK, -1)
+    for peak, cid in pairs:
+        peak, cid = int(peak), int(cid)
+        if cid < 0:
+            continue
+        if best[1] < 0 or (peak, cid) < best:
+            best = (peak, cid)
+    return best
+
+
+def allgather_best(best, group=None):
+    """Exchange each rank's best {peak, id} (int64[2] tensor on the rank's
+    device for NCCL, on CPU for gloo) and return the global lexicographic min
+    as a tensor of the same kind (every rank gets the same answer)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    out = torch.empty(world * 2, dtype=torch.int64, device=best.device)
+    dist.all_gather_into_tensor(out, best.contiguous(), group=group)
+    pk = out.view(world, 2)
+    big = torch.full_like(pk[:, 0], NONE_PEAK)
+    ids = torch.where(pk[:, 1] < 0, big, pk[:, 1])   # ranks with nothing valid lose
+    m = pk[:, 0].min()
+    idmin = torch.where(pk[:, 0] == m, ids, big).min()
+    return torch.stack([m, torch.where(idmin == NONE_PEAK, torch.full_like(idmin, -1), idmin)])
+
+
+@dataclass(frozen=True)
+class ShardResult:
+    best_peak: int
+    best_id: int
+    local_range: tuple[int, int]
+    local_valid: int
+
+
+def evaluate_sharded(g, total: int, seed: int = 0, group=None, stream=None) -> ShardResult:
+    """Generate this rank's candidate ids on its device (counter-RNG Kahn),
+    evaluate them with K1, take the local first strict minimum on device and
+    exchange it: the 8-GPU candidate search of BASELINE config 5."""
+    import torch
+    import torch.distributed as dist
+
+    from . import evaluator as ev
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    lo, hi = shard_range(total, world, rank)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    orders = ev.generate_orders(g, seed, lo, hi - lo, device=dev, stream=stream)
+    peak, _, valid = ev.evaluate_orders(g, orders, stream=stream)
+    best = ev.select_device(peak, valid, id_base=lo, stream=stream)
+    if world > 1:
+        best = allgather_best(best, group)
+    b = [int(x) for x in best.cpu().tolist()]
+    return ShardResult(b[0], b[1], (lo, hi), int(valid.sum().item()))
