@@ -18,6 +18,7 @@ def test_install_uninstall_roundtrip():
     names = [(mp.planner, n) for n in ("peak_memory", "tensor_lifetimes", "live_bytes_by_timestep",
                                        "_pool_map", "repair_conflicts", "validate_layout")]
     names += [(mp.layout, "layout_violations"), (mp.simulator, "layout_violations"),
+              (mp.ordering, "weight_update_cost"),
               (mp.simulator, "peak_memory")]
     before = {k: getattr(*k) for k in names}
     plug.install(mp)
@@ -73,3 +74,28 @@ def test_repair_mover_placement_matches_reference(monkeypatch):
         want = mp.layout.repair_conflicts(m, p)
         got = L.repair_conflicts(m, p)
         assert got == want
+
+
+@pytest.mark.skipif(mp is None, reason="reference memplan not importable")
+def test_weight_update_cost_sweep_matches_reference(monkeypatch):
+    """The event-sweep weight_update_cost answers every query the reference
+    planner makes exactly like the reference (host code, no GPU)."""
+    import memplan.graphgen as rgen
+
+    from paper_2310_19295_b200 import graphgen as gg
+    fast = plug._weight_update_cost_factory(mp)
+    orig = mp.ordering.weight_update_cost
+    seen = []
+
+    def both(g, bounds, t, branch, alpha=None):
+        a, b = orig(g, bounds, t, branch, alpha), fast(g, bounds, t, branch, alpha)
+        assert a == b and type(a[1]) is type(b[1])
+        seen.append(t)
+        return a
+
+    monkeypatch.setattr(mp.ordering, "weight_update_cost", both)
+    mp.planner.plan(mp.graph.load_graph(gg.config_doc("gpt2-small")))
+    for arch in ("mlp", "residual", "transformer_block"):
+        for opt in ("sgd", "adam"):
+            mp.planner.plan(rgen.gen_training_graph(arch, 3, optimizer=opt))
+    assert len(seen) > 100
