@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(1024, 1) k1_eval_orders(const K1Args a) {
 struct K1V2Args {
   const int32_t* orders;
   int64_t B;
-  int n, G, C3, C3L;  // C3 = positions per thread in P3 (power of two), C3L = log2
+  int n, G;
   int shift;
   const int2* opv;
   const uint32_t* edges;
@@ -274,7 +274,16 @@ struct K1V2Args {
   int32_t* argmax;
   uint8_t* valid;
   size_t off_edges, off_mptr, off_mcons, off_msz, off_groups, group_bytes, off_xs, off_red;
-  int xs_stride;  // int64 words per P3 chunk (C3 + pad)
+};
+
+// P3 chunk geometry: C3 = MAXC positions per thread (power of two); the
+// stride pads each chunk so that (stride / 2) is odd, which keeps the 16-byte
+// reads of 8 consecutive threads on distinct bank groups.
+template <int MAXC>
+struct XsGeom {
+  static constexpr int C3 = MAXC;
+  static constexpr int C3L = MAXC == 4 ? 2 : MAXC == 8 ? 3 : 4;
+  static constexpr int STRIDE = ((MAXC / 2) % 2 == 1) ? MAXC : MAXC + 2;
 };
 
 __device__ __forceinline__ unsigned pos_at(const uint16_t* pos, unsigned i) { return pos[i]; }
@@ -316,10 +325,11 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
   const int lane = tid & 31, warp = tid >> 5;
   constexpr int NWARPS = NT / 32;
   const int64_t cstride = int64_t(gridDim.x) * a.G;
-  // position k lives at xs[(k >> C3L) * stride + (k & (C3-1))]; NT is a
-  // multiple of C3, so P2a's slot j is xs_w + j * xs_step
-  long long* xs_w = xs + (tid >> a.C3L) * a.xs_stride + (tid & (a.C3 - 1));
-  const int xs_step = (NT >> a.C3L) * a.xs_stride;
+  // position k lives at xs[(k >> C3L) * STRIDE + (k & (C3-1))]; NT is a
+  // multiple of C3, so P2a's slot j is xs_w + j * XS_STEP (compile-time)
+  using X = XsGeom<MAXC>;
+  constexpr int XS_STEP = (NT / X::C3) * X::STRIDE;
+  long long* xs_w = xs + (tid >> X::C3L) * X::STRIDE + (tid & (X::C3 - 1));
   const int n_edges = a.n_edges, n_multi = a.n_multi;
   for (int i = tid; i < n; i += NT) pos[i] = 0;  // no stale garbage for P2b
   gbar(bar_id, NT);
@@ -365,7 +375,7 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
       bad |= ((int)pos_at(pos, o) != k) & (k < n);
       const int2 ov = opv[o];
       if (k < n)
-        xs_w[j * xs_step] =
+        xs_w[j * XS_STEP] =
             (long long)(((unsigned long long)(unsigned)ov.x << 32) | (unsigned)ov.y);
     }
     // prefetch the next candidate's row; it lands while P2b / P3 run
@@ -385,31 +395,34 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
       int kmax = 0;
       for (int q = q0; q < q1; ++q) kmax = max(kmax, (int)pos_at(pos, mcons[q]));
       if (kmax < n)  // (an invalid row may leave stale positions behind)
-        atomicAdd(reinterpret_cast<unsigned*>(xs + (kmax >> a.C3L) * a.xs_stride + (kmax & (a.C3 - 1))),
+        atomicAdd(reinterpret_cast<unsigned*>(xs + (kmax >> X::C3L) * X::STRIDE + (kmax & (X::C3 - 1))),
                   msz[m]);
     }
     gbar(bar_id, NT);
     // ---- P3: blocked scan over this thread's chunk of xs
-    const int k0 = tid << a.C3L;
-    const int mc = min(n - k0, a.C3);  // may be <= 0
-    const long long* xr = xs + size_t(tid) * a.xs_stride;
+    const int k0 = tid << X::C3L;
+    const int mc = n - k0;  // positions of this chunk: min(mc, C3); may be <= 0
+    const long long* xr = xs + tid * X::STRIDE;
     long long run = 0, best = LLONG_MIN;
     int bi = INT_MAX;
-    for (int i = 0; i < mc; i += 2) {
-      const longlong2 pr = *reinterpret_cast<const longlong2*>(xr + i);
-      long long live = run + (long long)((unsigned long long)pr.x >> 32);
-      if (live > best) {
-        best = live;
-        bi = i;
-      }
-      run = live - (long long)(unsigned)pr.x;
-      if (i + 1 < mc) {
-        live = run + (long long)((unsigned long long)pr.y >> 32);
+#pragma unroll
+    for (int i = 0; i < X::C3; i += 2) {
+      if (i < mc) {
+        const longlong2 pr = *reinterpret_cast<const longlong2*>(xr + i);
+        long long live = run + (long long)((unsigned long long)pr.x >> 32);
         if (live > best) {
           best = live;
-          bi = i + 1;
+          bi = i;
         }
-        run = live - (long long)(unsigned)pr.y;
+        run = live - (long long)(unsigned)pr.x;
+        if (i + 1 < mc) {
+          live = run + (long long)((unsigned long long)pr.y >> 32);
+          if (live > best) {
+            best = live;
+            bi = i + 1;
+          }
+          run = live - (long long)(unsigned)pr.y;
+        }
       }
     }
     const int bestk = bi == INT_MAX ? INT_MAX : k0 + bi;
@@ -762,20 +775,16 @@ static int launch_k1v2(RmGraph* g, const int32_t* orders_dev, int64_t B, int64_t
   const int NT = n <= 1024 ? 64 : n <= 2048 ? 128 : n <= 4096 ? 256 : n <= 8192 ? 512 : 1024;
   const int C = std::max(1, (n + NT - 1) / NT);
   if (C > 16) return 1;  // > 16384 ops: the generic evaluator
-  int C3L = 1;           // pairs for the 16-byte reads
-  while ((1 << C3L) < C) ++C3L;
-  a.C3 = 1 << C3L;
-  a.C3L = C3L;
-  // (C3 + pad) / 2 odd keeps 8 consecutive threads' 16-byte reads on
-  // distinct bank groups
-  a.xs_stride = ((a.C3 / 2) % 2 == 1) ? a.C3 : a.C3 + 2;
+  const int MAXC = C <= 4 ? 4 : C <= 8 ? 8 : 16;
+  const int C3 = MAXC;
+  const int stride = ((C3 / 2) % 2 == 1) ? C3 : C3 + 2;  // XsGeom<MAXC>::STRIDE
   a.off_edges = align16(8 * size_t(n + 1));
   a.off_mptr = align16(a.off_edges + 4 * size_t(a.n_edges));
   a.off_mcons = align16(a.off_mptr + 4 * size_t(a.n_multi + 1));
   a.off_msz = align16(a.off_mcons + 2 * size_t(a.n_mcons));
   a.off_groups = align16(a.off_msz + 4 * size_t(a.n_multi));
   a.off_xs = align16(2 * size_t(n + 1));
-  a.off_red = align16(a.off_xs + 8 * size_t((n + a.C3 - 1) / a.C3) * a.xs_stride);
+  a.off_red = align16(a.off_xs + 8 * size_t((n + C3 - 1) / C3) * stride);
   a.group_bytes = align16(a.off_red + 32 * 8 + 32 * 4);
   int dev = g->device;
   int max_smem = 0;
@@ -791,9 +800,9 @@ static int launch_k1v2(RmGraph* g, const int32_t* orders_dev, int64_t B, int64_t
   const size_t smem = a.off_groups + size_t(G) * a.group_bytes;
   const int grid = (int)std::min<int64_t>(sms, (B + G - 1) / G);
   switch (NT) {
-    case 64: return C <= 4 ? launch_k1v2_t<64, 4>(a, grid, smem, s)
-                   : C <= 8 ? launch_k1v2_t<64, 8>(a, grid, smem, s)
-                            : launch_k1v2_t<64, 16>(a, grid, smem, s);
+    case 64: return MAXC == 4 ? launch_k1v2_t<64, 4>(a, grid, smem, s)
+                   : MAXC == 8 ? launch_k1v2_t<64, 8>(a, grid, smem, s)
+                               : launch_k1v2_t<64, 16>(a, grid, smem, s);
     case 128: return launch_k1v2_t<128, 16>(a, grid, smem, s);
     case 256: return launch_k1v2_t<256, 16>(a, grid, smem, s);
     case 512: return launch_k1v2_t<512, 16>(a, grid, smem, s);
