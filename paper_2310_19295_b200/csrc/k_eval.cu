@@ -266,14 +266,15 @@ struct K1V2Args {
   const int2* opv;
   const uint32_t* edges;
   int n_edges;
+  const uint32_t* mpair;
   const uint32_t* mptr;
   const uint16_t* mcons;
   const uint32_t* msz;
-  int n_multi, n_mcons;
+  int n_pair, n_gen, n_mcons;
   int64_t* peak;
   int32_t* argmax;
   uint8_t* valid;
-  size_t off_edges, off_mptr, off_mcons, off_msz, off_groups, group_bytes, off_xs, off_red;
+  size_t off_edges, off_mpair, off_mptr, off_mcons, off_msz, off_groups, group_bytes, off_xs, off_red;
 };
 
 // P3 chunk geometry: C3 = MAXC positions per thread (power of two); the
@@ -301,13 +302,15 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
     };
     cp16(a.opv, 0, align16(8 * size_t(n + 1)));
     cp16(a.edges, a.off_edges, align16(4 * size_t(a.n_edges)));
-    cp16(a.mptr, a.off_mptr, align16(4 * size_t(a.n_multi + 1)));
+    cp16(a.mpair, a.off_mpair, align16(4 * size_t(a.n_pair)));
+    cp16(a.mptr, a.off_mptr, align16(4 * size_t(a.n_gen + 1)));
     cp16(a.mcons, a.off_mcons, align16(2 * size_t(a.n_mcons)));
-    cp16(a.msz, a.off_msz, align16(4 * size_t(a.n_multi)));
+    cp16(a.msz, a.off_msz, align16(4 * size_t(a.n_pair + a.n_gen)));
   }
   __syncthreads();
   const int2* opv = reinterpret_cast<const int2*>(smem);
   const uint32_t* edges = reinterpret_cast<const uint32_t*>(smem + a.off_edges);
+  const uint32_t* mpair = reinterpret_cast<const uint32_t*>(smem + a.off_mpair);
   const uint32_t* mptr = reinterpret_cast<const uint32_t*>(smem + a.off_mptr);
   const uint16_t* mcons = reinterpret_cast<const uint16_t*>(smem + a.off_mcons);
   const uint32_t* msz = reinterpret_cast<const uint32_t*>(smem + a.off_msz);
@@ -330,9 +333,14 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
   using X = XsGeom<MAXC>;
   constexpr int XS_STEP = (NT / X::C3) * X::STRIDE;
   long long* xs_w = xs + (tid >> X::C3L) * X::STRIDE + (tid & (X::C3 - 1));
-  const int n_edges = a.n_edges, n_multi = a.n_multi;
+  const int n_edges = a.n_edges, n_pair = a.n_pair, n_gen = a.n_gen;
   for (int i = tid; i < n; i += NT) pos[i] = 0;  // no stale garbage for P2b
+  if (tid == 0) {
+    pos[D + 1] = 0;        // dummy edge (D+1 -> D+2) of the predicated edge loop
+    pos[D + 2] = 0xffffu;  // always passes
+  }
   gbar(bar_id, NT);
+  const uint32_t dummy_edge = (uint32_t)(D + 1) | ((uint32_t)(D + 2) << 16);
 
   int32_t v[MAXC];
   int64_t c = int64_t(blockIdx.x) * a.G + gid;
@@ -356,16 +364,13 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
       pos[v[j]] = (uint16_t)k;
     }
     gbar(bar_id, NT);
-    // ---- P2a: checked edges
-    int e = tid;
-    for (; e + NT < n_edges; e += 2 * NT) {
-      const uint32_t w0 = edges[e], w1 = edges[e + NT];
-      bad |= (pos_at(pos, w0 & 0xffffu) >= pos_at(pos, w0 >> 16)) |
-             (pos_at(pos, w1 & 0xffffu) >= pos_at(pos, w1 >> 16));
-    }
-    if (e < n_edges) {
-      const uint32_t w0 = edges[e];
-      bad |= pos_at(pos, w0 & 0xffffu) >= pos_at(pos, w0 >> 16);
+    // ---- P2a: checked edges, four independent ones per thread per step
+    for (int e0 = tid; e0 < n_edges; e0 += 4 * NT) {
+      uint32_t w[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) w[i] = e0 + i * NT < n_edges ? edges[e0 + i * NT] : dummy_edge;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) bad |= pos_at(pos, w[i] & 0xffffu) >= pos_at(pos, w[i] >> 16);
     }
     // ---- P2a: per position: permutation readback, (out, single frees)
 #pragma unroll
@@ -390,13 +395,21 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
     }
     gbar(bar_id, NT);
     // ---- P2b: multi-consumer tensors free after their latest maximal consumer
-    for (int m = tid; m < n_multi; m += NT) {
+    // (a kmax >= n can only come from an invalid row's stale positions)
+    auto add_free = [&](int kmax, unsigned units) {
+      if (kmax < n)
+        atomicAdd(reinterpret_cast<unsigned*>(xs + (kmax >> X::C3L) * X::STRIDE + (kmax & (X::C3 - 1))),
+                  units);
+    };
+    for (int m = tid; m < n_pair; m += NT) {
+      const uint32_t w = mpair[m];
+      add_free(max((int)pos_at(pos, w & 0xffffu), (int)pos_at(pos, w >> 16)), msz[m]);
+    }
+    for (int m = tid; m < n_gen; m += NT) {
       const int q0 = mptr[m], q1 = mptr[m + 1];
       int kmax = 0;
       for (int q = q0; q < q1; ++q) kmax = max(kmax, (int)pos_at(pos, mcons[q]));
-      if (kmax < n)  // (an invalid row may leave stale positions behind)
-        atomicAdd(reinterpret_cast<unsigned*>(xs + (kmax >> X::C3L) * X::STRIDE + (kmax & (X::C3 - 1))),
-                  msz[m]);
+      add_free(kmax, msz[n_pair + m]);
     }
     gbar(bar_id, NT);
     // ---- P3: blocked scan over this thread's chunk of xs
@@ -764,10 +777,12 @@ static int launch_k1v2(RmGraph* g, const int32_t* orders_dev, int64_t B, int64_t
   a.opv = g->k2v.opv.as<int2>();
   a.edges = g->k2v.edges.as<uint32_t>();
   a.n_edges = (int)g->info.n_check_edges;
+  a.mpair = g->k2v.mpair.as<uint32_t>();
   a.mptr = g->k2v.mptr.as<uint32_t>();
   a.mcons = g->k2v.mcons.as<uint16_t>();
   a.msz = g->k2v.msz.as<uint32_t>();
-  a.n_multi = (int)g->k2v.n_multi;
+  a.n_pair = (int)g->k2v.n_pair;
+  a.n_gen = (int)g->k2v.n_gen;
   a.n_mcons = (int)g->k2v.n_mcons;
   a.peak = peak;
   a.argmax = argmax;
@@ -779,11 +794,12 @@ static int launch_k1v2(RmGraph* g, const int32_t* orders_dev, int64_t B, int64_t
   const int C3 = MAXC;
   const int stride = ((C3 / 2) % 2 == 1) ? C3 : C3 + 2;  // XsGeom<MAXC>::STRIDE
   a.off_edges = align16(8 * size_t(n + 1));
-  a.off_mptr = align16(a.off_edges + 4 * size_t(a.n_edges));
-  a.off_mcons = align16(a.off_mptr + 4 * size_t(a.n_multi + 1));
+  a.off_mpair = align16(a.off_edges + 4 * size_t(a.n_edges));
+  a.off_mptr = align16(a.off_mpair + 4 * size_t(a.n_pair));
+  a.off_mcons = align16(a.off_mptr + 4 * size_t(a.n_gen + 1));
   a.off_msz = align16(a.off_mcons + 2 * size_t(a.n_mcons));
-  a.off_groups = align16(a.off_msz + 4 * size_t(a.n_multi));
-  a.off_xs = align16(2 * size_t(n + 1));
+  a.off_groups = align16(a.off_msz + 4 * size_t(a.n_pair + a.n_gen));
+  a.off_xs = align16(2 * size_t(n + 3));
   a.off_red = align16(a.off_xs + 8 * size_t((n + C3 - 1) / C3) * stride);
   a.group_bytes = align16(a.off_red + 32 * 8 + 32 * 4);
   int dev = g->device;

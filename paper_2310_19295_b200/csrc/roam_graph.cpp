@@ -88,7 +88,7 @@ static void build_k1v2_host(RmGraph& g, const std::vector<int64_t>& out,
                             const std::vector<int64_t>& fs) {
   const int n = g.n, T = g.T;
   g.k2v.ok = 0;
-  if (n > 65534) return;  // ids and the padding op fit 16 bits
+  if (n > 65532) return;  // ids and the three dummy ops fit 16 bits
   int shift = 62;
   for (int t = 0; t < T; ++t) {
     if (g.size[t] < 0) return;
@@ -105,26 +105,40 @@ static void build_k1v2_host(RmGraph& g, const std::vector<int64_t>& out,
   g.h2_edges.resize(g.h_edge_u.size());
   for (size_t e = 0; e < g.h_edge_u.size(); ++e)
     g.h2_edges[e] = (uint32_t)g.h_edge_u[e] | ((uint32_t)g.h_edge_v[e] << 16);
-  // multi-consumer tensors: maximal-consumer CSR (u16 ids) and size units
+  // multi-consumer tensors: two-consumer ones first as packed pairs (the
+  // common case), the rest as a CSR; sizes in units
   const size_t M = g.h_msize.size();
-  g.h2_mptr.assign(g.h_mptr.begin(), g.h_mptr.end());
-  g.h2_mcons.assign(g.h_mcons.begin(), g.h_mcons.end());
-  g.h2_msz.resize(M);
-  // the frees that land on one position are added into a 32-bit field:
-  // bound each op's worst case (its single-consumer frees plus every
-  // multi-consumer tensor it may close)
   std::vector<int64_t> worst(n);
   for (int v = 0; v < n; ++v) worst[v] = fs[v] >> shift;
+  g.h2_mpair.clear();
+  g.h2_mptr.assign(1, 0);
+  g.h2_mcons.clear();
+  std::vector<uint32_t> sz_pair, sz_gen;
   for (size_t m = 0; m < M; ++m) {
     const int64_t u = g.h_msize[m] >> shift;
     if (u > (int64_t)UINT32_MAX) return;
-    g.h2_msz[m] = (uint32_t)u;
-    for (int q = g.h_mptr[m]; q < g.h_mptr[m + 1]; ++q) worst[g.h_mcons[q]] += u;
+    const int q0 = g.h_mptr[m], q1 = g.h_mptr[m + 1];
+    for (int q = q0; q < q1; ++q) worst[g.h_mcons[q]] += u;
+    if (q1 - q0 == 2) {
+      g.h2_mpair.push_back((uint32_t)g.h_mcons[q0] | ((uint32_t)g.h_mcons[q0 + 1] << 16));
+      sz_pair.push_back((uint32_t)u);
+    } else {
+      for (int q = q0; q < q1; ++q) g.h2_mcons.push_back((uint16_t)g.h_mcons[q]);
+      g.h2_mptr.push_back((uint32_t)g.h2_mcons.size());
+      sz_gen.push_back((uint32_t)u);
+    }
   }
+  // sizes: pairs first, then the generic tensors
+  g.h2_msz = sz_pair;
+  g.h2_msz.insert(g.h2_msz.end(), sz_gen.begin(), sz_gen.end());
+  // the frees that land on one position are added into a 32-bit field:
+  // bound each op's worst case (its single-consumer frees plus every
+  // multi-consumer tensor it may close)
   for (int v = 0; v < n; ++v)
     if (worst[v] > (int64_t)UINT32_MAX) return;
+  g.k2v.n_pair = (int64_t)g.h2_mpair.size();
+  g.k2v.n_gen = (int64_t)sz_gen.size();
   g.k2v.shift = shift;
-  g.k2v.n_multi = (int64_t)M;
   g.k2v.n_mcons = (int64_t)g.h2_mcons.size();
   g.k2v.ok = 1;
 }
@@ -382,6 +396,7 @@ int rm_graph_create(const RmGraphDesc* d, uint32_t flags, RmGraph** out) {
     cudaError_t e = g->info.wide_index ? upload_k1<int32_t>(*g) : upload_k1<uint16_t>(*g);
     if (!e && g->k2v.ok) e = up(g->k2v.opv, g->h2_opv);
     if (!e && g->k2v.ok) e = up(g->k2v.edges, g->h2_edges);
+    if (!e && g->k2v.ok) e = up(g->k2v.mpair, g->h2_mpair);
     if (!e && g->k2v.ok) e = up(g->k2v.mptr, g->h2_mptr);
     if (!e && g->k2v.ok) e = up(g->k2v.mcons, g->h2_mcons);
     if (!e && g->k2v.ok) e = up(g->k2v.msz, g->h2_msz);

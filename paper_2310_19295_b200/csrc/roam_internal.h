@@ -88,14 +88,14 @@ struct K1Meta {
 // frees that can land on one position < 2^32 units).
 //   opv[v]  = {out[v] >> shift, fs[v] >> shift} (int2), plus a zero padding op
 //   edges   = checked pred edges packed u | v << 16
-//   mptr/mcons/msz = the multi-consumer tensors: maximal consumers (u16) and
-//             size units (u32); a tensor is freed after its latest maximal
-//             consumer.
+//   multi-consumer tensors (freed after their latest maximal consumer):
+//             mpair = the two-consumer ones as packed u16 pairs; mptr/mcons =
+//             the rest as a CSR; msz = size units, pairs first.
 struct K1V2Meta {
   int ok = 0;
   int shift = 0;
-  int64_t n_multi = 0, n_mcons = 0;
-  DevBuf opv, edges, mptr, mcons, msz;
+  int64_t n_pair = 0, n_gen = 0, n_mcons = 0;
+  DevBuf opv, edges, mpair, mptr, mcons, msz;
 };
 
 }  // namespace roam
@@ -119,7 +119,7 @@ struct RmGraph {
   roam::K1Meta k1;
   roam::K1V2Meta k2v;
   std::vector<int32_t> h2_opv;     // 2n
-  std::vector<uint32_t> h2_edges, h2_mptr, h2_msz;
+  std::vector<uint32_t> h2_edges, h2_mpair, h2_mptr, h2_msz;
   std::vector<uint16_t> h2_mcons;
   roam::DevBuf d_size, d_producer, d_cons_ptr, d_cons_idx, d_in_ptr, d_in_idx, d_out_ptr,
       d_out_idx, d_pred_ptr, d_pred_idx, d_succ_ptr, d_succ_idx;
