@@ -21,6 +21,8 @@ Dispatch points rebound (reference file:line of the call site):
   planner.repair_conflicts       planner.py:259    K2 detection + mover placement
   planner.validate_layout        planner.py:260    K2
   ordering.weight_update_cost    ordering.py:310   event sweep once per (graph, bounds)
+  planner.build_window_problems  planner.py:141-149 interval stabbing on slot positions
+                                                   (windows.py)
   layout.layout_violations / simulator.layout_violations / simulator.peak_memory
 
 Results are bit-identical to the unpatched reference: the plan document bytes
@@ -38,6 +40,7 @@ from pathlib import Path
 from . import evaluator as _ev
 from . import layout as _lay
 from . import ordering as _ord
+from . import windows as _win
 from .graph import GraphError
 
 ROOT = Path(__file__).resolve().parents[1]
@@ -147,7 +150,18 @@ def install(mp=None):
         return orig_pool_map(fn, jobs, workers)
 
     T = functools.partial(_translate, mp)
+    ref_bwp = pl.build_window_problems
+
+    def build_window_problems(g, lin, wu_plan=None, ops_per_step=1, time_budget=60.0, node_cap=None):
+        try:
+            return _win.build_window_problems(g, lin, wu_plan, ops_per_step, time_budget, node_cap,
+                                              window_type=mp.segmentation.Window,
+                                              problem_type=ordm.OrderingProblem)
+        except _win.Unsupported:
+            return ref_bwp(g, lin, wu_plan, ops_per_step, time_budget, node_cap)
+
     patches = {
+        (pl, "build_window_problems"): build_window_problems,
         (ordm, "weight_update_cost"): _weight_update_cost_factory(mp),
         (pl, "peak_memory"): T(_ev.peak_memory),
         (pl, "tensor_lifetimes"): T(_ev.tensor_lifetimes),

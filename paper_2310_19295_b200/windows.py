@@ -1,0 +1,85 @@
+"""Window ordering problems from slot positions -- the batch
+that feeds K4 -- as interval stabbing instead of the reference's per-window
+scan of every tensor (ordering.py:470-542; 94 s of 279 s of ``plan()`` at
+10.8k ops in the reference).
+
+With op_pos[v] the slot of v (its window's slot for window ops, incl. placed
+weight-update branches, ordering.py:489-503), b = op_pos[producer] and
+L = max op_pos over consumers (the horizon ``len(slots)`` without consumers),
+the reference's per-tensor rule for window w at slot p reduces to
+
+    live_in(w)  = { t : b < p <= L }
+    live_out(w) = { t : b <= p <  L }
+
+(b == p exactly when the producer is inside w).  Each window is one vectorised
+pass over the tensors' (b, L) arrays.  Host code: the output is the reference's
+frozensets.  Equality with the reference is tested on every window the planner
+builds (tests/test_plugin_host.py).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .graph import graph_arrays
+
+
+class Unsupported(Exception):
+    """The linearisation lists an op in two windows; use the reference builder."""
+
+
+def window_intervals(g, lin, wu_plan=None):
+    """(final ops per window, slot per window, b[T], L[T], horizon)."""
+    a = graph_arrays(g)
+    n = a.n_ops
+    extra = {w.index: wu_plan.ops_for_window(w.index) for w in lin.windows} if wu_plan else {}
+    op_pos = np.full(n, -1, np.int64)
+    slot_of_window: dict[int, int] = {}
+    for i, (kind, ref) in enumerate(lin.slots):
+        if kind == "op":
+            op_pos[ref] = i
+        elif ref not in slot_of_window:  # _window_slot: first matching slot
+            slot_of_window[ref] = i
+    final_ops: dict[int, tuple[int, ...]] = {}
+    owner = np.full(n, -1, np.int64)
+    for w in lin.windows:
+        ops = tuple(sorted((*w.ops, *extra.get(w.index, ()))))
+        final_ops[w.index] = ops
+        if w.index not in slot_of_window:
+            raise ValueError(f"window {w.index} not in slot sequence")
+        if ops:
+            idx = np.asarray(ops, np.int64)
+            if (owner[idx] >= 0).any() and (owner[idx] != w.index).any():
+                raise Unsupported("op placed in two windows")
+            owner[idx] = w.index
+            op_pos[idx] = slot_of_window[w.index]
+    horizon = len(lin.slots)
+    producer = a.producer.astype(np.int64)
+    if (op_pos[producer] < 0).any() or (a.cons_idx.size and (op_pos[a.cons_idx] < 0).any()):
+        raise KeyError("op without a slot position")
+    b = op_pos[producer]
+    T = a.n_tensors
+    L = np.full(T, horizon, np.int64)
+    counts = np.diff(a.cons_ptr)
+    nz = np.flatnonzero(counts > 0)
+    if nz.size:
+        L[nz] = np.maximum.reduceat(op_pos[a.cons_idx], a.cons_ptr[:-1][nz].astype(np.int64))
+    return final_ops, slot_of_window, b, L, horizon
+
+
+def build_window_problems(g, lin, wu_plan=None, ops_per_step: int = 1, time_budget: float = 60.0,
+                          node_cap=None, *, window_type, problem_type):
+    """ordering.py:470-542 with the reference's own Window / OrderingProblem
+    types passed in; same list, same order, same sets."""
+    final_ops, slot_of_window, b, L, _ = window_intervals(g, lin, wu_plan)
+    out = []
+    for w in lin.windows:
+        p = slot_of_window[w.index]
+        live_in = np.flatnonzero((b < p) & (p <= L))
+        live_out = np.flatnonzero((b <= p) & (p < L))
+        ops = final_ops[w.index]
+        out.append((window_type(index=w.index, leaf=w.leaf, ops=ops),
+                    problem_type(graph=g, ops=ops, live_in=frozenset(live_in.tolist()),
+                                 live_out=frozenset(live_out.tolist()), ops_per_step=ops_per_step,
+                                 time_budget=time_budget, node_cap=node_cap)))
+    return out

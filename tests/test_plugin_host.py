@@ -18,7 +18,7 @@ def test_install_uninstall_roundtrip():
     names = [(mp.planner, n) for n in ("peak_memory", "tensor_lifetimes", "live_bytes_by_timestep",
                                        "_pool_map", "repair_conflicts", "validate_layout")]
     names += [(mp.layout, "layout_violations"), (mp.simulator, "layout_violations"),
-              (mp.ordering, "weight_update_cost"),
+              (mp.ordering, "weight_update_cost"), (mp.planner, "build_window_problems"),
               (mp.simulator, "peak_memory")]
     before = {k: getattr(*k) for k in names}
     plug.install(mp)
@@ -99,3 +99,33 @@ def test_weight_update_cost_sweep_matches_reference(monkeypatch):
         for opt in ("sgd", "adam"):
             mp.planner.plan(rgen.gen_training_graph(arch, 3, optimizer=opt))
     assert len(seen) > 100
+
+
+@pytest.mark.skipif(mp is None, reason="reference memplan not importable")
+def test_window_problems_interval_rule_matches_reference(monkeypatch):
+    """build_window_problems as interval stabbing (windows.py) returns the
+    reference's windows and live-in / live-out sets for every call the planner
+    makes (host code, no GPU)."""
+    import memplan.graphgen as rgen
+
+    from paper_2310_19295_b200 import graphgen as gg
+    from paper_2310_19295_b200 import windows as W
+    orig = mp.planner.build_window_problems
+    n_calls = []
+
+    def both(g, lin, wu_plan=None, ops_per_step=1, time_budget=60.0, node_cap=None):
+        want = orig(g, lin, wu_plan, ops_per_step, time_budget, node_cap)
+        got = W.build_window_problems(g, lin, wu_plan, ops_per_step, time_budget, node_cap,
+                                      window_type=mp.segmentation.Window,
+                                      problem_type=mp.ordering.OrderingProblem)
+        assert got == want
+        n_calls.append(len(want))
+        return want
+
+    monkeypatch.setattr(mp.planner, "build_window_problems", both)
+    for name in ("layered", "gpt2-small"):
+        mp.planner.plan(mp.graph.load_graph(gg.config_doc(name)))
+    for arch in ("mlp", "residual", "transformer_block"):
+        for opt in ("sgd", "adam"):
+            mp.planner.plan(rgen.gen_training_graph(arch, 4, optimizer=opt))
+    assert sum(n_calls) > 20

@@ -40,7 +40,12 @@ def main():
     plug.uninstall()
     rows = []
     for name in a.configs:
-        g = mp.graph.load_graph(gg.config_doc(name))
+        if name.startswith("ref-"):   # the reference's own generator, e.g. ref-transformer_block-600
+            import memplan.graphgen as rgen
+            _, arch, blocks = name.split("-")
+            g = rgen.gen_training_graph(arch, int(blocks))
+        else:
+            g = mp.graph.load_graph(gg.config_doc(name))
         row = {"config": name, "n_ops": len(g.ops), "n_tensors": len(g.tensors)}
         if not a.skip_ref:
             t0 = time.perf_counter()
