@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=3.0, help="wall budget of the CPU baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/cpu)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo lets N ranks share one GPU to exercise the N>1 path (testing only)")
     return ap.parse_args()
 
 
@@ -189,11 +191,20 @@ def main() -> None:
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     dev = torch.device("cuda", local)
+
+    def max_over_ranks(x: float) -> float:
+        t = torch.tensor([x], dtype=torch.float64,
+                         device=dev if args.dist_backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
     B = args.batch or DEFAULT_BATCH[args.config]
     g = graph_for(args.config)
     dg = ev.device_graph(g)
@@ -250,9 +261,7 @@ def main() -> None:
     k1_ms = [ev_s[i].elapsed_time(ev_k1[i]) for i in range(K)]
     tot_ms = sum(step_ms)
     if world > 1:
-        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot_ms = float(t.item())
+        tot_ms = max_over_ranks(tot_ms)
     ms_per_step = tot_ms / K
     value = world * B * K / (tot_ms / 1e3)
     best_host = [int(x) for x in best.cpu().tolist()]
@@ -289,9 +298,7 @@ def main() -> None:
             hbest = tuple(int(x) for x in allgather_best(b).cpu().tolist())
     e2e_s = (time.perf_counter() - t0) / ke
     if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+        e2e_s = max_over_ranks(e2e_s)
     assert tuple(hbest) == tuple(best_host), (hbest, best_host)
 
     cpu = None

@@ -49,8 +49,12 @@ def allgather_best(best, group=None):
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
+    dev = best.device
+    if dist.get_backend(group) == "gloo" and dev.type == "cuda":
+        best = best.cpu()  # gloo gathers host tensors (CPU tests / shared-GPU runs)
     out = torch.empty(world * 2, dtype=torch.int64, device=best.device)
     dist.all_gather_into_tensor(out, best.contiguous(), group=group)
+    out = out.to(dev)
     pk = out.view(world, 2)
     big = torch.full_like(pk[:, 0], NONE_PEAK)
     ids = torch.where(pk[:, 1] < 0, big, pk[:, 1])   # ranks with nothing valid lose
