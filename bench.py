@@ -187,7 +187,8 @@ def main() -> None:
     import torch.distributed as dist
 
     from paper_2310_19295_b200 import evaluator as ev
-    from paper_2310_19295_b200.sharding import allgather_best, shard_range
+    from paper_2310_19295_b200.sharding import (allgather_best, allreduce_key, decode_key, key_bits,
+                                                shard_range)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -222,12 +223,30 @@ def main() -> None:
     gen_ms = g0.elapsed_time(g1)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
 
+    # selection: packed (peak << id_bits) | id key + ONE 8-byte all_reduce(MIN)
+    # when the bits fit (they do for every config graph), else the 16-byte
+    # all_gather of {peak, id}
+    id_bits = key_bits(world * B)
+    use_key = info["total_bytes"] < (1 << (63 - id_bits))
+
+    def select(peak, val):
+        if use_key:
+            key = ev.select_key_device(g, peak, val, first_id, id_bits)  # argmin kernel
+            if world > 1:
+                allreduce_key(key)
+            return key
+        best = ev.select_device(peak, val, first_id)                    # argmin kernel
+        if world > 1:
+            best = allgather_best(best)                                 # 16 B per rank
+        return best
+
+    def to_pair(best) -> list[int]:
+        v = [int(x) for x in best.cpu().tolist()]
+        return list(decode_key(v[0], id_bits)) if use_key else v
+
     def step():
         peak, arg, val = ev.evaluate_orders(g, orders)          # K1
-        best = ev.select_device(peak, val, first_id)             # argmin kernel
-        if world > 1:
-            best = allgather_best(best)                          # 16 B per rank over NCCL
-        return best
+        return select(peak, val)
 
     for _ in range(args.warmup):
         step()
@@ -248,9 +267,7 @@ def main() -> None:
             ev_s[i].record(stream)
             peak, arg, val = ev.evaluate_orders(g, orders)
             ev_k1[i].record(stream)
-            best = ev.select_device(peak, val, first_id)
-            if world > 1:
-                best = allgather_best(best)
+            best = select(peak, val)
             ev_e[i].record(stream)
         torch.cuda.synchronize()
     launches = ev.launch_count() - launches0
@@ -264,7 +281,7 @@ def main() -> None:
         tot_ms = max_over_ranks(tot_ms)
     ms_per_step = tot_ms / K
     value = world * B * K / (tot_ms / 1e3)
-    best_host = [int(x) for x in best.cpu().tolist()]
+    best_host = to_pair(best)
 
     # roofline of K1: algorithmic bytes per launch / average K1 duration
     if info["k1_variant"] == 2:   # opv 8n + mref 4n + packed edges + partner words + sizes
@@ -335,7 +352,9 @@ def main() -> None:
                        "n_ops": n, "n_tensors": info["n_tensors"], "candidates_per_gpu": B,
                        "candidate_ids": f"rank r evaluates [r*{B}, (r+1)*{B})",
                        "l2": "flushed between timed steps (512 MiB write, outside the events)",
-                       "parallelism": f"candidate-sharded dp{world}" + (" + NCCL all_gather argmin" if world > 1 else ""),
+                       "parallelism": f"candidate-sharded dp{world}" + (
+                           (f" + {args.dist_backend} all_reduce(MIN) of a packed (peak, id) key" if use_key
+                            else f" + {args.dist_backend} all_gather of (peak, id)") if world > 1 else ""),
                        "generation_ms": gen_ms},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,

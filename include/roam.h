@@ -125,6 +125,15 @@ int rm_eval_select(RmGraph* g, const int32_t* orders, int64_t B, int64_t id_base
 int rm_argmin(const int64_t* peak, const uint8_t* valid, int64_t B, int64_t id_base,
               uint32_t flags, int64_t* out_best /* [2] */, void* stream);
 
+/* Device-only variant for multi-GPU selection: out_key (device int64[1]) =
+ * (peak << id_bits) | (id + id_base) of the first strict minimum, INT64_MAX
+ * when none is valid.  Ranks then combine with ONE all_reduce(MIN) of 8 bytes:
+ * the packed order equals the lexicographic (peak, id) order.  Fails with
+ * RM_ERR_OVERFLOW unless ids < 2^id_bits and max_peak < 2^(63 - id_bits)
+ * (max_peak: an upper bound of every peak, e.g. the graph's total bytes). */
+int rm_argmin_key(const int64_t* peak, const uint8_t* valid, int64_t B, int64_t id_base,
+                  int32_t id_bits, int64_t max_peak, int64_t* out_key, void* stream);
+
 /* Counter-RNG candidate generator: row c is the Kahn topological order that
  * breaks ties by the smallest (splitmix64(seed ^ splitmix64(id)) ^ op, op)
  * key with id = first_id + c (oracle: oracle/memplan_oracle.py kahn_candidate).

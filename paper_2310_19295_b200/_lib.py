@@ -114,6 +114,7 @@ SIGNATURES = {
     "rm_eval_orders": (C.c_int, [vp, vp, C.c_int64, C.c_uint32, vp, vp, vp, vp]),
     "rm_eval_select": (C.c_int, [vp, vp, C.c_int64, C.c_int64, C.c_uint32, vp, vp, vp, vp, vp]),
     "rm_argmin": (C.c_int, [vp, vp, C.c_int64, C.c_int64, C.c_uint32, vp, vp]),
+    "rm_argmin_key": (C.c_int, [vp, vp, C.c_int64, C.c_int64, C.c_int32, C.c_int64, vp, vp]),
     "rm_gen_orders": (C.c_int, [vp, C.c_uint64, C.c_int64, C.c_int64, vp, vp]),
     "rm_eval_schedule": (C.c_int, [vp, vp, C.c_int64, vp, C.c_int64, C.c_int32, C.c_uint32,
                                    C.POINTER(RmScheduleResult), vp, vp, vp, vp]),

@@ -490,9 +490,11 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
 
 // ---------------------------------------------------------------- argmin
 // Lexicographic min of (peak, id) over valid rows; last-block-done finish.
+// With out_key, also the packed key (peak << id_bits) | id (INT64_MAX when
+// none is valid) so that ranks can combine with one all_reduce(MIN).
 __global__ void k_argmin(const int64_t* __restrict__ peak, const uint8_t* __restrict__ valid,
                          int64_t B, int64_t id_base, long long* partial, unsigned* counter,
-                         int64_t* out) {
+                         int64_t* out, int64_t* out_key, int id_bits) {
   __shared__ long long sv[32], si[32];
   __shared__ bool last;
   long long bv = LLONG_MAX, bi = LLONG_MAX;
@@ -550,8 +552,12 @@ __global__ void k_argmin(const int64_t* __restrict__ peak, const uint8_t* __rest
     }
     wred(bv, bi);
     if (lane == 0) {
-      out[0] = bi == LLONG_MAX ? LLONG_MAX : bv;
-      out[1] = bi == LLONG_MAX ? -1 : bi + id_base;
+      if (out) {
+        out[0] = bi == LLONG_MAX ? LLONG_MAX : bv;
+        out[1] = bi == LLONG_MAX ? -1 : bi + id_base;
+      }
+      if (out_key)
+        out_key[0] = bi == LLONG_MAX ? LLONG_MAX : (bv << id_bits) | (bi + id_base);
     }
   }
 }
@@ -890,7 +896,7 @@ int launch_k1(RmGraph* g, const int32_t* orders_dev, int64_t B, int64_t* peak, i
 }
 
 int launch_argmin(const int64_t* peak_dev, const uint8_t* valid_dev, int64_t B, int64_t id_base,
-                  int64_t* out_dev, cudaStream_t s) {
+                  int64_t* out_dev, cudaStream_t s, int64_t* key_dev = nullptr, int id_bits = 0) {
   Scratch sc(s);
   long long* partial;
   unsigned* counter;
@@ -898,7 +904,8 @@ int launch_argmin(const int64_t* peak_dev, const uint8_t* valid_dev, int64_t B, 
   RM_CUDA(sc.alloc(&partial, 2 * size_t(grid)));
   RM_CUDA(sc.alloc(&counter, 1));
   RM_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), s));
-  k_argmin<<<grid, 1024, 0, s>>>(peak_dev, valid_dev, B, id_base, partial, counter, out_dev);
+  k_argmin<<<grid, 1024, 0, s>>>(peak_dev, valid_dev, B, id_base, partial, counter, out_dev,
+                                 key_dev, id_bits);
   RM_LAUNCH_CHECK("k_argmin launch");
   return RM_OK;
 }
@@ -1064,6 +1071,25 @@ int rm_argmin(const int64_t* peak, const uint8_t* valid, int64_t B, int64_t id_b
   RM_CUDA(cudaMemcpyAsync(out_best, d_out, 16, cudaMemcpyDeviceToHost, s));
   RM_CUDA(cudaStreamSynchronize(s));
   return RM_OK;
+}
+
+int rm_argmin_key(const int64_t* peak, const uint8_t* valid, int64_t B, int64_t id_base,
+                  int32_t id_bits, int64_t max_peak, int64_t* out_key, void* stream) {
+  if (B < 0 || !out_key || (B > 0 && (!peak || !valid)) || id_bits < 1 || id_bits > 62 ||
+      max_peak < 0)
+    return fail(RM_ERR_INVALID_ARG, "bad rm_argmin_key arguments");
+  if ((id_base + B) > (int64_t(1) << id_bits) || id_base < 0)
+    return fail(RM_ERR_OVERFLOW, "candidate ids do not fit id_bits");
+  if (max_peak >= (int64_t(1) << (63 - id_bits)))
+    return fail(RM_ERR_OVERFLOW, "peak bytes do not fit beside the id bits");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (B == 0) {
+    const int64_t none = INT64_MAX;
+    RM_CUDA(cudaMemcpyAsync(out_key, &none, 8, cudaMemcpyHostToDevice, s));
+    RM_CUDA(cudaStreamSynchronize(s));
+    return RM_OK;
+  }
+  return launch_argmin(peak, valid, B, id_base, nullptr, s, out_key, id_bits);
 }
 
 int rm_eval_schedule(RmGraph* g, const int32_t* order, int64_t order_len, const int32_t* timesteps,

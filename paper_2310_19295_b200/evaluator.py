@@ -274,6 +274,18 @@ def select_device(peak, valid, id_base: int = 0, stream=None):
     return out
 
 
+def select_key_device(g, peak, valid, id_base: int, id_bits: int, stream=None):
+    """Device-resident packed key (peak << id_bits) | id of the first strict
+    minimum (INT64_MAX if none valid): one int64 for all_reduce(MIN)."""
+    import torch
+    out = torch.empty(1, dtype=torch.int64, device=peak.device)
+    v = valid.view(torch.uint8) if valid.dtype == torch.bool else valid.to(torch.uint8)
+    check(lib().rm_argmin_key(ptr(peak), ptr(v), peak.shape[0], id_base, id_bits,
+                              device_graph(g).info()["total_bytes"], ptr(out), _stream_handle(stream)),
+          "rm_argmin_key")
+    return out
+
+
 def argmin_orders(peak, valid, id_base: int = 0, stream=None) -> tuple[int, int]:
     """First strict minimum (lexicographic (peak, id)) over valid candidates.
 

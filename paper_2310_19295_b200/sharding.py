@@ -63,6 +63,28 @@ def allgather_best(best, group=None):
     return torch.stack([m, torch.where(idmin == NONE_PEAK, torch.full_like(idmin, -1), idmin)])
 
 
+def key_bits(total_candidates: int) -> int:
+    """id bits of the packed (peak << bits) | id key for ids < total."""
+    return max(1, (max(total_candidates, 1) - 1).bit_length())
+
+
+def allreduce_key(key, group=None):
+    """One all_reduce(MIN) of the 8-byte packed key: the global first strict
+    minimum (lexicographic (peak, id), since ids fit below the peak bits)."""
+    import torch.distributed as dist
+    if dist.get_backend(group) == "gloo" and key.device.type == "cuda":
+        k = key.cpu()
+        dist.all_reduce(k, op=dist.ReduceOp.MIN, group=group)
+        key.copy_(k)
+    else:
+        dist.all_reduce(key, op=dist.ReduceOp.MIN, group=group)
+    return key
+
+
+def decode_key(key: int, bits: int) -> tuple[int, int]:
+    return (NONE_PEAK, -1) if key == NONE_PEAK else (key >> bits, key & ((1 << bits) - 1))
+
+
 @dataclass(frozen=True)
 class ShardResult:
     best_peak: int

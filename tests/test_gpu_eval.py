@@ -189,3 +189,21 @@ def test_unit_shift_and_v2_eligibility():
     peak, arg, val = evaluate_orders(g, np.array([[0, 1], [1, 0]]))
     assert val.tolist() == [True, False]
     assert (int(peak[0]), int(arg[0])) == O.peak_memory(g, (0, 1))
+
+
+def test_packed_key_selection_matches_first_strict_min():
+    import torch
+    from paper_2310_19295_b200.evaluator import select_key_device
+    from paper_2310_19295_b200.sharding import decode_key, key_bits
+    g = load_graph(gg.config_doc("gpt2-small"))
+    orders = generate_orders(g, 3, 0, 700)
+    host = orders.cpu().numpy()
+    host[::7] = host[::7][:, ::-1]                       # invalid rows
+    dev = torch.from_numpy(host).cuda()
+    peak, _, val = evaluate_orders(g, dev)
+    bits = key_bits(1 << 20)
+    key = int(select_key_device(g, peak, val, 1000, bits).item())
+    want = O.first_strict_min(peak.cpu().tolist(), val.cpu().tolist())
+    assert decode_key(key, bits) == (want[0], want[1] + 1000)
+    none = int(select_key_device(g, peak, torch.zeros_like(val), 0, bits).item())
+    assert decode_key(none, bits) == (2**63 - 1, -1)

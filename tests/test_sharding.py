@@ -70,3 +70,37 @@ def test_gloo_world2_argmin_equals_first_strict_min(case):
     want = O.first_strict_min(peaks, valids)
     want = (NONE_PEAK, -1) if want[0] is None else want
     assert res[0] == res[1] == want
+
+
+def _key_worker(rank, world, port, keys, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2310_19295_b200.sharding import allreduce_key
+        k = torch.tensor([keys[rank]], dtype=torch.int64)
+        q.put((rank, int(allreduce_key(k).item())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_packed_key_allreduce():
+    from paper_2310_19295_b200.sharding import decode_key, key_bits
+    bits = key_bits(1_048_576)
+    peaks, valids = [9, 5, 7, 5, 5, 6, 5, 8], [True, False, True, True, True, True, True, True]
+    keys = []
+    for r in range(2):
+        lo, hi = shard_range(len(peaks), 2, r)
+        p, i = lex_min((peaks[j], j) for j in range(lo, hi) if valids[j])
+        keys.append(NONE_PEAK if i < 0 else (p << bits) | i)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_key_worker, args=(r, 2, port, keys, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res[0] == res[1]
+    assert decode_key(res[0], bits) == O.first_strict_min(peaks, valids) == (5, 3)
