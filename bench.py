@@ -284,7 +284,7 @@ def main() -> None:
     best_host = to_pair(best)
 
     # roofline of K1: algorithmic bytes per launch / average K1 duration
-    if info["k1_variant"] == 2:   # opv 8n + mref 4n + packed edges + partner words + sizes
+    if info["k1_variant"] >= 2:   # opv 8n + packed edges + multi-consumer lists + sizes
         meta_bytes = 12 * n + 4 * info["n_check_edges"] + 8 * info["n_multi_cons"] + 8 * info["n_multi"]
     else:
         meta_bytes = (2 * n * (2 if not info["wide_index"] else 4) + 16 * info["n_values"]
@@ -358,7 +358,8 @@ def main() -> None:
                        "generation_ms": gen_ms},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
-                         "kernel": "k1v2_eval_orders" if info["k1_variant"] == 2 else "k1_eval_orders",
+                         "kernel": {3: "k1v3_eval_orders", 2: "k1v2_eval_orders"}.get(info["k1_variant"],
+                                                                                    "k1_eval_orders"),
                          "k1_ms": k1_avg,
                          "alg_bytes_per_launch": alg_bytes,
                          "alg_bytes_formula": "B*(4n+16) + graph metadata",

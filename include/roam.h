@@ -76,7 +76,7 @@ typedef struct {
   int32_t reduced;          /* 1 when the reduction ran */
   int32_t wide_index;       /* 1 when ids need int32 (n > 65535) */
   int64_t total_bytes;      /* sum of |size| */
-  int32_t k1_variant;       /* 2: unit-packed interleaved evaluator, 1: generic */
+  int32_t k1_variant;       /* default K1: 3 pairs, 2 unit-packed interleaved, 1 generic */
   int32_t unit_shift;       /* K1 v2 byte unit = 2^unit_shift */
 } RmGraphInfo;
 
@@ -248,9 +248,10 @@ int64_t rm_launch_count(void);
 /* Device time (ms) of the last rm_eval_orders K1 launch on this thread when
  * timing was requested through rm_set_timing(1); -1 if unavailable. */
 int rm_set_timing(int enable);
-/* Force the K1 evaluator variant on this thread: 0 auto (v2 when the graph
- * qualifies), 1 the generic evaluator, 2 v2 (falls back when unsupported).
- * For tests and A/B measurement. */
+/* Force the K1 evaluator variant on this thread: 0 auto (v3 pairs, else v2,
+ * else generic), 1 the generic evaluator, 2 v2 (one candidate per group),
+ * 3 v3 (two candidates per group); unsupported choices fall back.  For tests
+ * and A/B measurement. */
 int rm_set_k1_variant(int variant);
 double rm_last_kernel_ms(void);
 

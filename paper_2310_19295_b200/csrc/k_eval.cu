@@ -275,6 +275,7 @@ struct K1V2Args {
   int32_t* argmax;
   uint8_t* valid;
   size_t off_edges, off_mpair, off_mptr, off_mcons, off_msz, off_groups, group_bytes, off_xs, off_red;
+  int64_t xs_words;  // int64 words of one candidate's xs (v3 keeps two)
 };
 
 // P3 chunk geometry: C3 = MAXC positions per thread (power of two); the
@@ -484,6 +485,261 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
       a.peak[c] = (int64_t)bv << a.shift;
       a.argmax[c] = bk;
       a.valid[c] = bad ? 0 : 1;
+    }
+  }
+}
+
+// ------------------------------------------------------------- K1 v3
+// Two candidates per group (the default when n < 32767): positions of the
+// pair (A, B) share one 32-bit word per op (A in the low, B in the high
+// half), so every edge check and every multi-consumer lookup is ONE gather
+// for both candidates and the two comparisons run as one SIMD-within-a-word
+// subtraction: with positions < 2^15,
+//   ((pv | 0x80008000) - pu - 0x00010001) keeps bit 15 / bit 31 set
+// exactly when pv > pu in the low / high half (no borrow crosses halves).
+// Per-position work (scatter, readback, out/free units, blocked scan) stays
+// per candidate; barriers and the group scan are shared by the pair.
+template <int NT, int MAXC>
+__global__ void __launch_bounds__(1024, 1) k1v3_eval_orders(const K1V2Args a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = a.n;
+  {
+    auto cp16 = [&](const void* g, size_t off, size_t bytes) {
+      const uint4* src = static_cast<const uint4*>(g);
+      uint4* dst = reinterpret_cast<uint4*>(smem + off);
+      for (size_t i = threadIdx.x; i < bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+    };
+    cp16(a.opv, 0, align16(8 * size_t(n + 1)));
+    cp16(a.edges, a.off_edges, align16(4 * size_t(a.n_edges)));
+    cp16(a.mpair, a.off_mpair, align16(4 * size_t(a.n_pair)));
+    cp16(a.mptr, a.off_mptr, align16(4 * size_t(a.n_gen + 1)));
+    cp16(a.mcons, a.off_mcons, align16(2 * size_t(a.n_mcons)));
+    cp16(a.msz, a.off_msz, align16(4 * size_t(a.n_pair + a.n_gen)));
+  }
+  __syncthreads();
+  const int2* opv = reinterpret_cast<const int2*>(smem);
+  const uint32_t* edges = reinterpret_cast<const uint32_t*>(smem + a.off_edges);
+  const uint32_t* mpair = reinterpret_cast<const uint32_t*>(smem + a.off_mpair);
+  const uint32_t* mptr = reinterpret_cast<const uint32_t*>(smem + a.off_mptr);
+  const uint16_t* mcons = reinterpret_cast<const uint16_t*>(smem + a.off_mcons);
+  const uint32_t* msz = reinterpret_cast<const uint32_t*>(smem + a.off_msz);
+
+  const int gid = threadIdx.x / NT;
+  const int tid = threadIdx.x - gid * NT;
+  if (gid >= a.G) return;
+  const int D = n;
+  const int bar_id = 1 + gid;
+  using X = XsGeom<MAXC>;
+  constexpr int XS_STEP = (NT / X::C3) * X::STRIDE;
+  constexpr int NWARPS = NT / 32;
+  unsigned char* gbase = smem + a.off_groups + size_t(gid) * a.group_bytes;
+  uint32_t* pos2 = reinterpret_cast<uint32_t*>(gbase);        // [n + 3] (A | B << 16)
+  uint16_t* posh = reinterpret_cast<uint16_t*>(gbase);        // halves: 2*o (A), 2*o+1 (B)
+  long long* xsA = reinterpret_cast<long long*>(gbase + a.off_xs);
+  long long* xsB = xsA + size_t(a.xs_words);
+  long long* red_v = reinterpret_cast<long long*>(gbase + a.off_red);  // [2 * NWARPS]
+  int* red_i = reinterpret_cast<int*>(red_v + 2 * NWARPS);              // [2 * NWARPS]
+  unsigned* red_f = reinterpret_cast<unsigned*>(red_i + 2 * NWARPS);    // [NWARPS]
+  const int lane = tid & 31, warp = tid >> 5;
+  const int xw_off = (tid >> X::C3L) * X::STRIDE + (tid & (X::C3 - 1));
+  const int n_edges = a.n_edges, n_pair = a.n_pair, n_gen = a.n_gen;
+  for (int i = tid; i < n; i += NT) pos2[i] = 0;
+  if (tid == 0) {
+    pos2[D + 1] = 0;            // dummy edge (D+1 -> D+2) of the predicated loop
+    pos2[D + 2] = 0x7fff7fffu;  // always passes in both halves
+  }
+  gbar(bar_id, NT);
+  const uint32_t dummy_edge = (uint32_t)(D + 1) | ((uint32_t)(D + 2) << 16);
+
+  const int64_t npairs = (a.B + 1) / 2;
+  const int64_t pstride = int64_t(gridDim.x) * a.G;
+  uint32_t v[MAXC];
+  unsigned pend = 0;  // out-of-range ids seen while loading: bit0 A, bit1 B
+  auto load_pair = [&](int64_t pp) {
+    const int64_t cA = 2 * pp, cB = cA + 1 < a.B ? cA + 1 : cA;
+    const int32_t* rA = a.orders + cA * int64_t(n);
+    const int32_t* rB = a.orders + cB * int64_t(n);
+    pend = 0;
+#pragma unroll
+    for (int j = 0; j < MAXC; ++j) {
+      const int k = tid + j * NT;
+      uint32_t oa = D, ob = D;
+      if (k < n) {
+        const int32_t ra = __ldcs(rA + k), rb = __ldcs(rB + k);
+        const bool ba = (unsigned)ra >= (unsigned)n, bb = (unsigned)rb >= (unsigned)n;
+        pend |= (unsigned)ba | ((unsigned)bb << 1);
+        oa = ba ? D : ra;
+        ob = bb ? D : rb;
+      }
+      v[j] = oa | (ob << 16);
+    }
+  };
+  int64_t pp = int64_t(blockIdx.x) * a.G + gid;
+  if (pp < npairs) load_pair(pp);
+  for (; pp < npairs; pp += pstride) {
+    unsigned bad = pend;
+    // ---- P1: scatter both candidates' positions
+#pragma unroll
+    for (int j = 0; j < MAXC; ++j) {
+      const int k = tid + j * NT;
+      posh[2 * (v[j] & 0xffffu)] = (uint16_t)k;
+      posh[2 * (v[j] >> 16) + 1] = (uint16_t)k;
+    }
+    gbar(bar_id, NT);
+    // ---- P2a: checked edges for both candidates at once
+    uint32_t ok = 0xffffffffu;
+    for (int e0 = tid; e0 < n_edges; e0 += 4 * NT) {
+      uint32_t w[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) w[i] = e0 + i * NT < n_edges ? edges[e0 + i * NT] : dummy_edge;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        ok &= (pos2[w[i] >> 16] | 0x80008000u) - pos2[w[i] & 0xffffu] - 0x00010001u;
+    }
+    bad |= ((~ok >> 15) & 1u) | ((~ok >> 30) & 2u);
+    // ---- P2a: per position: readback, (out, single frees) for A and B
+#pragma unroll
+    for (int j = 0; j < MAXC; ++j) {
+      const int k = tid + j * NT;
+      const unsigned oa = v[j] & 0xffffu, ob = v[j] >> 16;
+      if (k < n) {
+        bad |= ((unsigned)posh[2 * oa] != (unsigned)k) | (((unsigned)posh[2 * ob + 1] != (unsigned)k) << 1);
+        const int2 va = opv[oa], vb = opv[ob];
+        xsA[xw_off + j * XS_STEP] = (long long)(((unsigned long long)(unsigned)va.x << 32) | (unsigned)va.y);
+        xsB[xw_off + j * XS_STEP] = (long long)(((unsigned long long)(unsigned)vb.x << 32) | (unsigned)vb.y);
+      }
+    }
+    const int64_t pn = pp + pstride;
+    const int64_t cA = 2 * pp;
+    const bool hasB = cA + 1 < a.B;
+    if (pn < npairs) load_pair(pn);
+    gbar(bar_id, NT);
+    // ---- P2b: multi-consumer tensors, both candidates per gather
+    auto add_free = [&](long long* xs, unsigned kmax, unsigned units) {
+      if ((int)kmax < n)
+        atomicAdd(reinterpret_cast<unsigned*>(xs + (kmax >> X::C3L) * X::STRIDE + (kmax & (X::C3 - 1))),
+                  units);
+    };
+    for (int m = tid; m < n_pair; m += NT) {
+      const uint32_t w = mpair[m];
+      const uint32_t p1 = pos2[w & 0xffffu], p2 = pos2[w >> 16];
+      const unsigned u = msz[m];
+      add_free(xsA, max(p1 & 0xffffu, p2 & 0xffffu), u);
+      add_free(xsB, max(p1 >> 16, p2 >> 16), u);
+    }
+    for (int m = tid; m < n_gen; m += NT) {
+      const int q0 = mptr[m], q1 = mptr[m + 1];
+      unsigned ka = 0, kb = 0;
+      for (int q = q0; q < q1; ++q) {
+        const uint32_t pq = pos2[mcons[q]];
+        ka = max(ka, pq & 0xffffu);
+        kb = max(kb, pq >> 16);
+      }
+      const unsigned u = msz[n_pair + m];
+      add_free(xsA, ka, u);
+      add_free(xsB, kb, u);
+    }
+    gbar(bar_id, NT);
+    // ---- P3: blocked scans of both candidates' chunks
+    const int k0 = tid << X::C3L;
+    const int mc = n - k0;
+    const long long* xa = xsA + tid * X::STRIDE;
+    const long long* xb = xsB + tid * X::STRIDE;
+    long long runA = 0, bestA = LLONG_MIN, runB = 0, bestB = LLONG_MIN;
+    int biA = INT_MAX, biB = INT_MAX;
+#pragma unroll
+    for (int i = 0; i < X::C3; i += 2) {
+      if (i < mc) {
+        const longlong2 pa = *reinterpret_cast<const longlong2*>(xa + i);
+        const longlong2 pb = *reinterpret_cast<const longlong2*>(xb + i);
+        long long la = runA + (long long)((unsigned long long)pa.x >> 32);
+        long long lb = runB + (long long)((unsigned long long)pb.x >> 32);
+        if (la > bestA) { bestA = la; biA = i; }
+        if (lb > bestB) { bestB = lb; biB = i; }
+        runA = la - (long long)(unsigned)pa.x;
+        runB = lb - (long long)(unsigned)pb.x;
+        if (i + 1 < mc) {
+          la = runA + (long long)((unsigned long long)pa.y >> 32);
+          lb = runB + (long long)((unsigned long long)pb.y >> 32);
+          if (la > bestA) { bestA = la; biA = i + 1; }
+          if (lb > bestB) { bestB = lb; biB = i + 1; }
+          runA = la - (long long)(unsigned)pa.y;
+          runB = lb - (long long)(unsigned)pb.y;
+        }
+      }
+    }
+    long long incA = runA, incB = runB;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const long long ta = __shfl_up_sync(0xffffffffu, incA, d);
+      const long long tb = __shfl_up_sync(0xffffffffu, incB, d);
+      if (lane >= d) {
+        incA += ta;
+        incB += tb;
+      }
+    }
+    const unsigned wbad = __reduce_or_sync(0xffffffffu, bad);
+    if (lane == 31) {
+      red_v[warp] = incA;
+      red_v[NWARPS + warp] = incB;
+    }
+    if (lane == 0) red_f[warp] = wbad;
+    gbar(bar_id, NT);
+    long long offA = incA - runA, offB = incB - runB;
+    unsigned gbad = 0;
+#pragma unroll
+    for (int w = 0; w < NWARPS; ++w) {
+      if (w < warp) {
+        offA += red_v[w];
+        offB += red_v[NWARPS + w];
+      }
+      gbad |= red_f[w];
+    }
+    long long candA = biA == INT_MAX ? LLONG_MIN : offA + bestA;
+    long long candB = biB == INT_MAX ? LLONG_MIN : offB + bestB;
+    int ckA = biA == INT_MAX ? INT_MAX : k0 + biA;
+    int ckB = biB == INT_MAX ? INT_MAX : k0 + biB;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      const long long oa = __shfl_down_sync(0xffffffffu, candA, d);
+      const int ia = __shfl_down_sync(0xffffffffu, ckA, d);
+      const long long ob = __shfl_down_sync(0xffffffffu, candB, d);
+      const int ib = __shfl_down_sync(0xffffffffu, ckB, d);
+      if (oa > candA || (oa == candA && ia < ckA)) {
+        candA = oa;
+        ckA = ia;
+      }
+      if (ob > candB || (ob == candB && ib < ckB)) {
+        candB = ob;
+        ckB = ib;
+      }
+    }
+    gbar(bar_id, NT);
+    if (lane == 0) {
+      red_v[warp] = candA;
+      red_i[warp] = ckA;
+      red_v[NWARPS + warp] = candB;
+      red_i[NWARPS + warp] = ckB;
+    }
+    gbar(bar_id, NT);
+    if (tid < 2 && (tid == 0 || hasB)) {
+      const int base = tid * NWARPS;
+      long long bv = red_v[base];
+      int bk = red_i[base];
+#pragma unroll
+      for (int w = 1; w < NWARPS; ++w)
+        if (red_v[base + w] > bv || (red_v[base + w] == bv && red_i[base + w] < bk)) {
+          bv = red_v[base + w];
+          bk = red_i[base + w];
+        }
+      if (n == 0) {
+        bv = 0;
+        bk = 0;
+      }
+      const int64_t c = cA + tid;
+      a.peak[c] = (int64_t)bv << a.shift;
+      a.argmax[c] = bk;
+      a.valid[c] = ((gbad >> tid) & 1u) ? 0 : 1;
     }
   }
 }
@@ -745,9 +1001,9 @@ static int launch_k1_idx(K1Args& a, int maxc, int grid, size_t smem, cudaStream_
   return fail(RM_ERR_CAPACITY, "K1: positions per thread exceed 64");
 }
 
-template <int NT, int MAXC>
+template <bool PAIRS, int NT, int MAXC>
 static int launch_k1v2_t(K1V2Args& a, int grid, size_t smem, cudaStream_t s) {
-  auto kern = k1v2_eval_orders<NT, MAXC>;
+  auto kern = PAIRS ? k1v3_eval_orders<NT, MAXC> : k1v2_eval_orders<NT, MAXC>;
   RM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (t_timing) {
@@ -756,7 +1012,7 @@ static int launch_k1v2_t(K1V2Args& a, int grid, size_t smem, cudaStream_t s) {
     cudaEventRecord(e0, s);
   }
   kern<<<grid, NT * a.G, smem, s>>>(a);
-  RM_LAUNCH_CHECK("k1v2_eval_orders launch");
+  RM_LAUNCH_CHECK(PAIRS ? "k1v3_eval_orders launch" : "k1v2_eval_orders launch");
   if (t_timing) {
     cudaEventRecord(e1, s);
     cudaEventSynchronize(e1);
@@ -769,12 +1025,27 @@ static int launch_k1v2_t(K1V2Args& a, int grid, size_t smem, cudaStream_t s) {
   return RM_OK;
 }
 
-// K1 v2 geometry: NT threads per group (<= 16 positions per thread in P1/P2),
-// as many groups per CTA as shared memory allows (<= 15 named barriers).
-// Returns 1 when the graph does not fit the v2 layout (caller falls back).
+template <bool PAIRS>
+static int launch_k1v2_nt(K1V2Args& a, int NT, int MAXC, int grid, size_t smem, cudaStream_t s) {
+  switch (NT) {
+    case 64: return MAXC == 4 ? launch_k1v2_t<PAIRS, 64, 4>(a, grid, smem, s)
+                   : MAXC == 8 ? launch_k1v2_t<PAIRS, 64, 8>(a, grid, smem, s)
+                               : launch_k1v2_t<PAIRS, 64, 16>(a, grid, smem, s);
+    case 128: return launch_k1v2_t<PAIRS, 128, 16>(a, grid, smem, s);
+    case 256: return launch_k1v2_t<PAIRS, 256, 16>(a, grid, smem, s);
+    case 512: return launch_k1v2_t<PAIRS, 512, 16>(a, grid, smem, s);
+    default: return launch_k1v2_t<PAIRS, 1024, 16>(a, grid, smem, s);
+  }
+}
+
+// K1 v2/v3 geometry: NT threads per group (<= 16 positions per thread in
+// P1/P2), as many groups per CTA as shared memory allows (<= 15 named
+// barriers).  v3 (pairs) evaluates two candidates per group.  Returns 1 when
+// the graph does not fit the layout (caller falls back).
 static int launch_k1v2(RmGraph* g, const int32_t* orders_dev, int64_t B, int64_t* peak,
-                       int32_t* argmax, uint8_t* valid, cudaStream_t s) {
+                       int32_t* argmax, uint8_t* valid, cudaStream_t s, bool pairs) {
   const int n = g->n;
+  if (pairs && n > 32766) return 1;  // 15-bit positions for the SIMD compare
   K1V2Args a{};
   a.orders = orders_dev;
   a.B = B;
@@ -805,9 +1076,10 @@ static int launch_k1v2(RmGraph* g, const int32_t* orders_dev, int64_t B, int64_t
   a.off_mcons = align16(a.off_mptr + 4 * size_t(a.n_gen + 1));
   a.off_msz = align16(a.off_mcons + 2 * size_t(a.n_mcons));
   a.off_groups = align16(a.off_msz + 4 * size_t(a.n_pair + a.n_gen));
-  a.off_xs = align16(2 * size_t(n + 3));
-  a.off_red = align16(a.off_xs + 8 * size_t((n + C3 - 1) / C3) * stride);
-  a.group_bytes = align16(a.off_red + 32 * 8 + 32 * 4);
+  a.xs_words = int64_t((n + C3 - 1) / C3) * stride;
+  a.off_xs = align16((pairs ? 4 : 2) * size_t(n + 3));
+  a.off_red = align16(a.off_xs + 8 * size_t(a.xs_words) * (pairs ? 2 : 1));
+  a.group_bytes = align16(a.off_red + 64 * 8 + 64 * 4 + 32 * 4);
   int dev = g->device;
   int max_smem = 0;
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
@@ -817,22 +1089,16 @@ static int launch_k1v2(RmGraph* g, const int32_t* orders_dev, int64_t B, int64_t
   G = std::min(G, 15);
   if (G < 1) return 1;
   const int64_t sms = sm_count(dev);
-  if (int64_t(G) * sms > B) G = (int)std::max<int64_t>(1, (B + sms - 1) / sms);
+  const int64_t units = pairs ? (B + 1) / 2 : B;  // what one group evaluates at a time
+  if (int64_t(G) * sms > units) G = (int)std::max<int64_t>(1, (units + sms - 1) / sms);
   a.G = G;
   const size_t smem = a.off_groups + size_t(G) * a.group_bytes;
-  const int grid = (int)std::min<int64_t>(sms, (B + G - 1) / G);
-  switch (NT) {
-    case 64: return MAXC == 4 ? launch_k1v2_t<64, 4>(a, grid, smem, s)
-                   : MAXC == 8 ? launch_k1v2_t<64, 8>(a, grid, smem, s)
-                               : launch_k1v2_t<64, 16>(a, grid, smem, s);
-    case 128: return launch_k1v2_t<128, 16>(a, grid, smem, s);
-    case 256: return launch_k1v2_t<256, 16>(a, grid, smem, s);
-    case 512: return launch_k1v2_t<512, 16>(a, grid, smem, s);
-    default: return launch_k1v2_t<1024, 16>(a, grid, smem, s);
-  }
+  const int grid = (int)std::min<int64_t>(sms, (units + G - 1) / G);
+  return pairs ? launch_k1v2_nt<true>(a, NT, MAXC, grid, smem, s)
+               : launch_k1v2_nt<false>(a, NT, MAXC, grid, smem, s);
 }
 
-static thread_local int t_force_variant = 0;  // 0 auto, 1 generic, 2 v2
+static thread_local int t_force_variant = 0;  // 0 auto, 1 generic, 2 v2, 3 v3 (pairs)
 
 // Launch geometry: NT threads per candidate group, G groups per CTA, one
 // CTA per SM.  Shared memory bounds G; NT keeps ~8-16 positions per thread.
@@ -840,7 +1106,11 @@ int launch_k1(RmGraph* g, const int32_t* orders_dev, int64_t B, int64_t* peak, i
               uint8_t* valid, cudaStream_t s) {
   if (B <= 0) return RM_OK;
   if (g->k2v.ok && t_force_variant != 1) {
-    const int rc = launch_k1v2(g, orders_dev, B, peak, argmax, valid, s);
+    if (t_force_variant != 2) {
+      const int rc = launch_k1v2(g, orders_dev, B, peak, argmax, valid, s, true);
+      if (rc != 1) return rc;
+    }
+    const int rc = launch_k1v2(g, orders_dev, B, peak, argmax, valid, s, false);
     if (rc != 1) return rc;
   }
   const int n = g->n;
@@ -927,7 +1197,7 @@ int rm_set_timing(int enable) {
   return RM_OK;
 }
 int rm_set_k1_variant(int variant) {
-  if (variant < 0 || variant > 2) return fail(RM_ERR_INVALID_ARG, "variant must be 0, 1 or 2");
+  if (variant < 0 || variant > 3) return fail(RM_ERR_INVALID_ARG, "variant must be 0..3");
   t_force_variant = variant;
   return RM_OK;
 }
