@@ -1027,15 +1027,21 @@ static int launch_k1v2_t(K1V2Args& a, int grid, size_t smem, cudaStream_t s) {
 
 template <bool PAIRS>
 static int launch_k1v2_nt(K1V2Args& a, int NT, int MAXC, int grid, size_t smem, cudaStream_t s) {
-  switch (NT) {
-    case 64: return MAXC == 4 ? launch_k1v2_t<PAIRS, 64, 4>(a, grid, smem, s)
-                   : MAXC == 8 ? launch_k1v2_t<PAIRS, 64, 8>(a, grid, smem, s)
-                               : launch_k1v2_t<PAIRS, 64, 16>(a, grid, smem, s);
-    case 128: return launch_k1v2_t<PAIRS, 128, 16>(a, grid, smem, s);
-    case 256: return launch_k1v2_t<PAIRS, 256, 16>(a, grid, smem, s);
-    case 512: return launch_k1v2_t<PAIRS, 512, 16>(a, grid, smem, s);
-    default: return launch_k1v2_t<PAIRS, 1024, 16>(a, grid, smem, s);
-  }
+#define RM_K1V2_CASE(nt, mc) \
+  if (NT == nt && MAXC == mc) return launch_k1v2_t<PAIRS, nt, mc>(a, grid, smem, s);
+  RM_K1V2_CASE(64, 4)
+  RM_K1V2_CASE(64, 8)
+  RM_K1V2_CASE(64, 16)
+  RM_K1V2_CASE(128, 8)
+  RM_K1V2_CASE(128, 16)
+  RM_K1V2_CASE(256, 8)
+  RM_K1V2_CASE(256, 16)
+  RM_K1V2_CASE(512, 8)
+  RM_K1V2_CASE(512, 16)
+  RM_K1V2_CASE(1024, 8)
+  RM_K1V2_CASE(1024, 16)
+#undef RM_K1V2_CASE
+  return 1;
 }
 
 // K1 v2/v3 geometry: NT threads per group (<= 16 positions per thread in
@@ -1064,10 +1070,14 @@ static int launch_k1v2(RmGraph* g, const int32_t* orders_dev, int64_t B, int64_t
   a.peak = peak;
   a.argmax = argmax;
   a.valid = valid;
-  const int NT = n <= 1024 ? 64 : n <= 2048 ? 128 : n <= 4096 ? 256 : n <= 8192 ? 512 : 1024;
+  // <= 16 positions per thread (v2) or <= 8 (v3: a pair's two scans keep
+  // twice the state, and twice the threads per group restores occupancy)
+  const int per = pairs ? 8 : 16;
+  int NT = 64;
+  while (NT < 1024 && NT * per < n) NT *= 2;
   const int C = std::max(1, (n + NT - 1) / NT);
   if (C > 16) return 1;  // > 16384 ops: the generic evaluator
-  const int MAXC = C <= 4 ? 4 : C <= 8 ? 8 : 16;
+  const int MAXC = C <= 4 && NT == 64 ? 4 : C <= 8 ? 8 : 16;
   const int C3 = MAXC;
   const int stride = ((C3 / 2) % 2 == 1) ? C3 : C3 + 2;  // XsGeom<MAXC>::STRIDE
   a.off_edges = align16(8 * size_t(n + 1));
