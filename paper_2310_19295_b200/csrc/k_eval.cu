@@ -1116,7 +1116,11 @@ int launch_k1(RmGraph* g, const int32_t* orders_dev, int64_t B, int64_t* peak, i
               uint8_t* valid, cudaStream_t s) {
   if (B <= 0) return RM_OK;
   if (g->k2v.ok && t_force_variant != 1) {
-    if (t_force_variant != 2) {
+    // v3 (pairs) wins on small graphs; from ~1k ops its doubled per-group
+    // shared memory costs more occupancy than the shared gathers save
+    // (tools/k1_ab.py: layered 1k ops 0.088 vs 0.100 ms; GPT-2 small 0.127 vs
+    // 0.113 ms)
+    if (t_force_variant == 3 || (t_force_variant == 0 && g->n <= 1024)) {
       const int rc = launch_k1v2(g, orders_dev, B, peak, argmax, valid, s, true);
       if (rc != 1) return rc;
     }

@@ -225,7 +225,7 @@ static int build_k1_host(RmGraph& g, bool allow_reduce) {
   build_k1v2_host(g, out, fs);
 
   RmGraphInfo& I = g.info;
-  I.k1_variant = g.k2v.ok ? (g.n <= 32766 ? 3 : 2) : 1;
+  I.k1_variant = g.k2v.ok ? (g.n <= 1024 ? 3 : 2) : 1;
   I.unit_shift = g.k2v.shift;
   I.n_check_edges = (int64_t)g.h_edge_u.size();
   I.n_multi = (int64_t)g.h_msize.size();

@@ -146,7 +146,7 @@ def test_both_k1_variants_vs_c_oracle(name, variant):
     including on corrupted rows (invalid -> valid=False)."""
     from paper_2310_19295_b200.evaluator import device_graph, set_k1_variant
     g = load_graph(gg.config_doc(name))
-    assert device_graph(g).info()["k1_variant"] == 3
+    assert device_graph(g).info()["k1_variant"] == (3 if len(g.ops) <= 1024 else 2)
     B = 1501                                    # odd: the last v3 pair has no partner
     host = generate_orders(g, 7, 0, B).cpu().numpy()
     rng = np.random.default_rng(0)
