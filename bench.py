@@ -298,25 +298,39 @@ def main() -> None:
 
     # end to end through the public API with HOST buffers: H2D of the orders
     # from pinned memory, K1 + argmin, D2H of per-candidate results + best
+    # rows travel as uint16 when the graph has < 65,536 ops (RM_ORDERS_U16):
+    # half the PCIe bytes; the int32 form is measured beside it
     host_orders = torch.empty((B, n), dtype=torch.int32, pin_memory=True)
     host_orders.copy_(orders.cpu())
     host_np = host_orders.numpy()
-    for _ in range(2):
-        ev.evaluate_and_select(g, host_np, id_base=first_id)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    ke = max(3, min(K, 10))
-    t0 = time.perf_counter()
-    for _ in range(ke):
-        hp, ha, hv, hbest = ev.evaluate_and_select(g, host_np, id_base=first_id)
+    u16 = n < 65536
+    host_u16 = torch.empty((B, n), dtype=torch.uint16, pin_memory=True) if u16 else None
+    if u16:
+        host_u16.copy_(orders.to(torch.uint16).cpu())
+
+    def time_e2e(rows):
+        for _ in range(2):
+            ev.evaluate_and_select(g, rows, id_base=first_id)
+        torch.cuda.synchronize()
         if world > 1:
-            b = torch.tensor(hbest, dtype=torch.int64, device=dev)
-            hbest = tuple(int(x) for x in allgather_best(b).cpu().tolist())
-    e2e_s = (time.perf_counter() - t0) / ke
-    if world > 1:
-        e2e_s = max_over_ranks(e2e_s)
-    assert tuple(hbest) == tuple(best_host), (hbest, best_host)
+            dist.barrier()
+        ke = max(3, min(K, 10))
+        t0 = time.perf_counter()
+        for _ in range(ke):
+            out = ev.evaluate_and_select(g, rows, id_base=first_id)
+            hbest = out[3]
+            if world > 1:
+                b = torch.tensor(hbest, dtype=torch.int64, device=dev)
+                hbest = tuple(int(x) for x in allgather_best(b).cpu().tolist())
+        e2e_s = (time.perf_counter() - t0) / ke
+        if world > 1:
+            e2e_s = max_over_ranks(e2e_s)
+        assert tuple(hbest) == tuple(best_host), (hbest, best_host)
+        return e2e_s, out
+
+    e2e32_s, (hp, ha, hv, _) = time_e2e(host_np)
+    e2e_s = time_e2e(host_u16.numpy())[0] if u16 else e2e32_s
+    row_bytes = 2 if u16 else 4
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
@@ -366,9 +380,11 @@ def main() -> None:
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst)" if "_fallback" not in peaks
                          else "fallback 6650 GB/s (B200_PROFILING.md)"},
             "e2e": {"value": world * B / e2e_s, "unit": UNIT,
-                    "h2d_bytes_per_step": B * n * 4,
+                    "h2d_bytes_per_step": B * n * row_bytes,
                     "d2h_bytes_per_step": B * (8 + 4 + 1) + 16,
-                    "api": "evaluate_and_select(g, pinned_host_orders) -> rm_eval_select"},
+                    "api": "evaluate_and_select(g, pinned_host_orders) -> rm_eval_select"
+                           + (" (uint16 rows, RM_ORDERS_U16)" if u16 else " (int32 rows)"),
+                    "int32_rows": {"value": world * B / e2e32_s, "h2d_bytes_per_step": B * n * 4}},
             "gpu_launches": launches,
             "clocks": sampler.summary(),
             "best": {"peak": best_host[0], "id": best_host[1]},

@@ -41,7 +41,9 @@ typedef enum {
 
 enum {
   RM_DEVICE_PTRS = 1u << 0,  /* array arguments are device pointers; async */
-  RM_NO_REDUCE = 1u << 1     /* rm_graph_create: skip transitive reduction */
+  RM_NO_REDUCE = 1u << 1,    /* rm_graph_create: skip transitive reduction */
+  RM_ORDERS_U16 = 1u << 2    /* rm_eval_orders/select: rows are uint16[B, n] (n <= 65535):
+                                half the bytes to stage and to read */
 };
 
 /* ------------------------------------------------------------------ graph */
@@ -107,7 +109,7 @@ int rm_graph_k1_export(const RmGraph* g, int32_t* vidx, int32_t* slot, int64_t* 
  *   argmax[b] = first timestep attaining it.
  * Rows with valid == 0 have unspecified peak/argmax (the reference raises
  * ScheduleError for them).  Replaces graph.py:461 peak_memory in a loop. */
-int rm_eval_orders(RmGraph* g, const int32_t* orders, int64_t B, uint32_t flags,
+int rm_eval_orders(RmGraph* g, const void* orders, int64_t B, uint32_t flags,
                    int64_t* peak, int32_t* argmax, uint8_t* valid, void* stream);
 
 /* rm_eval_orders followed by rm_argmin in one call: the candidate-plan
@@ -115,7 +117,7 @@ int rm_eval_orders(RmGraph* g, const int32_t* orders, int64_t B, uint32_t flags,
  * of the first strict minimum, ids numbered from id_base.  With host
  * pointers the orders are staged through the device in chunks (copy/compute
  * overlap) and every output is back on the host when the call returns. */
-int rm_eval_select(RmGraph* g, const int32_t* orders, int64_t B, int64_t id_base, uint32_t flags,
+int rm_eval_select(RmGraph* g, const void* orders, int64_t B, int64_t id_base, uint32_t flags,
                    int64_t* peak, int32_t* argmax, uint8_t* valid, int64_t* best /* [2] */,
                    void* stream);
 

@@ -21,7 +21,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB_PATH = PKG / "libroam.so"
-SOURCES = ("roam_graph.cpp", "k_eval.cu", "k_gen.cu", "k_layout.cu", "k_pack.cu", "k_greedy.cu")
+SOURCES = ("roam_graph.cpp", "k_eval.cu", "k_eval_v2.cu", "k_gen.cu", "k_layout.cu", "k_pack.cu", "k_greedy.cu")
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 
 
@@ -39,7 +39,7 @@ def _nvcc() -> str:
 def build(force: bool = False, verbose: bool = False) -> Path:
     """Compile every translation unit for sm_100a and link libroam.so."""
     srcs = [CSRC / s for s in SOURCES]
-    deps = srcs + [CSRC / "roam_internal.h", ROOT / "include" / "roam.h"]
+    deps = srcs + [CSRC / "roam_internal.h", CSRC / "k_common.cuh", ROOT / "include" / "roam.h"]
     if not force and LIB_PATH.exists():
         newest = max(p.stat().st_mtime for p in deps)
         if LIB_PATH.stat().st_mtime >= newest:
@@ -101,6 +101,7 @@ class RmScheduleResult(C.Structure):
 
 RM_DEVICE_PTRS = 1
 RM_NO_REDUCE = 2
+RM_ORDERS_U16 = 4
 RM_SCHED_VALIDATE = 1 << 8
 RM_SCHED_PEAK = 1 << 9
 RM_LLFB_PLAIN, RM_LLFB_CONSTRAINED, RM_LLFB_COMPONENTS = 0, 1, 2

@@ -1,0 +1,51 @@
+// Device and host helpers shared by the K1 translation units.
+#pragma once
+
+#include <algorithm>
+#include <climits>
+
+#include "roam_internal.h"
+
+namespace roam {
+
+extern thread_local bool g_timing;     // rm_set_timing
+extern thread_local double g_last_ms;  // rm_last_kernel_ms
+
+__device__ __forceinline__ void gbar(int id, int nt) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nt) : "memory");
+}
+__device__ __forceinline__ int gbar_or(int id, int nt, int pred) {
+  int r;
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.s32 p, %1, 0;\n\t"
+      "bar.red.or.pred q, %2, %3, p;\n\t"
+      "selp.s32 %0, 1, 0, q;\n\t}"
+      : "=r"(r)
+      : "r"(pred), "r"(id), "r"(nt)
+      : "memory");
+  return r;
+}
+
+__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+inline int sm_count(int dev) {
+  static int cached[64] = {0};
+  if (dev < 0 || dev >= 64) return 148;
+  if (!cached[dev]) {
+    int c = 0;
+    cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = c > 0 ? c : 148;
+  }
+  return cached[dev];
+}
+
+
+
+// K1 v2/v3 (k_eval_v2.cu): returns 1 when the graph does not fit the layout
+// (the caller falls back to the generic evaluator).  u16_rows: orders are
+// uint16[B, n] instead of int32[B, n].
+int launch_k1v2(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, int32_t* argmax,
+                uint8_t* valid, cudaStream_t s, bool pairs, bool u16_rows);
+
+}  // namespace roam

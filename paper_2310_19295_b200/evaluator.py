@@ -183,45 +183,75 @@ def peak_memory(g, s: Schedule) -> tuple[int, int]:
 
 # ------------------------------------------------------- candidate batches
 
-def evaluate_orders(g, orders, stream=None):
-    """Batched ``peak_memory(g, sequential_schedule(g, o))`` over rows of orders.
-
-    ``orders``: host array-like int32[B, n_ops] (numpy; staged through the
-    device inside the call) or a CUDA int32 torch tensor (device path, async on
-    ``stream``).  Returns ``(peak int64[B], argmax int32[B], valid bool[B])``
-    of the same kind.  Invalid rows (not a topological permutation) have
-    valid=False and unspecified peak/argmax; the reference raises for them.
-    """
-    dg = device_graph(g)
-    n = dg.n_ops
+def _row_kind(orders):
+    """('dev'|'host', flags) for an orders array: int32 rows, or uint16 rows
+    (RM_ORDERS_U16: half the bytes to stage over PCIe and to read from HBM)."""
     if hasattr(orders, "is_cuda") and orders.is_cuda:
         import torch
-        if orders.dtype != torch.int32 or orders.dim() != 2 or orders.shape[1] != n:
-            raise ValueError(f"orders must be int32[B, {n}]")
-        orders = orders.contiguous()
-        B = orders.shape[0]
-        peak = torch.empty(B, dtype=torch.int64, device=orders.device)
-        arg = torch.empty(B, dtype=torch.int32, device=orders.device)
-        val = torch.empty(B, dtype=torch.uint8, device=orders.device)
-        check(lib().rm_eval_orders(dg.handle, ptr(orders), B, _lib.RM_DEVICE_PTRS, ptr(peak),
-                                   ptr(arg), ptr(val), _stream_handle(stream)), "rm_eval_orders")
-        return peak, arg, val.view(torch.bool)
-    _lib.require_device()
+        if orders.dtype == torch.int32:
+            return "dev", _lib.RM_DEVICE_PTRS
+        if orders.dtype == torch.uint16:
+            return "dev", _lib.RM_DEVICE_PTRS | _lib.RM_ORDERS_U16
+        raise ValueError("device orders must be int32 or uint16")
+    return "host", 0
+
+
+def _device_outputs(orders, B):
+    import torch
+    return (torch.empty(B, dtype=torch.int64, device=orders.device),
+            torch.empty(B, dtype=torch.int32, device=orders.device),
+            torch.empty(B, dtype=torch.uint8, device=orders.device))
+
+
+def _host_rows(orders, n):
+    """Host rows as a C-contiguous int32 or uint16 array (other integer
+    types are checked and converted to int32; out-of-range ids become -1 so
+    the row is reported invalid, as the reference would raise)."""
     if hasattr(orders, "numpy"):
         orders = orders.numpy()
+    o = np.asarray(orders)
+    if o.dtype in (np.int32, np.uint16) and o.ndim == 2 and o.shape[1] == n:
+        return np.ascontiguousarray(o), (_lib.RM_ORDERS_U16 if o.dtype == np.uint16 else 0)
     o = np.ascontiguousarray(np.asarray(orders, dtype=np.int64))
     if o.ndim != 2 or o.shape[1] != n:
         if o.size == 0 and n == 0:
             o = o.reshape(-1, 0)
         else:
-            raise ValueError(f"orders must be int32[B, {n}]")
-    B = o.shape[0]
+            raise ValueError(f"orders must be [B, {n}]")
     oor = (o < 0) | (o >= max(n, 1)) if o.size else np.zeros(o.shape, bool)
-    o32 = np.where(oor, -1, o).astype(np.int32)
+    return np.where(oor, -1, o).astype(np.int32), 0
+
+
+def evaluate_orders(g, orders, stream=None):
+    """Batched ``peak_memory(g, sequential_schedule(g, o))`` over rows of orders.
+
+    ``orders``: [B, n_ops] host array-like (numpy; staged through the device
+    inside the call) or a CUDA torch tensor (device path, async on
+    ``stream``); int32 rows, or uint16 rows for graphs under 65,536 ops.
+    Returns ``(peak int64[B], argmax int32[B], valid bool[B])`` of the same
+    kind.  Invalid rows (not a topological permutation) have valid=False and
+    unspecified peak/argmax; the reference raises for them.
+    """
+    dg = device_graph(g)
+    n = dg.n_ops
+    kind, flags = _row_kind(orders)
+    if kind == "dev":
+        import torch
+        if orders.dim() != 2 or orders.shape[1] != n:
+            raise ValueError(f"orders must be [B, {n}]")
+        orders = orders.contiguous()
+        B = orders.shape[0]
+        peak, arg, val = _device_outputs(orders, B)
+        check(lib().rm_eval_orders(dg.handle, ptr(orders), B, flags, ptr(peak), ptr(arg), ptr(val),
+                                   _stream_handle(stream)), "rm_eval_orders")
+        return peak, arg, val.view(torch.bool)
+    _lib.require_device()
+    o, flags = _host_rows(orders, n)
+    B = o.shape[0]
     peak = np.empty(B, np.int64)
     arg = np.empty(B, np.int32)
     val = np.empty(B, np.uint8)
-    check(lib().rm_eval_orders(dg.handle, ptr(o32), B, 0, ptr(peak), ptr(arg), ptr(val),
+    check(lib().rm_eval_orders(dg.handle, ptr(o), B, flags, ptr(peak), ptr(arg), ptr(val),
                                _stream_handle(stream)), "rm_eval_orders")
     return peak, arg, val.astype(bool)
 
@@ -233,32 +263,26 @@ def evaluate_and_select(g, orders, id_base: int = 0, stream=None):
     inputs (no host sync), a tuple for host inputs."""
     dg = device_graph(g)
     n = dg.n_ops
-    if hasattr(orders, "is_cuda") and orders.is_cuda:
+    kind, flags = _row_kind(orders)
+    if kind == "dev":
         import torch
-        if orders.dtype != torch.int32 or orders.dim() != 2 or orders.shape[1] != n:
-            raise ValueError(f"orders must be int32[B, {n}]")
+        if orders.dim() != 2 or orders.shape[1] != n:
+            raise ValueError(f"orders must be [B, {n}]")
         orders = orders.contiguous()
         B = orders.shape[0]
-        peak = torch.empty(B, dtype=torch.int64, device=orders.device)
-        arg = torch.empty(B, dtype=torch.int32, device=orders.device)
-        val = torch.empty(B, dtype=torch.uint8, device=orders.device)
+        peak, arg, val = _device_outputs(orders, B)
         best = torch.empty(2, dtype=torch.int64, device=orders.device)
-        check(lib().rm_eval_select(dg.handle, ptr(orders), B, id_base, _lib.RM_DEVICE_PTRS, ptr(peak),
-                                   ptr(arg), ptr(val), ptr(best), _stream_handle(stream)),
-              "rm_eval_select")
+        check(lib().rm_eval_select(dg.handle, ptr(orders), B, id_base, flags, ptr(peak), ptr(arg),
+                                   ptr(val), ptr(best), _stream_handle(stream)), "rm_eval_select")
         return peak, arg, val, best
     _lib.require_device()
-    o = orders
-    if not (isinstance(o, np.ndarray) and o.dtype == np.int32 and o.flags.c_contiguous):
-        o = np.ascontiguousarray(np.asarray(o, dtype=np.int32))
-    if o.ndim != 2 or o.shape[1] != n:
-        raise ValueError(f"orders must be int32[B, {n}]")
+    o, flags = _host_rows(orders, n)
     B = o.shape[0]
     peak = np.empty(B, np.int64)
     arg = np.empty(B, np.int32)
     val = np.empty(B, np.uint8)
     best = np.empty(2, np.int64)
-    check(lib().rm_eval_select(dg.handle, ptr(o), B, id_base, 0, ptr(peak), ptr(arg), ptr(val),
+    check(lib().rm_eval_select(dg.handle, ptr(o), B, id_base, flags, ptr(peak), ptr(arg), ptr(val),
                                ptr(best), _stream_handle(stream)), "rm_eval_select")
     return peak, arg, val.astype(bool), (int(best[0]), int(best[1]))
 

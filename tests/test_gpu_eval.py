@@ -207,3 +207,28 @@ def test_packed_key_selection_matches_first_strict_min():
     assert decode_key(key, bits) == (want[0], want[1] + 1000)
     none = int(select_key_device(g, peak, torch.zeros_like(val), 0, bits).item())
     assert decode_key(none, bits) == (2**63 - 1, -1)
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+def test_uint16_rows_match_int32(variant):
+    """uint16 rows (RM_ORDERS_U16) give exactly the int32 results on every
+    evaluator, host-staged and device-resident."""
+    import torch
+    from paper_2310_19295_b200.evaluator import evaluate_and_select, set_k1_variant
+    g = load_graph(gg.config_doc("gpt2-small"))
+    orders = generate_orders(g, 11, 0, 999)
+    host = orders.cpu().numpy()
+    host[::9] = host[::9][:, ::-1]
+    want = coracle.eval_orders(coracle.CGraph(g), host)
+    set_k1_variant(variant)
+    try:
+        for rows in (host.astype(np.uint16), torch.from_numpy(host).cuda().to(torch.uint16)):
+            p, a, v = evaluate_orders(g, rows)
+            p, a, v = (x.cpu().numpy() if hasattr(x, "cpu") else x for x in (p, a, v))
+            assert np.array_equal(v, want[2])
+            assert np.array_equal(p[want[2]], want[0][want[2]]) and np.array_equal(a[want[2]], want[1][want[2]])
+        *_, best = evaluate_and_select(g, host.astype(np.uint16), id_base=5)
+        b = O.first_strict_min(want[0].tolist(), want[2].tolist())
+        assert best == (b[0], b[1] + 5)
+    finally:
+        set_k1_variant(0)
