@@ -631,14 +631,23 @@ static int eval_impl(RmGraph* g, const void* orders, int64_t B, uint32_t flags, 
   const int64_t n = g->n;
   const int64_t esz = u16 ? 2 : 4;
   const int64_t row_bytes = std::max<int64_t>(esz * n, 4);
-  int64_t chunk = std::max<int64_t>(1, (int64_t(64) << 20) / row_bytes);
+  // ~8 MB chunks: the copy engine streams chunk i+1 while K1 runs on chunk i
+  int64_t chunk = std::max<int64_t>(1, (int64_t(8) << 20) / row_bytes);
   chunk = std::min(chunk, std::max<int64_t>(B, 1));
-  cudaStream_t cs;
-  RM_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-  struct Guard {
-    cudaStream_t cs;
-    ~Guard() { cudaStreamDestroy(cs); }
-  } guard{cs};
+  // per-thread copy stream and events, created once (re-entrant: calls on
+  // different threads never share them)
+  struct CopyCtx {
+    int dev = -1;
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  };
+  static thread_local CopyCtx ctx;
+  if (ctx.dev != g->device) {
+    RM_CUDA(cudaStreamCreateWithFlags(&ctx.cs, cudaStreamNonBlocking));
+    for (auto& e : ctx.ev) RM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx.dev = g->device;
+  }
+  cudaStream_t cs = ctx.cs;
   Scratch sc(s);
   unsigned char* d_ord[2];
   int64_t* d_peak;
@@ -651,11 +660,7 @@ static int eval_impl(RmGraph* g, const void* orders, int64_t B, uint32_t flags, 
   RM_CUDA(sc.alloc(&d_val, size_t(B)));
   int64_t* d_best;
   RM_CUDA(sc.alloc(&d_best, 2));
-  cudaEvent_t copied[2], consumed[2];
-  for (int i = 0; i < 2; ++i) {
-    RM_CUDA(cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming));
-    RM_CUDA(cudaEventCreateWithFlags(&consumed[i], cudaEventDisableTiming));
-  }
+  cudaEvent_t copied[2] = {ctx.ev[0], ctx.ev[1]}, consumed[2] = {ctx.ev[2], ctx.ev[3]};
   // the allocations above are ordered on s; the copy stream must see them
   RM_CUDA(cudaEventRecord(consumed[0], s));
   RM_CUDA(cudaEventRecord(consumed[1], s));
@@ -689,10 +694,6 @@ static int eval_impl(RmGraph* g, const void* orders, int64_t B, uint32_t flags, 
   cudaError_t e = cudaStreamSynchronize(s);
   cudaError_t e2 = cudaStreamSynchronize(cs);
   if (e == cudaSuccess) e = e2;
-  for (int i = 0; i < 2; ++i) {
-    cudaEventDestroy(copied[i]);
-    cudaEventDestroy(consumed[i]);
-  }
   if (rc != RM_OK) return rc;
   if (e != cudaSuccess) return cuda_fail(e, "rm_eval_orders");
   return RM_OK;

@@ -393,6 +393,14 @@ int rm_graph_create(const RmGraphDesc* d, uint32_t flags, RmGraph** out) {
     int dev = 0;
     cudaGetDevice(&dev);
     g->device = dev;
+    // keep freed stream-ordered scratch cached in the device's default pool
+    // (every call allocates its scratch with cudaMallocAsync)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
     cudaError_t e = g->info.wide_index ? upload_k1<int32_t>(*g) : upload_k1<uint16_t>(*g);
     if (!e && g->k2v.ok) e = up(g->k2v.opv, g->h2_opv);
     if (!e && g->k2v.ok) e = up(g->k2v.edges, g->h2_edges);
