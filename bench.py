@@ -331,6 +331,19 @@ def main() -> None:
     e2e32_s, (hp, ha, hv, _) = time_e2e(host_np)
     e2e_s = time_e2e(host_u16.numpy())[0] if u16 else e2e32_s
     row_bytes = 2 if u16 else 4
+    # the e2e bound: a plain pinned host -> device copy of the same bytes
+    src = host_u16 if u16 else host_orders
+    dst = torch.empty(src.shape, dtype=src.dtype, device=dev)
+    dst.copy_(src, non_blocking=True)
+    torch.cuda.synchronize()
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0.record()
+    for _ in range(5):
+        dst.copy_(src, non_blocking=True)
+    c1.record()
+    torch.cuda.synchronize()
+    h2d_gbs = 5 * src.numel() * src.element_size() / (c0.elapsed_time(c1) / 1e3) / 1e9
+    del dst
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
@@ -384,7 +397,9 @@ def main() -> None:
                     "d2h_bytes_per_step": B * (8 + 4 + 1) + 16,
                     "api": "evaluate_and_select(g, pinned_host_orders) -> rm_eval_select"
                            + (" (uint16 rows, RM_ORDERS_U16)" if u16 else " (int32 rows)"),
-                    "int32_rows": {"value": world * B / e2e32_s, "h2d_bytes_per_step": B * n * 4}},
+                    "int32_rows": {"value": world * B / e2e32_s, "h2d_bytes_per_step": B * n * 4},
+                    "h2d_gbs_plain_copy": h2d_gbs,
+                    "pcie_bound_value": world * h2d_gbs * 1e9 / (n * row_bytes)},
             "gpu_launches": launches,
             "clocks": sampler.summary(),
             "best": {"peak": best_host[0], "id": best_host[1]},
