@@ -24,6 +24,7 @@ Dispatch points rebound (reference file:line of the call site):
   planner.build_window_problems  planner.py:141-149 interval stabbing on slot positions
                                                    (windows.py)
   layout.layout_violations / simulator.layout_violations / simulator.peak_memory
+  cli.peak_memory / validate_schedule / tensor_lifetimes / validate_layout (memplan eval)
 
 Results are bit-identical to the unpatched reference: the plan document bytes
 (``plan_doc_bytes``) are the parity artefact (tests/test_gpu_plan.py).
@@ -173,6 +174,16 @@ def install(mp=None):
         (sim, "layout_violations"): T(_lay.layout_violations),
         (sim, "peak_memory"): T(_ev.peak_memory),
     }
+    try:  # the CLI binds its own names at import (cli.py:14-40)
+        cli = importlib.import_module(mp.__name__ + ".cli")
+        patches.update({
+            (cli, "peak_memory"): T(_ev.peak_memory),
+            (cli, "validate_schedule"): T(_ev.validate_schedule),
+            (cli, "tensor_lifetimes"): T(_ev.tensor_lifetimes),
+            (cli, "validate_layout"): T(_lay.validate_layout),
+        })
+    except ImportError:
+        pass
     saved = {}
     for (mod, name), fn in patches.items():
         saved[(mod, name)] = getattr(mod, name)

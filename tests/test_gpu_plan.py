@@ -62,3 +62,21 @@ def test_replay_and_compare_through_plugin():
         assert rows
     finally:
         plug.uninstall()
+
+
+@needs_ref
+def test_cli_plan_and_eval_through_plugin(tmp_path):
+    """`python -m paper_2310_19295_b200 plan/eval` = the reference CLI on the
+    GPU path: same plan file bytes, eval exit code 0."""
+    import json
+    from paper_2310_19295_b200.__main__ import main
+    c = golden("plans")["transformer_block-2-adam"]
+    gpath = tmp_path / "g.json"
+    gpath.write_text(json.dumps(c["doc"]))
+    out = tmp_path / "p.json"
+    try:
+        assert main(["plan", "--graph", str(gpath), "--out", str(out)]) == 0
+        assert out.read_text() == c["plan"]
+        assert main(["eval", "--graph", str(gpath), "--plan", str(out)]) == 0
+    finally:
+        plug.uninstall()
