@@ -232,3 +232,53 @@ def test_uint16_rows_match_int32(variant):
         assert best == (b[0], b[1] + 5)
     finally:
         set_k1_variant(0)
+
+
+def _random_doc(rng, n_ops, max_in=3):
+    """Random DAG document with the parity hazards mixed in: duplicate inputs
+    (h1), self-consuming ops (h2), zero-consumer tensors (h3), sizes 0..8 MB."""
+    MB = 1 << 20
+    ops, tensors = [], []
+    for v in range(n_ops):
+        ins = []
+        if tensors:
+            for _ in range(rng.randint(0, max_in)):
+                ins.append(rng.randrange(len(tensors)))
+            if ins and rng.random() < 0.15:
+                ins.append(ins[0])                       # duplicate input
+        outs = []
+        for _ in range(rng.randint(0, 2)):
+            outs.append(len(tensors))
+            tensors.append({"id": len(tensors), "size_bytes": rng.choice([0, 1, 3, 8]) * MB // rng.choice([1, 2])})
+        if outs and rng.random() < 0.1:
+            ins.append(outs[0])                          # self-consuming op
+        ops.append({"id": v, "name": f"op{v}", "kind": "forward", "inputs": ins, "outputs": outs})
+    return {"ops": ops, "tensors": tensors}
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_hazard_graphs_vs_oracle(seed):
+    import random
+    rng = random.Random(seed)
+    for trial in range(25):
+        g = load_graph(_random_doc(rng, rng.randint(1, 60)))
+        n = len(g.ops)
+        preds, succs = O.direct_preds(g), O.direct_succs(g)
+        rows = [O.kahn_candidate(n, preds, succs, seed, c) for c in range(20)]
+        for r in range(5):                               # random permutations: mostly invalid
+            perm = list(range(n))
+            rng.shuffle(perm)
+            rows.append(perm)
+        orders = np.array(rows, np.int64).reshape(len(rows), n)
+        for variant in (0, 1, 2, 3):
+            from paper_2310_19295_b200.evaluator import set_k1_variant
+            set_k1_variant(variant)
+            try:
+                peak, arg, val = evaluate_orders(g, orders)
+            finally:
+                set_k1_variant(0)
+            for k, row in enumerate(rows):
+                want = O.evaluate_order(g, row, preds)
+                assert bool(val[k]) == want[2], (seed, trial, variant, row)
+                if want[2]:
+                    assert (int(peak[k]), int(arg[k])) == want[:2], (seed, trial, variant, row)
