@@ -29,7 +29,7 @@ struct K1V2Args {
   int64_t B;
   int n, G;
   int shift;
-  const int2* opv;
+  const void* opv;  // int2 {fs, out} units per op, zero beyond n
   const uint32_t* edges;
   int n_edges;
   const uint32_t* mpair;
@@ -59,6 +59,11 @@ __device__ __forceinline__ unsigned pos_at(const uint16_t* pos, unsigned i) { re
 template <typename RowT, int NT, int MAXC>
 __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
   extern __shared__ __align__(16) unsigned char smem[];
+  // SLOTS positions per group: the row plus padding slots; padding slot k
+  // holds op id k (zero bytes, its own position), so no slot needs a bounds
+  // predicate.  Ids SLOTS and SLOTS+1 have pinned positions 0 and 0xffff and
+  // form the dummy edge of the predicated edge loop.
+  constexpr int SLOTS = NT * MAXC;
   const int n = a.n;
   const RowT* orders = static_cast<const RowT*>(a.orders);
   // ---- stage the graph metadata once per CTA
@@ -68,7 +73,7 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
       uint4* dst = reinterpret_cast<uint4*>(smem + off);
       for (size_t i = threadIdx.x; i < bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
     };
-    cp16(a.opv, 0, align16(8 * size_t(n + 1)));
+    cp16(a.opv, 0, 8 * size_t(SLOTS));
     cp16(a.edges, a.off_edges, align16(4 * size_t(a.n_edges)));
     cp16(a.mpair, a.off_mpair, align16(4 * size_t(a.n_pair)));
     cp16(a.mptr, a.off_mptr, align16(4 * size_t(a.n_gen + 1)));
@@ -76,7 +81,7 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
     cp16(a.msz, a.off_msz, align16(4 * size_t(a.n_pair + a.n_gen)));
   }
   __syncthreads();
-  const int2* opv = reinterpret_cast<const int2*>(smem);
+  const long long* opv = reinterpret_cast<const long long*>(smem);  // fs | out << 32
   const uint32_t* edges = reinterpret_cast<const uint32_t*>(smem + a.off_edges);
   const uint32_t* mpair = reinterpret_cast<const uint32_t*>(smem + a.off_mpair);
   const uint32_t* mptr = reinterpret_cast<const uint32_t*>(smem + a.off_mptr);
@@ -86,10 +91,9 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
   const int gid = threadIdx.x / NT;
   const int tid = threadIdx.x - gid * NT;
   if (gid >= a.G) return;
-  const int D = n;  // padding op (zero bytes)
   const int bar_id = 1 + gid;
   unsigned char* gbase = smem + a.off_groups + size_t(gid) * a.group_bytes;
-  uint16_t* pos = reinterpret_cast<uint16_t*>(gbase);
+  uint16_t* pos = reinterpret_cast<uint16_t*>(gbase);  // [SLOTS + 2]
   long long* xs = reinterpret_cast<long long*>(gbase + a.off_xs);
   long long* red_v = reinterpret_cast<long long*>(gbase + a.off_red);  // [32]
   int* red_i = reinterpret_cast<int*>(red_v + 32);                      // [32]
@@ -102,72 +106,66 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
   constexpr int XS_STEP = (NT / X::C3) * X::STRIDE;
   long long* xs_w = xs + (tid >> X::C3L) * X::STRIDE + (tid & (X::C3 - 1));
   const int n_edges = a.n_edges, n_pair = a.n_pair, n_gen = a.n_gen;
-  for (int i = tid; i < n; i += NT) pos[i] = 0;  // no stale garbage for P2b
+  for (int i = tid; i < SLOTS; i += NT) pos[i] = 0;  // no stale garbage for P2b
   if (tid == 0) {
-    pos[D + 1] = 0;        // dummy edge (D+1 -> D+2) of the predicated edge loop
-    pos[D + 2] = 0xffffu;  // always passes
+    pos[SLOTS] = 0;
+    pos[SLOTS + 1] = 0xffffu;
   }
   gbar(bar_id, NT);
-  const uint32_t dummy_edge = (uint32_t)(D + 1) | ((uint32_t)(D + 2) << 16);
+  const uint32_t dummy_edge = (uint32_t)SLOTS | ((uint32_t)(SLOTS + 1) << 16);
 
   int32_t v[MAXC];
+  unsigned pend = 0;  // out-of-range ids seen while loading the row
+  auto load_row = [&](int64_t cc) {
+    const RowT* row = orders + cc * int64_t(n);
+    pend = 0;
+#pragma unroll
+    for (int j = 0; j < MAXC; ++j) {
+      const int k = tid + j * NT;
+      if (k < n) {
+        const unsigned r = (unsigned)(int32_t)__ldcs(row + k);
+        pend |= r >= (unsigned)n;
+        v[j] = (int32_t)min(r, (unsigned)(SLOTS - 1));  // an invalid row stays in bounds
+      } else {
+        v[j] = k;
+      }
+    }
+  };
   int64_t c = int64_t(blockIdx.x) * a.G + gid;
-  if (c < a.B) {
-    const RowT* row = orders + c * int64_t(n);
-#pragma unroll
-    for (int j = 0; j < MAXC; ++j) {
-      const int k = tid + j * NT;
-      v[j] = k < n ? (int32_t)__ldcs(row + k) : D;
-    }
-  }
+  if (c < a.B) load_row(c);
   for (; c < a.B; c += cstride) {
-    int bad = 0;
-    // ---- P1: scatter positions (padding slots hold the op D)
+    unsigned bad = pend;
+    // ---- P1: scatter positions
 #pragma unroll
-    for (int j = 0; j < MAXC; ++j) {
-      const int k = tid + j * NT;
-      const bool oor = (unsigned)v[j] >= (unsigned)(k < n ? n : n + 1);
-      bad |= oor;
-      v[j] = oor ? D : v[j];
-      pos[v[j]] = (uint16_t)k;
-    }
+    for (int j = 0; j < MAXC; ++j) pos[v[j]] = (uint16_t)(tid + j * NT);
     gbar(bar_id, NT);
-    // ---- P2a: checked edges, four independent ones per thread per step
+    // ---- P2a: checked edges (pv - pu - 1 < 0 marks a violation; OR keeps the sign)
+    int edge_acc = 0;
     for (int e0 = tid; e0 < n_edges; e0 += 4 * NT) {
       uint32_t w[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) w[i] = e0 + i * NT < n_edges ? edges[e0 + i * NT] : dummy_edge;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) bad |= pos_at(pos, w[i] & 0xffffu) >= pos_at(pos, w[i] >> 16);
+      for (int i = 0; i < 4; ++i)
+        edge_acc |= (int)pos_at(pos, w[i] >> 16) - (int)pos_at(pos, w[i] & 0xffffu) - 1;
     }
-    // ---- P2a: per position: permutation readback, (out, single frees)
+    // ---- P2a: per position: permutation readback, (single frees, out) units
+    unsigned diff = 0;
 #pragma unroll
     for (int j = 0; j < MAXC; ++j) {
-      const int k = tid + j * NT;
       const int o = v[j];
-      bad |= ((int)pos_at(pos, o) != k) & (k < n);
-      const int2 ov = opv[o];
-      if (k < n)
-        xs_w[j * XS_STEP] =
-            (long long)(((unsigned long long)(unsigned)ov.x << 32) | (unsigned)ov.y);
+      diff |= pos_at(pos, o) ^ (unsigned)(tid + j * NT);
+      xs_w[j * XS_STEP] = opv[o];
     }
+    bad |= (diff != 0) | (edge_acc < 0);
     // prefetch the next candidate's row; it lands while P2b / P3 run
     const int64_t cn = c + cstride;
-    if (cn < a.B) {
-      const RowT* row = orders + cn * int64_t(n);
-#pragma unroll
-      for (int j = 0; j < MAXC; ++j) {
-        const int k = tid + j * NT;
-        v[j] = k < n ? (int32_t)__ldcs(row + k) : D;
-      }
-    }
+    if (cn < a.B) load_row(cn);
     gbar(bar_id, NT);
     // ---- P2b: multi-consumer tensors free after their latest maximal consumer
-    // (a kmax >= n can only come from an invalid row's stale positions)
     auto add_free = [&](int kmax, unsigned units) {
-      if (kmax < n)
-        atomicAdd(reinterpret_cast<unsigned*>(xs + (kmax >> X::C3L) * X::STRIDE + (kmax & (X::C3 - 1))),
-                  units);
+      atomicAdd(reinterpret_cast<unsigned*>(xs + (kmax >> X::C3L) * X::STRIDE + (kmax & (X::C3 - 1))),
+                units);
     };
     for (int m = tid; m < n_pair; m += NT) {
       const uint32_t w = mpair[m];
@@ -180,33 +178,29 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
       add_free(kmax, msz[n_pair + m]);
     }
     gbar(bar_id, NT);
-    // ---- P3: blocked scan over this thread's chunk of xs
+    // ---- P3: blocked scan over this thread's full chunk of xs (padding
+    // slots carry zero bytes: they never raise the running max)
     const int k0 = tid << X::C3L;
-    const int mc = n - k0;  // positions of this chunk: min(mc, C3); may be <= 0
     const long long* xr = xs + tid * X::STRIDE;
     long long run = 0, best = LLONG_MIN;
-    int bi = INT_MAX;
+    int bi = 0;
 #pragma unroll
     for (int i = 0; i < X::C3; i += 2) {
-      if (i < mc) {
-        const longlong2 pr = *reinterpret_cast<const longlong2*>(xr + i);
-        long long live = run + (long long)((unsigned long long)pr.x >> 32);
-        if (live > best) {
-          best = live;
-          bi = i;
-        }
-        run = live - (long long)(unsigned)pr.x;
-        if (i + 1 < mc) {
-          live = run + (long long)((unsigned long long)pr.y >> 32);
-          if (live > best) {
-            best = live;
-            bi = i + 1;
-          }
-          run = live - (long long)(unsigned)pr.y;
-        }
+      const longlong2 pr = *reinterpret_cast<const longlong2*>(xr + i);
+      long long live = run + (long long)((unsigned long long)pr.x >> 32);
+      if (live > best) {
+        best = live;
+        bi = i;
       }
+      run = live - (long long)(unsigned)pr.x;
+      live = run + (long long)((unsigned long long)pr.y >> 32);
+      if (live > best) {
+        best = live;
+        bi = i + 1;
+      }
+      run = live - (long long)(unsigned)pr.y;
     }
-    const int bestk = bi == INT_MAX ? INT_MAX : k0 + bi;
+    const int bestk = k0 + bi;
     long long incl = run;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -219,7 +213,7 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
 #pragma unroll
     for (int w = 0; w < NWARPS - 1; ++w)
       if (w < warp) off += red_v[w];
-    long long cand = bestk == INT_MAX ? LLONG_MIN : off + best;
+    long long cand = off + best;
     int ck = bestk;
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
@@ -285,7 +279,7 @@ __global__ void __launch_bounds__(1024, 1) k1v3_eval_orders(const K1V2Args a) {
     cp16(a.msz, a.off_msz, align16(4 * size_t(a.n_pair + a.n_gen)));
   }
   __syncthreads();
-  const int2* opv = reinterpret_cast<const int2*>(smem);
+  const long long* opv = reinterpret_cast<const long long*>(smem);  // fs | out << 32
   const uint32_t* edges = reinterpret_cast<const uint32_t*>(smem + a.off_edges);
   const uint32_t* mpair = reinterpret_cast<const uint32_t*>(smem + a.off_mpair);
   const uint32_t* mptr = reinterpret_cast<const uint32_t*>(smem + a.off_mptr);
@@ -372,9 +366,8 @@ __global__ void __launch_bounds__(1024, 1) k1v3_eval_orders(const K1V2Args a) {
       const unsigned oa = v[j] & 0xffffu, ob = v[j] >> 16;
       if (k < n) {
         bad |= ((unsigned)posh[2 * oa] != (unsigned)k) | (((unsigned)posh[2 * ob + 1] != (unsigned)k) << 1);
-        const int2 va = opv[oa], vb = opv[ob];
-        xsA[xw_off + j * XS_STEP] = (long long)(((unsigned long long)(unsigned)va.x << 32) | (unsigned)va.y);
-        xsB[xw_off + j * XS_STEP] = (long long)(((unsigned long long)(unsigned)vb.x << 32) | (unsigned)vb.y);
+        xsA[xw_off + j * XS_STEP] = opv[oa];  // fs | out << 32
+        xsB[xw_off + j * XS_STEP] = opv[ob];
       }
     }
     const int64_t pn = pp + pstride;
@@ -568,7 +561,7 @@ int launch_k1v2(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, in
   a.B = B;
   a.n = n;
   a.shift = g->k2v.shift;
-  a.opv = g->k2v.opv.as<int2>();
+  a.opv = g->k2v.opv.p;
   a.edges = g->k2v.edges.as<uint32_t>();
   a.n_edges = (int)g->info.n_check_edges;
   a.mpair = g->k2v.mpair.as<uint32_t>();
@@ -591,14 +584,15 @@ int launch_k1v2(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, in
   const int MAXC = C <= 4 && NT == 64 ? 4 : C <= 8 ? 8 : 16;
   const int C3 = MAXC;
   const int stride = ((C3 / 2) % 2 == 1) ? C3 : C3 + 2;  // XsGeom<MAXC>::STRIDE
-  a.off_edges = align16(8 * size_t(n + 1));
+  const size_t slots = size_t(NT) * MAXC;  // v2: row + padding slots (padding slot k = op id k)
+  a.off_edges = align16(8 * (pairs ? size_t(n + 1) : slots));
   a.off_mpair = align16(a.off_edges + 4 * size_t(a.n_edges));
   a.off_mptr = align16(a.off_mpair + 4 * size_t(a.n_pair));
   a.off_mcons = align16(a.off_mptr + 4 * size_t(a.n_gen + 1));
   a.off_msz = align16(a.off_mcons + 2 * size_t(a.n_mcons));
   a.off_groups = align16(a.off_msz + 4 * size_t(a.n_pair + a.n_gen));
-  a.xs_words = int64_t((n + C3 - 1) / C3) * stride;
-  a.off_xs = align16((pairs ? 4 : 2) * size_t(n + 3));
+  a.xs_words = int64_t(pairs ? (n + C3 - 1) / C3 : NT) * stride;
+  a.off_xs = align16(pairs ? 4 * size_t(n + 3) : 2 * (slots + 2));
   a.off_red = align16(a.off_xs + 8 * size_t(a.xs_words) * (pairs ? 2 : 1));
   a.group_bytes = align16(a.off_red + 64 * 8 + 64 * 4 + 32 * 4);
   int dev = g->device;

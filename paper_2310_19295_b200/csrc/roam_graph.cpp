@@ -96,11 +96,13 @@ static void build_k1v2_host(RmGraph& g, const std::vector<int64_t>& out,
   }
   if (shift == 62) shift = 0;
   const int64_t lim = INT32_MAX;
-  g.h2_opv.assign(2 * (size_t(n) + 1), 0);  // + padding op D = n with zero bytes
+  // {fs, out} units per op (one 64-bit word: fs | out << 32), zero-byte
+  // entries beyond n for the evaluators' padding ids (<= max(2n, 1024))
+  g.h2_opv.assign(2 * (size_t(std::max(2 * n, 1024)) + 4), 0);
   for (int v = 0; v < n; ++v) {
     if ((out[v] >> shift) > lim || (fs[v] >> shift) > lim) return;
-    g.h2_opv[2 * v] = (int32_t)(out[v] >> shift);
-    g.h2_opv[2 * v + 1] = (int32_t)(fs[v] >> shift);
+    g.h2_opv[2 * v] = (int32_t)(fs[v] >> shift);
+    g.h2_opv[2 * v + 1] = (int32_t)(out[v] >> shift);
   }
   g.h2_edges.resize(g.h_edge_u.size());
   for (size_t e = 0; e < g.h_edge_u.size(); ++e)
