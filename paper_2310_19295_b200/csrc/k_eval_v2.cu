@@ -574,13 +574,44 @@ int launch_k1v2(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, in
   a.peak = peak;
   a.argmax = argmax;
   a.valid = valid;
-  // <= 16 positions per thread (v2) or <= 8 (v3: a pair's two scans keep
-  // twice the state, and twice the threads per group restores occupancy)
-  const int per = pairs ? 8 : 16;
-  int NT = 64;
-  while (NT < 1024 && NT * per < n) NT *= 2;
+  int dev = g->device;
+  int max_smem = 0;
+  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  // Geometry: NT threads per group, MAXC positions per thread (<= 16; v3 <=
+  // 8, a pair keeps twice the scan state).  Among the NT that fit, take the
+  // one with the most resident warps (groups x NT/32, one CTA per SM, shared
+  // memory and the 1024-thread CTA bound both count), then the most groups.
+  int best_nt = 0, best_warps = -1, best_g = 0;
+  for (int nt = 64; nt <= 1024; nt *= 2) {
+    const int c = std::max(1, (n + nt - 1) / nt);
+    if (c > (pairs ? 8 : 16)) continue;
+    const int mc = c <= 4 && nt == 64 ? 4 : c <= 8 ? 8 : 16;
+    const int st = ((mc / 2) % 2 == 1) ? mc : mc + 2;  // XsGeom<mc>::STRIDE
+    const size_t sl = size_t(nt) * mc;
+    size_t off = align16(8 * (pairs ? size_t(n + 1) : sl));
+    off = align16(off + 4 * size_t(a.n_edges));
+    off = align16(off + 4 * size_t(a.n_pair));
+    off = align16(off + 4 * size_t(a.n_gen + 1));
+    off = align16(off + 2 * size_t(a.n_mcons));
+    off = align16(off + 4 * size_t(a.n_pair + a.n_gen));
+    const size_t xw = size_t(pairs ? (n + mc - 1) / mc : nt) * st;
+    size_t gb = align16(pairs ? 4 * size_t(n + 3) : 2 * (sl + 2));
+    gb = align16(gb + 8 * xw * (pairs ? 2 : 1));
+    gb = align16(gb + 64 * 8 + 64 * 4 + 32 * 4);
+    if (size_t(max_smem) <= off) continue;
+    int gg = (int)((size_t(max_smem) - off) / gb);
+    gg = std::min(gg, std::min(1024 / nt, 15));
+    if (gg < 1) continue;
+    const int warps = gg * nt / 32;
+    if (warps > best_warps || (warps == best_warps && gg > best_g)) {
+      best_nt = nt;
+      best_warps = warps;
+      best_g = gg;
+    }
+  }
+  if (!best_nt) return 1;
+  const int NT = best_nt;
   const int C = std::max(1, (n + NT - 1) / NT);
-  if (C > 16) return 1;  // > 16384 ops: the generic evaluator
   const int MAXC = C <= 4 && NT == 64 ? 4 : C <= 8 ? 8 : 16;
   const int C3 = MAXC;
   const int stride = ((C3 / 2) % 2 == 1) ? C3 : C3 + 2;  // XsGeom<MAXC>::STRIDE
@@ -595,14 +626,7 @@ int launch_k1v2(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, in
   a.off_xs = align16(pairs ? 4 * size_t(n + 3) : 2 * (slots + 2));
   a.off_red = align16(a.off_xs + 8 * size_t(a.xs_words) * (pairs ? 2 : 1));
   a.group_bytes = align16(a.off_red + 64 * 8 + 64 * 4 + 32 * 4);
-  int dev = g->device;
-  int max_smem = 0;
-  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  const size_t avail = max_smem > (int)a.off_groups ? size_t(max_smem) - a.off_groups : 0;
-  int G = (int)(avail / a.group_bytes);
-  G = std::min(G, 1024 / NT);
-  G = std::min(G, 15);
-  if (G < 1) return 1;
+  int G = best_g;
   const int64_t sms = sm_count(dev);
   const int64_t units = pairs ? (B + 1) / 2 : B;  // what one group evaluates at a time
   if (int64_t(G) * sms > units) G = (int)std::max<int64_t>(1, (units + sms - 1) / sms);
