@@ -42,6 +42,7 @@ struct K1V2Args {
   uint8_t* valid;
   size_t off_edges, off_mpair, off_mptr, off_mcons, off_msz, off_groups, group_bytes, off_xs, off_red;
   int64_t xs_words;  // int64 words of one candidate's xs (v3 keeps two)
+  int C;             // v2: rounds of NT positions (ceil(n / NT))
 };
 
 // P3 chunk geometry: C3 = MAXC positions per thread (power of two); the
@@ -59,12 +60,14 @@ __device__ __forceinline__ unsigned pos_at(const uint16_t* pos, unsigned i) { re
 template <typename RowT, int NT, int MAXC>
 __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  // SLOTS positions per group: the row plus padding slots; padding slot k
-  // holds op id k (zero bytes, its own position), so no slot needs a bounds
-  // predicate.  Ids SLOTS and SLOTS+1 have pinned positions 0 and 0xffff and
-  // form the dummy edge of the predicated edge loop.
-  constexpr int SLOTS = NT * MAXC;
+  // SL = C * NT positions per group (C = ceil(n / NT) <= MAXC rounds of NT):
+  // the row plus padding slots; padding slot k holds op id k (zero bytes, its
+  // own position), so no slot needs a bounds predicate -- only the round
+  // index is tested, against the group-uniform C.  Ids SL and SL+1 have
+  // pinned positions 0 and 0xffff and form the dummy edge of the edge loop.
   const int n = a.n;
+  const int C = a.C;
+  const int SL = C * NT;
   const RowT* orders = static_cast<const RowT*>(a.orders);
   // ---- stage the graph metadata once per CTA
   {
@@ -73,7 +76,7 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
       uint4* dst = reinterpret_cast<uint4*>(smem + off);
       for (size_t i = threadIdx.x; i < bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
     };
-    cp16(a.opv, 0, 8 * size_t(SLOTS));
+    cp16(a.opv, 0, align16(8 * size_t(SL)));
     cp16(a.edges, a.off_edges, align16(4 * size_t(a.n_edges)));
     cp16(a.mpair, a.off_mpair, align16(4 * size_t(a.n_pair)));
     cp16(a.mptr, a.off_mptr, align16(4 * size_t(a.n_gen + 1)));
@@ -93,7 +96,7 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
   if (gid >= a.G) return;
   const int bar_id = 1 + gid;
   unsigned char* gbase = smem + a.off_groups + size_t(gid) * a.group_bytes;
-  uint16_t* pos = reinterpret_cast<uint16_t*>(gbase);  // [SLOTS + 2]
+  uint16_t* pos = reinterpret_cast<uint16_t*>(gbase);  // [SL + 2]
   long long* xs = reinterpret_cast<long long*>(gbase + a.off_xs);
   long long* red_v = reinterpret_cast<long long*>(gbase + a.off_red);  // [32]
   int* red_i = reinterpret_cast<int*>(red_v + 32);                      // [32]
@@ -106,13 +109,13 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
   constexpr int XS_STEP = (NT / X::C3) * X::STRIDE;
   long long* xs_w = xs + (tid >> X::C3L) * X::STRIDE + (tid & (X::C3 - 1));
   const int n_edges = a.n_edges, n_pair = a.n_pair, n_gen = a.n_gen;
-  for (int i = tid; i < SLOTS; i += NT) pos[i] = 0;  // no stale garbage for P2b
+  for (int i = tid; i < SL; i += NT) pos[i] = 0;  // no stale garbage for P2b
   if (tid == 0) {
-    pos[SLOTS] = 0;
-    pos[SLOTS + 1] = 0xffffu;
+    pos[SL] = 0;
+    pos[SL + 1] = 0xffffu;
   }
   gbar(bar_id, NT);
-  const uint32_t dummy_edge = (uint32_t)SLOTS | ((uint32_t)(SLOTS + 1) << 16);
+  const uint32_t dummy_edge = (uint32_t)SL | ((uint32_t)(SL + 1) << 16);
 
   int32_t v[MAXC];
   unsigned pend = 0;  // out-of-range ids seen while loading the row
@@ -125,7 +128,7 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
       if (k < n) {
         const unsigned r = (unsigned)(int32_t)__ldcs(row + k);
         pend |= r >= (unsigned)n;
-        v[j] = (int32_t)min(r, (unsigned)(SLOTS - 1));  // an invalid row stays in bounds
+        v[j] = (int32_t)min(r, (unsigned)(SL - 1));  // an invalid row stays in bounds
       } else {
         v[j] = k;
       }
@@ -137,7 +140,8 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
     unsigned bad = pend;
     // ---- P1: scatter positions
 #pragma unroll
-    for (int j = 0; j < MAXC; ++j) pos[v[j]] = (uint16_t)(tid + j * NT);
+    for (int j = 0; j < MAXC; ++j)
+      if (j < C) pos[v[j]] = (uint16_t)(tid + j * NT);
     gbar(bar_id, NT);
     // ---- P2a: checked edges (pv - pu - 1 < 0 marks a violation; OR keeps the sign)
     int edge_acc = 0;
@@ -153,9 +157,11 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
     unsigned diff = 0;
 #pragma unroll
     for (int j = 0; j < MAXC; ++j) {
-      const int o = v[j];
-      diff |= pos_at(pos, o) ^ (unsigned)(tid + j * NT);
-      xs_w[j * XS_STEP] = opv[o];
+      if (j < C) {
+        const int o = v[j];
+        diff |= pos_at(pos, o) ^ (unsigned)(tid + j * NT);
+        xs_w[j * XS_STEP] = opv[o];
+      }
     }
     bad |= (diff != 0) | (edge_acc < 0);
     // prefetch the next candidate's row; it lands while P2b / P3 run
@@ -178,29 +184,32 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
       add_free(kmax, msz[n_pair + m]);
     }
     gbar(bar_id, NT);
-    // ---- P3: blocked scan over this thread's full chunk of xs (padding
-    // slots carry zero bytes: they never raise the running max)
+    // ---- P3: blocked scan over this thread's chunk of xs (padding slots
+    // carry zero bytes: they never raise the running max); threads past the
+    // last chunk hold none
     const int k0 = tid << X::C3L;
     const long long* xr = xs + tid * X::STRIDE;
     long long run = 0, best = LLONG_MIN;
-    int bi = 0;
+    int bi = INT_MAX;
+    if (k0 < SL) {
 #pragma unroll
-    for (int i = 0; i < X::C3; i += 2) {
-      const longlong2 pr = *reinterpret_cast<const longlong2*>(xr + i);
-      long long live = run + (long long)((unsigned long long)pr.x >> 32);
-      if (live > best) {
-        best = live;
-        bi = i;
+      for (int i = 0; i < X::C3; i += 2) {
+        const longlong2 pr = *reinterpret_cast<const longlong2*>(xr + i);
+        long long live = run + (long long)((unsigned long long)pr.x >> 32);
+        if (live > best) {
+          best = live;
+          bi = i;
+        }
+        run = live - (long long)(unsigned)pr.x;
+        live = run + (long long)((unsigned long long)pr.y >> 32);
+        if (live > best) {
+          best = live;
+          bi = i + 1;
+        }
+        run = live - (long long)(unsigned)pr.y;
       }
-      run = live - (long long)(unsigned)pr.x;
-      live = run + (long long)((unsigned long long)pr.y >> 32);
-      if (live > best) {
-        best = live;
-        bi = i + 1;
-      }
-      run = live - (long long)(unsigned)pr.y;
     }
-    const int bestk = k0 + bi;
+    const int bestk = bi == INT_MAX ? INT_MAX : k0 + bi;
     long long incl = run;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -213,7 +222,7 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
 #pragma unroll
     for (int w = 0; w < NWARPS - 1; ++w)
       if (w < warp) off += red_v[w];
-    long long cand = off + best;
+    long long cand = bestk == INT_MAX ? LLONG_MIN : off + best;
     int ck = bestk;
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
@@ -577,56 +586,34 @@ int launch_k1v2(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, in
   int dev = g->device;
   int max_smem = 0;
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  // Geometry: NT threads per group, MAXC positions per thread (<= 16; v3 <=
-  // 8, a pair keeps twice the scan state).  Among the NT that fit, take the
-  // one with the most resident warps (groups x NT/32, one CTA per SM, shared
-  // memory and the 1024-thread CTA bound both count), then the most groups.
-  int best_nt = 0, best_warps = -1, best_g = 0;
-  for (int nt = 64; nt <= 1024; nt *= 2) {
-    const int c = std::max(1, (n + nt - 1) / nt);
-    if (c > (pairs ? 8 : 16)) continue;
-    const int mc = c <= 4 && nt == 64 ? 4 : c <= 8 ? 8 : 16;
-    const int st = ((mc / 2) % 2 == 1) ? mc : mc + 2;  // XsGeom<mc>::STRIDE
-    const size_t sl = size_t(nt) * mc;
-    size_t off = align16(8 * (pairs ? size_t(n + 1) : sl));
-    off = align16(off + 4 * size_t(a.n_edges));
-    off = align16(off + 4 * size_t(a.n_pair));
-    off = align16(off + 4 * size_t(a.n_gen + 1));
-    off = align16(off + 2 * size_t(a.n_mcons));
-    off = align16(off + 4 * size_t(a.n_pair + a.n_gen));
-    const size_t xw = size_t(pairs ? (n + mc - 1) / mc : nt) * st;
-    size_t gb = align16(pairs ? 4 * size_t(n + 3) : 2 * (sl + 2));
-    gb = align16(gb + 8 * xw * (pairs ? 2 : 1));
-    gb = align16(gb + 64 * 8 + 64 * 4 + 32 * 4);
-    if (size_t(max_smem) <= off) continue;
-    int gg = (int)((size_t(max_smem) - off) / gb);
-    gg = std::min(gg, std::min(1024 / nt, 15));
-    if (gg < 1) continue;
-    const int warps = gg * nt / 32;
-    if (warps > best_warps || (warps == best_warps && gg > best_g)) {
-      best_nt = nt;
-      best_warps = warps;
-      best_g = gg;
-    }
-  }
-  if (!best_nt) return 1;
+  // <= 16 positions per thread (v2) or <= 8 (v3: a pair's two scans keep
+  // twice the state, and twice the threads per group restores occupancy)
+  const int per = pairs ? 8 : 16;
+  int best_nt = 64;
+  while (best_nt < 1024 && best_nt * per < n) best_nt *= 2;
   const int NT = best_nt;
   const int C = std::max(1, (n + NT - 1) / NT);
   const int MAXC = C <= 4 && NT == 64 ? 4 : C <= 8 ? 8 : 16;
   const int C3 = MAXC;
   const int stride = ((C3 / 2) % 2 == 1) ? C3 : C3 + 2;  // XsGeom<MAXC>::STRIDE
-  const size_t slots = size_t(NT) * MAXC;  // v2: row + padding slots (padding slot k = op id k)
+  if (C > 16) return 1;  // > 16384 ops: the generic evaluator
+  a.C = C;
+  const size_t slots = size_t(NT) * C;  // v2: row + padding slots (padding slot k = op id k)
   a.off_edges = align16(8 * (pairs ? size_t(n + 1) : slots));
   a.off_mpair = align16(a.off_edges + 4 * size_t(a.n_edges));
   a.off_mptr = align16(a.off_mpair + 4 * size_t(a.n_pair));
   a.off_mcons = align16(a.off_mptr + 4 * size_t(a.n_gen + 1));
   a.off_msz = align16(a.off_mcons + 2 * size_t(a.n_mcons));
   a.off_groups = align16(a.off_msz + 4 * size_t(a.n_pair + a.n_gen));
-  a.xs_words = int64_t(pairs ? (n + C3 - 1) / C3 : NT) * stride;
+  a.xs_words = int64_t(pairs ? (n + C3 - 1) / C3 : (slots + C3 - 1) / C3) * stride;
   a.off_xs = align16(pairs ? 4 * size_t(n + 3) : 2 * (slots + 2));
   a.off_red = align16(a.off_xs + 8 * size_t(a.xs_words) * (pairs ? 2 : 1));
   a.group_bytes = align16(a.off_red + 64 * 8 + 64 * 4 + 32 * 4);
-  int G = best_g;
+  const size_t avail = max_smem > (int)a.off_groups ? size_t(max_smem) - a.off_groups : 0;
+  int G = (int)(avail / a.group_bytes);
+  G = std::min(G, 1024 / NT);
+  G = std::min(G, 15);
+  if (G < 1) return 1;
   const int64_t sms = sm_count(dev);
   const int64_t units = pairs ? (B + 1) / 2 : B;  // what one group evaluates at a time
   if (int64_t(G) * sms > units) G = (int)std::max<int64_t>(1, (units + sms - 1) / sms);
