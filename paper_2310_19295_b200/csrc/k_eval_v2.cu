@@ -587,47 +587,33 @@ int launch_k1v2(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, in
   int max_smem = 0;
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   // <= 16 positions per thread (v2) or <= 8 (v3: a pair's two scans keep
-  // twice the state, and twice the threads per group restores occupancy).
-  // When only one group fits in shared memory, twice the threads per group
-  // doubles the resident warps (measured: GPT2-XL, 7.4k ops).
+  // twice the state, and twice the threads per group restores occupancy)
   const int per = pairs ? 8 : 16;
-  int nt0 = 64;
-  while (nt0 < 1024 && nt0 * per < n) nt0 *= 2;
-  auto layout = [&](int NT, K1V2Args& a) -> int {  // fills a, returns the group count
-    const int C = std::max(1, (n + NT - 1) / NT);
-    if (C > 16) return 0;  // > 16384 ops: the generic evaluator
-    const int MAXC = C <= 4 && NT == 64 ? 4 : C <= 8 ? 8 : 16;
-    const int C3 = MAXC;
-    const int stride = ((C3 / 2) % 2 == 1) ? C3 : C3 + 2;  // XsGeom<MAXC>::STRIDE
-    a.C = C;
-    const size_t slots = size_t(NT) * C;  // v2: row + padding slots (padding slot k = op id k)
-    a.off_edges = align16(8 * (pairs ? size_t(n + 1) : slots));
-    a.off_mpair = align16(a.off_edges + 4 * size_t(a.n_edges));
-    a.off_mptr = align16(a.off_mpair + 4 * size_t(a.n_pair));
-    a.off_mcons = align16(a.off_mptr + 4 * size_t(a.n_gen + 1));
-    a.off_msz = align16(a.off_mcons + 2 * size_t(a.n_mcons));
-    a.off_groups = align16(a.off_msz + 4 * size_t(a.n_pair + a.n_gen));
-    a.xs_words = int64_t(pairs ? (n + C3 - 1) / C3 : (slots + C3 - 1) / C3) * stride;
-    a.off_xs = align16(pairs ? 4 * size_t(n + 3) : 2 * (slots + 2));
-    a.off_red = align16(a.off_xs + 8 * size_t(a.xs_words) * (pairs ? 2 : 1));
-    a.group_bytes = align16(a.off_red + 64 * 8 + 64 * 4 + 32 * 4);
-    if (size_t(max_smem) <= a.off_groups) return 0;
-    const int gg = (int)((size_t(max_smem) - a.off_groups) / a.group_bytes);
-    return std::min(gg, std::min(1024 / NT, 15));
-  };
-  int NT = nt0;
-  int G = layout(NT, a);
-  if (G == 1 && nt0 < 1024) {
-    K1V2Args b2 = a;
-    const int g2 = layout(2 * nt0, b2);
-    if (g2 >= 1) {
-      NT = 2 * nt0;
-      G = g2;
-      a = b2;
-    }
-  }
+  int best_nt = 64;
+  while (best_nt < 1024 && best_nt * per < n) best_nt *= 2;
+  const int NT = best_nt;
+  const int C = std::max(1, (n + NT - 1) / NT);
+  const int MAXC = C <= 4 && NT == 64 ? 4 : C <= 8 ? 8 : 16;
+  const int C3 = MAXC;
+  const int stride = ((C3 / 2) % 2 == 1) ? C3 : C3 + 2;  // XsGeom<MAXC>::STRIDE
+  if (C > 16) return 1;  // > 16384 ops: the generic evaluator
+  a.C = C;
+  const size_t slots = size_t(NT) * C;  // v2: row + padding slots (padding slot k = op id k)
+  a.off_edges = align16(8 * (pairs ? size_t(n + 1) : slots));
+  a.off_mpair = align16(a.off_edges + 4 * size_t(a.n_edges));
+  a.off_mptr = align16(a.off_mpair + 4 * size_t(a.n_pair));
+  a.off_mcons = align16(a.off_mptr + 4 * size_t(a.n_gen + 1));
+  a.off_msz = align16(a.off_mcons + 2 * size_t(a.n_mcons));
+  a.off_groups = align16(a.off_msz + 4 * size_t(a.n_pair + a.n_gen));
+  a.xs_words = int64_t(pairs ? (n + C3 - 1) / C3 : (slots + C3 - 1) / C3) * stride;
+  a.off_xs = align16(pairs ? 4 * size_t(n + 3) : 2 * (slots + 2));
+  a.off_red = align16(a.off_xs + 8 * size_t(a.xs_words) * (pairs ? 2 : 1));
+  a.group_bytes = align16(a.off_red + 64 * 8 + 64 * 4 + 32 * 4);
+  const size_t avail = max_smem > (int)a.off_groups ? size_t(max_smem) - a.off_groups : 0;
+  int G = (int)(avail / a.group_bytes);
+  G = std::min(G, 1024 / NT);
+  G = std::min(G, 15);
   if (G < 1) return 1;
-  const int MAXC = a.C <= 4 && NT == 64 ? 4 : a.C <= 8 ? 8 : 16;
   const int64_t sms = sm_count(dev);
   const int64_t units = pairs ? (B + 1) / 2 : B;  // what one group evaluates at a time
   if (int64_t(G) * sms > units) G = (int)std::max<int64_t>(1, (units + sms - 1) / sms);
