@@ -21,6 +21,11 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   return x ^ (x >> 31);
 }
 
+// Per warp (one candidate at a time): indeg[n], the ready set as op ids
+// ready[] plus the high 32 bits of their keys rk[] (computed once, when an op
+// becomes ready).  Each step selects the minimum (key, op) with warp
+// min-reductions (REDUX) on the key's high word; only ties on it (rare)
+// recompute the full 64-bit keys of the tied ops.
 template <class IdxT>
 __global__ void __launch_bounds__(256) k_gen_orders(int n, uint64_t seed, int64_t first_id, int64_t B,
                                                     const int32_t* __restrict__ pred_ptr,
@@ -29,9 +34,12 @@ __global__ void __launch_bounds__(256) k_gen_orders(int n, uint64_t seed, int64_
                                                     int32_t* __restrict__ out, int warps_per_block) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const size_t per_warp = ((2 * size_t(n) * sizeof(IdxT)) + 15) & ~size_t(15);
-  IdxT* indeg = reinterpret_cast<IdxT*>(smem + per_warp * warp);
-  IdxT* ready = indeg + n;
+  const size_t per_warp = ((size_t(n) * (2 * sizeof(IdxT) + 4)) + 15) & ~size_t(15);
+  unsigned char* wbase = smem + per_warp * warp;
+  uint32_t* rk = reinterpret_cast<uint32_t*>(wbase);          // [n] key high words
+  IdxT* indeg = reinterpret_cast<IdxT*>(rk + n);                // [n]
+  IdxT* ready = indeg + n;                                      // [n]
+  const unsigned lt = (1u << lane) - 1;
   const int64_t stride = int64_t(gridDim.x) * warps_per_block;
   for (int64_t c = int64_t(blockIdx.x) * warps_per_block + warp; c < B; c += stride) {
     const uint64_t h = mix64(seed ^ mix64((uint64_t)(first_id + c)));
@@ -44,39 +52,65 @@ __global__ void __launch_bounds__(256) k_gen_orders(int n, uint64_t seed, int64_
         d = __ldg(pred_ptr + v + 1) - __ldg(pred_ptr + v);
         indeg[v] = (IdxT)d;
       }
-      const unsigned m = __ballot_sync(0xffffffffu, v < n && d == 0);
-      if (v < n && d == 0) ready[nready + __popc(m & ((1u << lane) - 1))] = (IdxT)v;
+      const bool r = v < n && d == 0;
+      const unsigned m = __ballot_sync(0xffffffffu, r);
+      if (r) {
+        const int slot = nready + __popc(m & lt);
+        ready[slot] = (IdxT)v;
+        rk[slot] = (uint32_t)(mix64(h ^ (uint64_t)v) >> 32);
+      }
       nready += __popc(m);
     }
     __syncwarp();
     int keep = 0;
     int step = 0;
     for (; step < n && nready > 0; ++step) {
-      uint64_t bk = ~0ull;
+      // this lane's best among its strided ready entries (high key word, op)
+      uint32_t bk = 0xffffffffu;
       int bv = INT_MAX, bi = -1;
       for (int i = lane; i < nready; i += 32) {
+        const uint32_t k = rk[i];
         const int v = (int)ready[i];
-        const uint64_t k = mix64(h ^ (uint64_t)v);
         if (k < bk || (k == bk && v < bv)) {
           bk = k;
           bv = v;
           bi = i;
         }
       }
-#pragma unroll
-      for (int d = 16; d > 0; d >>= 1) {
-        const uint64_t ok = __shfl_xor_sync(0xffffffffu, bk, d);
-        const int ov = __shfl_xor_sync(0xffffffffu, bv, d);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, d);
-        if (ok < bk || (ok == bk && ov < bv)) {
-          bk = ok;
-          bv = ov;
-          bi = oi;
+      const uint32_t mk = __reduce_min_sync(0xffffffffu, bk);
+      unsigned tied = __ballot_sync(0xffffffffu, bi >= 0 && bk == mk);
+      int win;
+      if (__popc(tied) == 1 && nready <= 32) {
+        win = __ffs(tied) - 1;  // one entry per lane: a unique high word decides
+      } else {
+        // general case: full 64-bit keys of every entry whose high word ties
+        uint64_t fk = ~0ull;
+        int fv = INT_MAX, fi = -1;
+        for (int i = lane; i < nready; i += 32) {
+          if (rk[i] != mk) continue;
+          const int v = (int)ready[i];
+          const uint64_t k = mix64(h ^ (uint64_t)v);
+          if (k < fk || (k == fk && v < fv)) {
+            fk = k;
+            fv = v;
+            fi = i;
+          }
         }
+        const uint32_t mlo = __reduce_min_sync(0xffffffffu, fi >= 0 ? (uint32_t)fk : 0xffffffffu);
+        const unsigned t2 = __ballot_sync(0xffffffffu, fi >= 0 && (uint32_t)fk == mlo);
+        const int mv = (int)__reduce_min_sync(0xffffffffu, (t2 >> lane) & 1u ? (unsigned)fv : 0xffffffffu);
+        const unsigned t3 = __ballot_sync(0xffffffffu, ((t2 >> lane) & 1u) && fv == mv);
+        win = __ffs(t3) - 1;
+        bv = fv;
+        bi = fi;
       }
-      const int v = bv;
+      const int v = __shfl_sync(0xffffffffu, bv, win);
+      const int vi = __shfl_sync(0xffffffffu, bi, win);
       __syncwarp();
-      if (lane == 0) ready[bi] = ready[nready - 1];
+      if (lane == 0) {
+        ready[vi] = ready[nready - 1];
+        rk[vi] = rk[nready - 1];
+      }
       --nready;
       if ((step & 31) == lane) keep = v;
       if ((step & 31) == 31) row[step - 31 + lane] = keep;
@@ -92,7 +126,11 @@ __global__ void __launch_bounds__(256) k_gen_orders(int n, uint64_t seed, int64_
           if (d != 0) w = -1;
         }
         const unsigned m = __ballot_sync(0xffffffffu, w >= 0);
-        if (w >= 0) ready[nready + __popc(m & ((1u << lane) - 1))] = (IdxT)w;
+        if (w >= 0) {
+          const int slot = nready + __popc(m & lt);
+          ready[slot] = (IdxT)w;
+          rk[slot] = (uint32_t)(mix64(h ^ (uint64_t)w) >> 32);
+        }
         nready += __popc(m);
       }
       __syncwarp();
@@ -109,7 +147,7 @@ int launch_gen(RmGraph* g, uint64_t seed, int64_t first_id, int64_t B, int32_t* 
   if (B <= 0) return RM_OK;
   const int n = g->n;
   const bool wide = g->info.wide_index != 0;
-  const size_t per_warp = ((2 * size_t(n) * (wide ? 4 : 2)) + 15) & ~size_t(15);
+  const size_t per_warp = ((size_t(n) * (2 * (wide ? 4 : 2) + 4)) + 15) & ~size_t(15);
   int max_smem = 0;
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device);
   int wpb = (int)std::min<size_t>(8, per_warp ? size_t(max_smem) / per_warp : 8);
