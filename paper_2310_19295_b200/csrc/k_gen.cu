@@ -27,7 +27,7 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
 // min-reductions (REDUX) on the key's high word; only ties on it (rare)
 // recompute the full 64-bit keys of the tied ops.
 template <class IdxT>
-__global__ void __launch_bounds__(256) k_gen_orders(int n, uint64_t seed, int64_t first_id, int64_t B,
+__global__ void __launch_bounds__(1024) k_gen_orders(int n, uint64_t seed, int64_t first_id, int64_t B,
                                                     const int32_t* __restrict__ pred_ptr,
                                                     const int32_t* __restrict__ succ_ptr,
                                                     const int32_t* __restrict__ succ_idx,
@@ -68,9 +68,11 @@ __global__ void __launch_bounds__(256) k_gen_orders(int n, uint64_t seed, int64_
       // this lane's best among its strided ready entries (high key word, op)
       uint32_t bk = 0xffffffffu;
       int bv = INT_MAX, bi = -1;
+      bool dup = false;  // two of this lane's entries share the best high word
       for (int i = lane; i < nready; i += 32) {
         const uint32_t k = rk[i];
         const int v = (int)ready[i];
+        dup = k < bk ? false : (dup || k == bk);
         if (k < bk || (k == bk && v < bv)) {
           bk = k;
           bv = v;
@@ -78,10 +80,11 @@ __global__ void __launch_bounds__(256) k_gen_orders(int n, uint64_t seed, int64_
         }
       }
       const uint32_t mk = __reduce_min_sync(0xffffffffu, bk);
-      unsigned tied = __ballot_sync(0xffffffffu, bi >= 0 && bk == mk);
+      const unsigned tied = __ballot_sync(0xffffffffu, bi >= 0 && bk == mk);
+      const unsigned dups = __ballot_sync(0xffffffffu, bi >= 0 && bk == mk && dup);
       int win;
-      if (__popc(tied) == 1 && nready <= 32) {
-        win = __ffs(tied) - 1;  // one entry per lane: a unique high word decides
+      if (__popc(tied) == 1 && !dups) {
+        win = __ffs(tied) - 1;  // a unique minimal high word decides
       } else {
         // general case: full 64-bit keys of every entry whose high word ties
         uint64_t fk = ~0ull;
@@ -150,7 +153,7 @@ int launch_gen(RmGraph* g, uint64_t seed, int64_t first_id, int64_t B, int32_t* 
   const size_t per_warp = ((size_t(n) * (2 * (wide ? 4 : 2) + 4)) + 15) & ~size_t(15);
   int max_smem = 0;
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device);
-  int wpb = (int)std::min<size_t>(8, per_warp ? size_t(max_smem) / per_warp : 8);
+  int wpb = (int)std::min<size_t>(32, per_warp ? size_t(max_smem) / per_warp : 32);
   if (wpb < 1) return fail(RM_ERR_CAPACITY, "generator: graph too large for shared memory");
   const size_t smem = per_warp * wpb;
   int sms = 148;

@@ -48,6 +48,16 @@ def main():
             print(json.dumps({"graph": name, "n": n, "B": B, "variant": variant, "ms": ms,
                               "gbs": B * (4 * n + 16) / ms / 1e6, "same_as_v1": same}), flush=True)
         ev.set_k1_variant(0)
+        ev.generate_orders(g, 1, 0, 1024)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        ev.generate_orders(g, 2, 0, B)
+        e1.record()
+        torch.cuda.synchronize()
+        gms = e0.elapsed_time(e1)
+        print(json.dumps({"graph": name, "n": n, "B": B, "generator_ms": gms,
+                          "generated_per_s": B / gms * 1e3}), flush=True)
 
 
 if __name__ == "__main__":
