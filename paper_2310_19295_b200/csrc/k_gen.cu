@@ -27,15 +27,28 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
 // min-reductions (REDUX) on the key's high word; only ties on it (rare)
 // recompute the full 64-bit keys of the tied ops.
 template <class IdxT>
-__global__ void __launch_bounds__(1024) k_gen_orders(int n, uint64_t seed, int64_t first_id, int64_t B,
-                                                    const int32_t* __restrict__ pred_ptr,
-                                                    const int32_t* __restrict__ succ_ptr,
-                                                    const int32_t* __restrict__ succ_idx,
-                                                    int32_t* __restrict__ out, int warps_per_block) {
+__global__ void __launch_bounds__(1024) k_gen_orders(int n, int n_succ, uint64_t seed, int64_t first_id,
+                                                     int64_t B, const int32_t* __restrict__ pred_ptr,
+                                                     const int32_t* __restrict__ succ_ptr,
+                                                     const int32_t* __restrict__ succ_idx,
+                                                     int32_t* __restrict__ out, int warps_per_block,
+                                                     size_t meta_bytes) {
   extern __shared__ __align__(16) unsigned char smem[];
+  // CTA-shared graph: initial in-degrees and the successor CSR (each Kahn
+  // step reads them on its critical path: shared memory, not L2)
+  IdxT* s_indeg0 = reinterpret_cast<IdxT*>(smem);
+  IdxT* s_sptr = s_indeg0 + n;          // [n + 1]
+  IdxT* s_sidx = s_sptr + (n + 1);      // [n_succ]
+  for (int v = threadIdx.x; v < n; v += blockDim.x) {
+    s_indeg0[v] = (IdxT)(__ldg(pred_ptr + v + 1) - __ldg(pred_ptr + v));
+    s_sptr[v] = (IdxT)__ldg(succ_ptr + v);
+  }
+  if (threadIdx.x == 0) s_sptr[n] = (IdxT)__ldg(succ_ptr + n);
+  for (int k = threadIdx.x; k < n_succ; k += blockDim.x) s_sidx[k] = (IdxT)__ldg(succ_idx + k);
+  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t per_warp = ((size_t(n) * (2 * sizeof(IdxT) + 4)) + 15) & ~size_t(15);
-  unsigned char* wbase = smem + per_warp * warp;
+  unsigned char* wbase = smem + meta_bytes + per_warp * warp;
   uint32_t* rk = reinterpret_cast<uint32_t*>(wbase);          // [n] key high words
   IdxT* indeg = reinterpret_cast<IdxT*>(rk + n);                // [n]
   IdxT* ready = indeg + n;                                      // [n]
@@ -49,7 +62,7 @@ __global__ void __launch_bounds__(1024) k_gen_orders(int n, uint64_t seed, int64
       const int v = base + lane;
       int d = 1;
       if (v < n) {
-        d = __ldg(pred_ptr + v + 1) - __ldg(pred_ptr + v);
+        d = (int)s_indeg0[v];
         indeg[v] = (IdxT)d;
       }
       const bool r = v < n && d == 0;
@@ -117,13 +130,13 @@ __global__ void __launch_bounds__(1024) k_gen_orders(int n, uint64_t seed, int64
       --nready;
       if ((step & 31) == lane) keep = v;
       if ((step & 31) == 31) row[step - 31 + lane] = keep;
-      const int s0 = __ldg(succ_ptr + v), s1 = __ldg(succ_ptr + v + 1);
+      const int s0 = (int)s_sptr[v], s1 = (int)s_sptr[v + 1];
       __syncwarp();
       for (int k0 = s0; k0 < s1; k0 += 32) {
         const int k = k0 + lane;
         int w = -1;
         if (k < s1) {
-          w = __ldg(succ_idx + k);
+          w = (int)s_sidx[k];
           const int d = (int)indeg[w] - 1;
           indeg[w] = (IdxT)d;
           if (d != 0) w = -1;
@@ -149,29 +162,34 @@ __global__ void __launch_bounds__(1024) k_gen_orders(int n, uint64_t seed, int64
 int launch_gen(RmGraph* g, uint64_t seed, int64_t first_id, int64_t B, int32_t* out, cudaStream_t s) {
   if (B <= 0) return RM_OK;
   const int n = g->n;
-  const bool wide = g->info.wide_index != 0;
-  const size_t per_warp = ((size_t(n) * (2 * (wide ? 4 : 2) + 4)) + 15) & ~size_t(15);
+  const int n_succ = (int)g->succ_idx.size();
+  // u16 ids and successor offsets when both fit
+  const bool wide = n > 65535 || n_succ > 65535;
+  const size_t isz = wide ? 4 : 2;
+  const size_t meta = ((isz * (size_t(n) * 2 + 1 + size_t(n_succ))) + 15) & ~size_t(15);
+  const size_t per_warp = ((size_t(n) * (2 * isz + 4)) + 15) & ~size_t(15);
   int max_smem = 0;
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device);
-  int wpb = (int)std::min<size_t>(32, per_warp ? size_t(max_smem) / per_warp : 32);
-  if (wpb < 1) return fail(RM_ERR_CAPACITY, "generator: graph too large for shared memory");
-  const size_t smem = per_warp * wpb;
+  if (size_t(max_smem) < meta + per_warp)
+    return fail(RM_ERR_CAPACITY, "generator: graph too large for shared memory");
+  const int wpb = (int)std::min<size_t>(32, (size_t(max_smem) - meta) / per_warp);
+  const size_t smem = meta + per_warp * wpb;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
   const int64_t blocks_needed = (B + wpb - 1) / wpb;
-  const int grid = (int)std::min<int64_t>(blocks_needed, int64_t(sms) * 8);
+  const int grid = (int)std::min<int64_t>(blocks_needed, int64_t(sms));
   if (wide) {
     RM_CUDA(cudaFuncSetAttribute(k_gen_orders<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
     k_gen_orders<int32_t><<<grid, 32 * wpb, smem, s>>>(
-        n, seed, first_id, B, g->d_pred_ptr.as<int32_t>(), g->d_succ_ptr.as<int32_t>(),
-        g->d_succ_idx.as<int32_t>(), out, wpb);
+        n, n_succ, seed, first_id, B, g->d_pred_ptr.as<int32_t>(), g->d_succ_ptr.as<int32_t>(),
+        g->d_succ_idx.as<int32_t>(), out, wpb, meta);
   } else {
     RM_CUDA(cudaFuncSetAttribute(k_gen_orders<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
     k_gen_orders<uint16_t><<<grid, 32 * wpb, smem, s>>>(
-        n, seed, first_id, B, g->d_pred_ptr.as<int32_t>(), g->d_succ_ptr.as<int32_t>(),
-        g->d_succ_idx.as<int32_t>(), out, wpb);
+        n, n_succ, seed, first_id, B, g->d_pred_ptr.as<int32_t>(), g->d_succ_ptr.as<int32_t>(),
+        g->d_succ_idx.as<int32_t>(), out, wpb, meta);
   }
   RM_LAUNCH_CHECK("k_gen_orders launch");
   return RM_OK;
