@@ -118,30 +118,32 @@ __global__ void __launch_bounds__(1024, 1) k1v2_eval_orders(const K1V2Args a) {
   const uint32_t dummy_edge = (uint32_t)SL | ((uint32_t)(SL + 1) << 16);
 
   int32_t v[MAXC];
-  unsigned pend = 0;  // out-of-range ids seen while loading the row
+  // the raw row goes straight into registers; nothing reads it until the
+  // next P1, so the loads stay in flight behind P2b / P3
   auto load_row = [&](int64_t cc) {
     const RowT* row = orders + cc * int64_t(n);
-    pend = 0;
 #pragma unroll
     for (int j = 0; j < MAXC; ++j) {
       const int k = tid + j * NT;
-      if (k < n) {
-        const unsigned r = (unsigned)(int32_t)__ldcs(row + k);
-        pend |= r >= (unsigned)n;
-        v[j] = (int32_t)min(r, (unsigned)(SL - 1));  // an invalid row stays in bounds
-      } else {
-        v[j] = k;
-      }
+      v[j] = k < n ? (int32_t)__ldcs(row + k) : k;
     }
   };
   int64_t c = int64_t(blockIdx.x) * a.G + gid;
   if (c < a.B) load_row(c);
   for (; c < a.B; c += cstride) {
-    unsigned bad = pend;
-    // ---- P1: scatter positions
+    unsigned bad = 0;
+    // ---- P1: range check (an out-of-range id is clamped so the row stays in
+    // bounds, and flagged), scatter positions
 #pragma unroll
-    for (int j = 0; j < MAXC; ++j)
-      if (j < C) pos[v[j]] = (uint16_t)(tid + j * NT);
+    for (int j = 0; j < MAXC; ++j) {
+      if (j < C) {
+        const int k = tid + j * NT;
+        const unsigned r = (unsigned)v[j];
+        bad |= (r >= (unsigned)n) & (k < n);
+        v[j] = (int32_t)min(r, (unsigned)(SL - 1));
+        pos[v[j]] = (uint16_t)k;
+      }
+    }
     gbar(bar_id, NT);
     // ---- P2a: checked edges (pv - pu - 1 < 0 marks a violation; OR keeps the sign)
     int edge_acc = 0;
