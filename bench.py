@@ -385,7 +385,8 @@ def main() -> None:
                        "generation_ms": gen_ms},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
-                         "kernel": {3: "k1v3_eval_orders", 2: "k1v2_eval_orders"}.get(info["k1_variant"],
+                         "kernel": {4: "k1v4_eval_orders", 3: "k1v3_eval_orders",
+                                    2: "k1v2_eval_orders"}.get(info["k1_variant"],
                                                                                     "k1_eval_orders"),
                          "k1_ms": k1_avg,
                          "alg_bytes_per_launch": alg_bytes,

@@ -78,7 +78,7 @@ typedef struct {
   int32_t reduced;          /* 1 when the reduction ran */
   int32_t wide_index;       /* 1 when ids need int32 (n > 65535) */
   int64_t total_bytes;      /* sum of |size| */
-  int32_t k1_variant;       /* default K1: 3 pairs, 2 unit-packed interleaved, 1 generic */
+  int32_t k1_variant;       /* default K1: 4 v4, 3 pairs, 2 unit-packed interleaved, 1 generic */
   int32_t unit_shift;       /* K1 v2 byte unit = 2^unit_shift */
 } RmGraphInfo;
 
@@ -250,10 +250,11 @@ int64_t rm_launch_count(void);
 /* Device time (ms) of the last rm_eval_orders K1 launch on this thread when
  * timing was requested through rm_set_timing(1); -1 if unavailable. */
 int rm_set_timing(int enable);
-/* Force the K1 evaluator variant on this thread: 0 auto (v3 pairs, else v2,
- * else generic), 1 the generic evaluator, 2 v2 (one candidate per group),
- * 3 v3 (two candidates per group); unsupported choices fall back.  For tests
- * and A/B measurement. */
+/* Force the K1 evaluator variant on this thread: 0 auto (v4, else v3 pairs /
+ * v2, else generic), 1 the generic evaluator, 2 v2 (one candidate per group),
+ * 3 v3 (two candidates per group), 4 v4 (sentinel permutation check, SIMD
+ * edge checks); unsupported choices fall back.  For tests and A/B
+ * measurement. */
 int rm_set_k1_variant(int variant);
 double rm_last_kernel_ms(void);
 

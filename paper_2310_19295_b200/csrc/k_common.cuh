@@ -48,4 +48,8 @@ inline int sm_count(int dev) {
 int launch_k1v2(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, int32_t* argmax,
                 uint8_t* valid, cudaStream_t s, bool pairs, bool u16_rows);
 
+// K1 v4 (k_eval_v4.cu): same contract; returns 1 when g->k4v.ok == 0.
+int launch_k1v4(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, int32_t* argmax,
+                uint8_t* valid, cudaStream_t s, bool u16_rows);
+
 }  // namespace roam

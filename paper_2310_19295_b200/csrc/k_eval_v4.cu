@@ -1,0 +1,372 @@
+// K1 v4: the default candidate-order evaluator.
+//
+// Reference: pkg/src/memplan/graph.py:375-468 (validate_schedule,
+// sequential_schedule, tensor_lifetimes, live_bytes_by_timestep, peak_memory).
+//
+// Same arithmetic as v2 (k_eval_v2.cu): live[k] = sum_{j<k}(out - free)(o_j)
+// + out(o_k) over unit-packed {fs, out} words, multi-consumer frees added at
+// the latest maximal consumer's position.  What changes is how little each
+// position costs:
+//   * compile-time geometry: SL = NT * C slots, every thread owns exactly C
+//     positions (padding slot k >= n holds op id k, zero bytes), so no loop
+//     carries a runtime guard;
+//   * permutation check by sentinel: pos[] holds 0x8000 for every id before
+//     the scatter; an out-of-range id is clamped to the sink slot SL, so any
+//     duplicate or out-of-range entry leaves some id in [0, SL) at 0x8000 --
+//     one OR per id instead of a range check and a readback per position;
+//   * the edges (u, u+1) and (u, u+2) of the transitive reduction (77 % of a
+//     training graph's) are checked for two ids per 32-bit word in an id-major
+//     pass over pos[] (LDS.128 of 8 ids): with positions < 2^15,
+//     ((pv | 0x80008000) - pu - 0x00010001) keeps bit 15 / 31 iff pv > pu;
+//   * the remaining edges and the two-consumer tensors come as pre-scaled byte
+//     offsets, padded so the loops have a uniform trip count;
+//   * the group's (max, first argmax) is three warp REDUX operations.
+#include "k_common.cuh"
+
+namespace roam {
+
+struct K1V4Args {
+  const void* orders;  // int32 or uint16 rows [B, n]
+  int64_t B;
+  int n, G, shift;
+  const void* opv;  // int2 {fs, out} units per id [SL + 1]
+  const uint4* nm1;
+  const uint4* nm2;
+  const uint32_t* edges;
+  int n_edges;  // multiple of 4 * NT
+  const uint32_t* mpair;
+  int n_pair;  // multiple of NT
+  const uint32_t* mptr;
+  const uint16_t* mcons;
+  const uint32_t* msz;
+  int n_gen, n_mcons;
+  int64_t* peak;
+  int32_t* argmax;
+  uint8_t* valid;
+  size_t off_nm1, off_nm2, off_edges, off_mpair, off_mptr, off_mcons, off_msz;
+  size_t off_groups, group_bytes, off_xs, off_red;
+};
+
+template <int C>
+struct V4Geom {
+  static constexpr int L = C == 4 ? 2 : C == 8 ? 3 : 4;
+  static constexpr int STRIDE = C + 2;  // (STRIDE / 2) odd: conflict-free LDS.128 rows
+};
+
+__device__ __forceinline__ unsigned lds_u16(const unsigned char* base, unsigned byte_off) {
+  return *reinterpret_cast<const uint16_t*>(base + byte_off);
+}
+
+// ((v | 0x80008000) - u - 0x00010001) | nm: bit 15 / 31 set iff the half's
+// edge holds (pv > pu) or is not checked
+__device__ __forceinline__ unsigned simd_gt(unsigned v, unsigned u, unsigned nm) {
+  return ((v | 0x80008000u) - u - 0x00010001u) | nm;
+}
+
+template <typename RowT, int NT, int C>
+__global__ void __launch_bounds__((1024 / NT) * NT, 1) k1v4_eval_orders(const K1V4Args a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int SL = NT * C;
+  constexpr int Q = SL / 8;                 // 8-id chunks
+  constexpr int QR = (Q + NT - 1) / NT;     // chunk rounds per thread
+  constexpr bool QFULL = (Q % NT) == 0;
+  constexpr int NWARPS = NT / 32;
+  using X = V4Geom<C>;
+  constexpr int XS_STEP = (NT / C) * X::STRIDE;
+  const int n = a.n;
+  const RowT* orders = static_cast<const RowT*>(a.orders);
+  {
+    auto cp16 = [&](const void* g, size_t off, size_t bytes) {
+      const uint4* src = static_cast<const uint4*>(g);
+      uint4* dst = reinterpret_cast<uint4*>(smem + off);
+      for (size_t i = threadIdx.x; i < bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+    };
+    cp16(a.opv, 0, align16(8 * size_t(SL + 1)));
+    cp16(a.nm1, a.off_nm1, 16 * size_t(Q));
+    cp16(a.nm2, a.off_nm2, 16 * size_t(Q));
+    cp16(a.edges, a.off_edges, 4 * size_t(a.n_edges));
+    cp16(a.mpair, a.off_mpair, align16(4 * size_t(a.n_pair)));
+    cp16(a.mptr, a.off_mptr, align16(4 * size_t(a.n_gen + 1)));
+    cp16(a.mcons, a.off_mcons, align16(2 * size_t(a.n_mcons)));
+    cp16(a.msz, a.off_msz, align16(4 * size_t(a.n_pair + a.n_gen)));
+  }
+  __syncthreads();
+  const long long* opv = reinterpret_cast<const long long*>(smem);  // fs | out << 32
+  const uint4* nm1 = reinterpret_cast<const uint4*>(smem + a.off_nm1);
+  const uint4* nm2 = reinterpret_cast<const uint4*>(smem + a.off_nm2);
+  const uint32_t* edges = reinterpret_cast<const uint32_t*>(smem + a.off_edges);
+  const uint32_t* mpair = reinterpret_cast<const uint32_t*>(smem + a.off_mpair);
+  const uint32_t* mptr = reinterpret_cast<const uint32_t*>(smem + a.off_mptr);
+  const uint16_t* mcons = reinterpret_cast<const uint16_t*>(smem + a.off_mcons);
+  const uint32_t* msz = reinterpret_cast<const uint32_t*>(smem + a.off_msz);
+
+  const int gid = threadIdx.x / NT;
+  const int tid = threadIdx.x - gid * NT;
+  if (gid >= a.G) return;
+  const int bar_id = 1 + gid;
+  unsigned char* gbase = smem + a.off_groups + size_t(gid) * a.group_bytes;
+  uint16_t* pos = reinterpret_cast<uint16_t*>(gbase);  // [SL + 8]: ids, sink SL, lookahead
+  const unsigned char* posb = gbase;
+  long long* xs = reinterpret_cast<long long*>(gbase + a.off_xs);
+  long long* red_t = reinterpret_cast<long long*>(gbase + a.off_red);  // [NWARPS] warp totals
+  long long* red_c = red_t + NWARPS;                                    // [NWARPS] warp maxima
+  int* red_i = reinterpret_cast<int*>(red_c + NWARPS);                  // [NWARPS] their indices
+  const int lane = tid & 31, warp = tid >> 5;
+  const int64_t cstride = int64_t(gridDim.x) * a.G;
+  long long* xs_w = xs + (tid >> X::L) * X::STRIDE + (tid & (C - 1));
+  const int n_edges = a.n_edges, n_pair = a.n_pair, n_gen = a.n_gen;
+  for (int i = tid; i < (SL + 8) / 2; i += NT) reinterpret_cast<uint32_t*>(pos)[i] = 0x80008000u;
+  gbar(bar_id, NT);
+
+  uint32_t v[C];
+  auto load_row = [&](int64_t cc) {
+    const RowT* row = orders + cc * int64_t(n);
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      const int k = tid + j * NT;
+      v[j] = k < n ? (uint32_t)__ldcs(row + k) : (uint32_t)k;
+    }
+  };
+  int64_t c = int64_t(blockIdx.x) * a.G + gid;
+  if (c < a.B) load_row(c);
+  for (; c < a.B; c += cstride) {
+    // ---- P1: scatter positions; out-of-range ids land in the sink slot
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      v[j] = min(v[j], (uint32_t)SL);
+      pos[v[j]] = (uint16_t)(tid + j * NT);
+    }
+    gbar(bar_id, NT);
+    // ---- P2a (id-major): missing ids (sentinel) and the (u, u+1), (u, u+2) edges
+    unsigned sent = 0, ok = 0xffffffffu;
+#pragma unroll
+    for (int r = 0; r < QR; ++r) {
+      const int q = tid + r * NT;
+      if (QFULL || q < Q) {
+        const uint4 w = *reinterpret_cast<const uint4*>(pos + 8 * q);
+        const unsigned w4 = *reinterpret_cast<const uint32_t*>(pos + 8 * q + 8);
+        const uint4 m1 = nm1[q], m2 = nm2[q];
+        sent |= w.x | w.y | w.z | w.w;
+        ok &= simd_gt(__byte_perm(w.x, w.y, 0x5432), w.x, m1.x);
+        ok &= simd_gt(__byte_perm(w.y, w.z, 0x5432), w.y, m1.y);
+        ok &= simd_gt(__byte_perm(w.z, w.w, 0x5432), w.z, m1.z);
+        ok &= simd_gt(__byte_perm(w.w, w4, 0x5432), w.w, m1.w);
+        ok &= simd_gt(w.y, w.x, m2.x);
+        ok &= simd_gt(w.z, w.y, m2.y);
+        ok &= simd_gt(w.w, w.z, m2.z);
+        ok &= simd_gt(w4, w.w, m2.w);
+      }
+    }
+    // ---- P2a: the other checked edges (pv - pu - 1 < 0 marks a violation)
+    int eacc = 0;
+    for (int e0 = tid; e0 < n_edges; e0 += 4 * NT) {
+      uint32_t w[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) w[i] = edges[e0 + i * NT];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) eacc |= (int)lds_u16(posb, w[i] >> 16) - (int)lds_u16(posb, w[i] & 0xffffu) - 1;
+    }
+    // ---- P2a (position-major): {fs, out} units of the op at each position
+#pragma unroll
+    for (int j = 0; j < C; ++j) xs_w[j * XS_STEP] = opv[v[j]];
+    unsigned bad = ((sent & 0x80008000u) != 0) | ((ok & 0x80008000u) != 0x80008000u) | (eacc < 0);
+    // prefetch the next candidate's row; it lands while P2b / P3 run
+    const int64_t cn = c + cstride;
+    if (cn < a.B) load_row(cn);
+    gbar(bar_id, NT);
+    // ---- P2b: multi-consumer tensors free after their latest maximal consumer
+    // (positions of a broken row may be the sentinel: clamp into the group)
+    auto add_free = [&](unsigned kmax, unsigned units) {
+      kmax = min(kmax, (unsigned)(SL - 1));
+      atomicAdd(reinterpret_cast<unsigned*>(xs + (kmax >> X::L) * X::STRIDE + (kmax & (C - 1))), units);
+    };
+    for (int m = tid; m < n_pair; m += NT) {
+      const uint32_t w = mpair[m];
+      add_free(max(lds_u16(posb, w & 0xffffu), lds_u16(posb, w >> 16)), msz[m]);
+    }
+    for (int m = tid; m < n_gen; m += NT) {
+      const int q0 = mptr[m], q1 = mptr[m + 1];
+      unsigned kmax = 0;
+      for (int q = q0; q < q1; ++q) kmax = max(kmax, (unsigned)pos[mcons[q]]);
+      add_free(kmax, msz[n_pair + m]);
+    }
+    gbar(bar_id, NT);
+    // ---- P3: reset this thread's ids to the sentinel for the next candidate
+#pragma unroll
+    for (int r = 0; r < QR; ++r) {
+      const int q = tid + r * NT;
+      if (QFULL || q < Q)
+        *reinterpret_cast<uint4*>(pos + 8 * q) = make_uint4(0x80008000u, 0x80008000u, 0x80008000u, 0x80008000u);
+    }
+    // ---- P3: blocked scan over this thread's C positions (padding slots
+    // carry zero bytes: they never raise the running max above a real slot)
+    const int k0 = tid * C;
+    const long long* xr = xs + tid * X::STRIDE;
+    long long run = 0, best = LLONG_MIN;
+    int bi = 0;
+#pragma unroll
+    for (int i = 0; i < C; i += 2) {
+      const longlong2 pr = *reinterpret_cast<const longlong2*>(xr + i);
+      long long live = run + (long long)((unsigned long long)pr.x >> 32);
+      if (live > best) {
+        best = live;
+        bi = i;
+      }
+      run = live - (long long)(unsigned)pr.x;
+      live = run + (long long)((unsigned long long)pr.y >> 32);
+      if (live > best) {
+        best = live;
+        bi = i + 1;
+      }
+      run = live - (long long)(unsigned)pr.y;
+    }
+    long long incl = run;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const long long t = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += t;
+    }
+    if (lane == 31) red_t[warp] = incl;
+    bad = gbar_or(bar_id, NT, bad);
+    long long off = incl - run;
+#pragma unroll
+    for (int w = 0; w < NWARPS - 1; ++w)
+      if (w < warp) off += red_t[w];
+    // warp (max, first index): REDUX on the high word, then the low word among
+    // the lanes holding the maximal high word, then the smallest index
+    const long long cand = off + best;
+    const int hi = (int)(cand >> 32);
+    const unsigned lo = (unsigned)cand;
+    const int mh = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+    const unsigned mi = __reduce_min_sync(0xffffffffu, (hi == mh && lo == ml) ? (unsigned)(k0 + bi) : 0xffffffffu);
+    if (lane == 0) {
+      red_c[warp] = (long long)(((unsigned long long)(unsigned)mh << 32) | ml);
+      red_i[warp] = (int)mi;
+    }
+    gbar(bar_id, NT);
+    if (tid == 0) {
+      long long bv = red_c[0];
+      int bk = red_i[0];
+#pragma unroll
+      for (int w = 1; w < NWARPS; ++w)
+        if (red_c[w] > bv) {  // warps hold increasing index ranges: strict > keeps the first
+          bv = red_c[w];
+          bk = red_i[w];
+        }
+      if (n == 0) {
+        bv = 0;
+        bk = 0;
+      }
+      a.peak[c] = (int64_t)bv << a.shift;
+      a.argmax[c] = bk;
+      a.valid[c] = bad ? 0 : 1;
+    }
+  }
+}
+
+template <typename RowT, int NT, int C>
+static int launch_k1v4_t(K1V4Args& a, int grid, size_t smem, cudaStream_t s) {
+  auto kern = k1v4_eval_orders<RowT, NT, C>;
+  RM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (g_timing) {
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, s);
+  }
+  kern<<<grid, NT * a.G, smem, s>>>(a);
+  RM_LAUNCH_CHECK("k1v4_eval_orders launch");
+  if (g_timing) {
+    cudaEventRecord(e1, s);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    g_last_ms = ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+  return RM_OK;
+}
+
+// the instance table must list every (NT, C) k1v4_geometry (roam_graph.cpp) picks
+template <typename RowT>
+static int launch_k1v4_nt(K1V4Args& a, int NT, int C, int grid, size_t smem, cudaStream_t s) {
+#define RM_K1V4_CASE(nt, cc) \
+  if (NT == nt && C == cc) return launch_k1v4_t<RowT, nt, cc>(a, grid, smem, s);
+  RM_K1V4_CASE(32, 4)
+  RM_K1V4_CASE(32, 8)
+  RM_K1V4_CASE(64, 8)
+  RM_K1V4_CASE(96, 8)
+  RM_K1V4_CASE(128, 8)
+  RM_K1V4_CASE(64, 16)
+  RM_K1V4_CASE(96, 16)
+  RM_K1V4_CASE(128, 16)
+  RM_K1V4_CASE(160, 16)
+  RM_K1V4_CASE(192, 16)
+  RM_K1V4_CASE(256, 16)
+  RM_K1V4_CASE(320, 16)
+  RM_K1V4_CASE(384, 16)
+  RM_K1V4_CASE(512, 16)
+  RM_K1V4_CASE(640, 16)
+  RM_K1V4_CASE(768, 16)
+  RM_K1V4_CASE(1024, 16)
+#undef RM_K1V4_CASE
+  return 1;
+}
+
+int launch_k1v4(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, int32_t* argmax,
+                uint8_t* valid, cudaStream_t s, bool u16_rows) {
+  const K1V4Meta& m = g->k4v;
+  if (!m.ok) return 1;
+  const int NT = m.NT, C = m.C, SL = m.SL, Q = SL / 8;
+  K1V4Args a{};
+  a.orders = orders_dev;
+  a.B = B;
+  a.n = g->n;
+  a.shift = g->k2v.shift;
+  a.opv = g->k2v.opv.p;
+  a.nm1 = m.nm1.as<uint4>();
+  a.nm2 = m.nm2.as<uint4>();
+  a.edges = m.edges.as<uint32_t>();
+  a.n_edges = (int)m.n_edges;
+  a.mpair = m.mpair.as<uint32_t>();
+  a.n_pair = (int)m.n_pair;
+  a.mptr = g->k2v.mptr.as<uint32_t>();
+  a.mcons = g->k2v.mcons.as<uint16_t>();
+  a.msz = m.msz.as<uint32_t>();
+  a.n_gen = (int)g->k2v.n_gen;
+  a.n_mcons = (int)g->k2v.n_mcons;
+  a.peak = peak;
+  a.argmax = argmax;
+  a.valid = valid;
+  const int stride = C + 2;  // V4Geom<C>::STRIDE
+  a.off_nm1 = align16(8 * size_t(SL + 1));
+  a.off_nm2 = a.off_nm1 + 16 * size_t(Q);
+  a.off_edges = a.off_nm2 + 16 * size_t(Q);
+  a.off_mpair = align16(a.off_edges + 4 * size_t(a.n_edges));
+  a.off_mptr = align16(a.off_mpair + 4 * size_t(a.n_pair));
+  a.off_mcons = align16(a.off_mptr + 4 * size_t(a.n_gen + 1));
+  a.off_msz = align16(a.off_mcons + 2 * size_t(a.n_mcons));
+  a.off_groups = align16(a.off_msz + 4 * size_t(a.n_pair + a.n_gen));
+  a.off_xs = align16(2 * size_t(SL + 8));
+  a.off_red = align16(a.off_xs + 8 * size_t(SL / C) * stride);
+  a.group_bytes = align16(a.off_red + 3 * 8 * size_t(NT / 32));
+  int dev = g->device;
+  int max_smem = 0;
+  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const size_t avail = max_smem > (int)a.off_groups ? size_t(max_smem) - a.off_groups : 0;
+  int G = (int)(avail / a.group_bytes);
+  G = std::min(G, 1024 / NT);
+  G = std::min(G, 15);
+  if (G < 1) return 1;
+  const int64_t sms = sm_count(dev);
+  if (int64_t(G) * sms > B) G = (int)std::max<int64_t>(1, (B + sms - 1) / sms);
+  a.G = G;
+  const size_t smem = a.off_groups + size_t(G) * a.group_bytes;
+  const int grid = (int)std::min<int64_t>(sms, (B + G - 1) / G);
+  return u16_rows ? launch_k1v4_nt<uint16_t>(a, NT, C, grid, smem, s)
+                  : launch_k1v4_nt<int32_t>(a, NT, C, grid, smem, s);
+}
+
+}  // namespace roam

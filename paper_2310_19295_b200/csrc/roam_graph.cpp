@@ -145,6 +145,85 @@ static void build_k1v2_host(RmGraph& g, const std::vector<int64_t>& out,
   g.k2v.ok = 1;
 }
 
+// K1 v4 geometry: the smallest slot count SL = NT * C >= n among the compiled
+// instances (k_eval_v4.cu launch table); C = 8 positions per thread up to 1k
+// ops, 16 beyond.
+static bool k1v4_geometry(int n, int& NT, int& C) {
+  static const int nt8[] = {32, 64, 96, 128};
+  static const int nt16[] = {64, 96, 128, 160, 192, 256, 320, 384, 512, 640, 768, 1024};
+  if (n <= 128) {
+    NT = 32;
+    C = 4;
+    return true;
+  }
+  for (int nt : nt8)
+    if (nt * 8 >= n) {
+      NT = nt;
+      C = 8;
+      return true;
+    }
+  for (int nt : nt16)
+    if (nt * 16 >= n) {
+      NT = nt;
+      C = 16;
+      return true;
+    }
+  return false;
+}
+
+// K1 v4 metadata (see roam_internal.h); needs the v2 layout (unit-packed
+// opv, 32-bit free fields) and 15-bit positions.
+static void build_k1v4_host(RmGraph& g) {
+  g.k4v.ok = 0;
+  const int n = g.n;
+  int NT = 0, C = 0;
+  if (!g.k2v.ok || !k1v4_geometry(n, NT, C)) return;
+  const int SL = NT * C;
+  if (SL + 8 > 32768) return;
+  if (g.h2_opv.size() < 2 * size_t(SL + 1)) g.h2_opv.resize(2 * size_t(SL + 1), 0);
+  const int Q = SL / 8;
+  g.h4_nm1.assign(4 * size_t(Q), 0x80008000u);
+  g.h4_nm2.assign(4 * size_t(Q), 0x80008000u);
+  std::vector<uint32_t> gen;
+  for (size_t e = 0; e < g.h_edge_u.size(); ++e) {
+    const int u = g.h_edge_u[e], v = g.h_edge_v[e];
+    const int d = v - u;
+    const uint32_t bit = 1u << (15 + 16 * (u & 1));
+    const size_t word = size_t(u >> 3) * 4 + ((u & 7) >> 1);
+    if (d == 1) {
+      g.h4_nm1[word] &= ~bit;
+    } else if (d == 2) {
+      g.h4_nm2[word] &= ~bit;
+    } else {
+      gen.push_back((uint32_t)(2 * u) | ((uint32_t)(2 * v) << 16));
+    }
+  }
+  if (!gen.empty()) {
+    const size_t pad = 4 * size_t(NT);
+    const uint32_t first = gen[0];
+    while (gen.size() % pad) gen.push_back(first);
+  }
+  g.h4_edges = gen;
+  g.h4_mpair.clear();
+  g.h4_msz.clear();
+  for (size_t m = 0; m < g.h2_mpair.size(); ++m) {
+    const uint32_t w = g.h2_mpair[m];
+    g.h4_mpair.push_back(((w & 0xffffu) << 1) | ((w >> 16) << 17));
+    g.h4_msz.push_back(g.h2_msz[m]);
+  }
+  while (g.h4_mpair.size() % NT) {
+    g.h4_mpair.push_back(0);
+    g.h4_msz.push_back(0);
+  }
+  g.h4_msz.insert(g.h4_msz.end(), g.h2_msz.begin() + g.h2_mpair.size(), g.h2_msz.end());
+  g.k4v.NT = NT;
+  g.k4v.C = C;
+  g.k4v.SL = SL;
+  g.k4v.n_edges = (int64_t)g.h4_edges.size();
+  g.k4v.n_pair = (int64_t)g.h4_mpair.size();
+  g.k4v.ok = 1;
+}
+
 static int build_k1_host(RmGraph& g, bool allow_reduce) {
   const int n = g.n, T = g.T;
   std::vector<uint64_t> desc;
@@ -225,9 +304,10 @@ static int build_k1_host(RmGraph& g, bool allow_reduce) {
     if (g.h_slot[c] < 0) g.h_slot[c] = K++;
 
   build_k1v2_host(g, out, fs);
+  build_k1v4_host(g);
 
   RmGraphInfo& I = g.info;
-  I.k1_variant = g.k2v.ok ? (g.n <= 1024 ? 3 : 2) : 1;
+  I.k1_variant = g.k4v.ok ? 4 : g.k2v.ok ? (g.n <= 1024 ? 3 : 2) : 1;
   I.unit_shift = g.k2v.shift;
   I.n_check_edges = (int64_t)g.h_edge_u.size();
   I.n_multi = (int64_t)g.h_msize.size();
@@ -410,6 +490,11 @@ int rm_graph_create(const RmGraphDesc* d, uint32_t flags, RmGraph** out) {
     if (!e && g->k2v.ok) e = up(g->k2v.mptr, g->h2_mptr);
     if (!e && g->k2v.ok) e = up(g->k2v.mcons, g->h2_mcons);
     if (!e && g->k2v.ok) e = up(g->k2v.msz, g->h2_msz);
+    if (!e && g->k4v.ok) e = up(g->k4v.nm1, g->h4_nm1);
+    if (!e && g->k4v.ok) e = up(g->k4v.nm2, g->h4_nm2);
+    if (!e && g->k4v.ok) e = up(g->k4v.edges, g->h4_edges);
+    if (!e && g->k4v.ok) e = up(g->k4v.mpair, g->h4_mpair);
+    if (!e && g->k4v.ok) e = up(g->k4v.msz, g->h4_msz);
     if (!e) e = up(g->d_size, g->size);
     if (!e) e = up(g->d_producer, g->producer);
     if (!e) e = up(g->d_cons_ptr, g->cons_ptr);
