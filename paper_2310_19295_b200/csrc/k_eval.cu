@@ -486,7 +486,7 @@ static int launch_k1_int32(RmGraph* g, const int32_t* orders_dev, int64_t B, int
 int launch_k1(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, int32_t* argmax,
               uint8_t* valid, cudaStream_t s, bool u16_rows) {
   if (B <= 0) return RM_OK;
-  if (g->k4v.ok && (t_force_variant == 0 || t_force_variant == 4)) {
+  if (g->k4v.ok && (t_force_variant == 0 || t_force_variant >= 4)) {
     const int rc = launch_k1v4(g, orders_dev, B, peak, argmax, valid, s, u16_rows);
     if (rc != 1) return rc;
   }
@@ -495,7 +495,7 @@ int launch_k1(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, int3
     // shared memory costs more occupancy than the shared gathers save
     // (tools/k1_ab.py: layered 1k ops 0.088 vs 0.100 ms; GPT-2 small 0.127 vs
     // 0.113 ms)
-    if (t_force_variant == 3 || ((t_force_variant == 0 || t_force_variant == 4) && g->n <= 1024)) {
+    if (t_force_variant == 3 || ((t_force_variant == 0 || t_force_variant >= 4) && g->n <= 1024)) {
       const int rc = launch_k1v2(g, orders_dev, B, peak, argmax, valid, s, true, u16_rows);
       if (rc != 1) return rc;
     }

@@ -20,7 +20,8 @@
 //     ((pv | 0x80008000) - pu - 0x00010001) keeps bit 15 / 31 iff pv > pu;
 //   * the remaining edges and the two-consumer tensors come as pre-scaled byte
 //     offsets, padded so the loops have a uniform trip count;
-//   * the group's (max, first argmax) is three warp REDUX operations.
+//   * the group's (max, first argmax) is three warp REDUX operations;
+//   * the edge masks of a thread's chunks are register words (build_k1_em).
 #include "k_common.cuh"
 
 namespace roam {
@@ -30,8 +31,7 @@ struct K1V4Args {
   int64_t B;
   int n, G, shift;
   const void* opv;  // int2 {fs, out} units per id [SL + 1]
-  const uint4* nm1;
-  const uint4* nm2;
+  const uint32_t* em;  // SIMD edge-mask word per 8-id chunk (roam_graph.cpp build_k1_em)
   const uint32_t* edges;
   int n_edges;  // multiple of 4 * NT
   const uint32_t* mpair;
@@ -43,7 +43,7 @@ struct K1V4Args {
   int64_t* peak;
   int32_t* argmax;
   uint8_t* valid;
-  size_t off_nm1, off_nm2, off_edges, off_mpair, off_mptr, off_mcons, off_msz;
+  size_t off_edges, off_mpair, off_mptr, off_mcons, off_msz;
   size_t off_groups, group_bytes, off_xs, off_red;
 };
 
@@ -82,8 +82,6 @@ __global__ void __launch_bounds__((1024 / NT) * NT, 1) k1v4_eval_orders(const K1
       for (size_t i = threadIdx.x; i < bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
     };
     cp16(a.opv, 0, align16(8 * size_t(SL + 1)));
-    cp16(a.nm1, a.off_nm1, 16 * size_t(Q));
-    cp16(a.nm2, a.off_nm2, 16 * size_t(Q));
     cp16(a.edges, a.off_edges, 4 * size_t(a.n_edges));
     cp16(a.mpair, a.off_mpair, align16(4 * size_t(a.n_pair)));
     cp16(a.mptr, a.off_mptr, align16(4 * size_t(a.n_gen + 1)));
@@ -92,8 +90,6 @@ __global__ void __launch_bounds__((1024 / NT) * NT, 1) k1v4_eval_orders(const K1
   }
   __syncthreads();
   const long long* opv = reinterpret_cast<const long long*>(smem);  // fs | out << 32
-  const uint4* nm1 = reinterpret_cast<const uint4*>(smem + a.off_nm1);
-  const uint4* nm2 = reinterpret_cast<const uint4*>(smem + a.off_nm2);
   const uint32_t* edges = reinterpret_cast<const uint32_t*>(smem + a.off_edges);
   const uint32_t* mpair = reinterpret_cast<const uint32_t*>(smem + a.off_mpair);
   const uint32_t* mptr = reinterpret_cast<const uint32_t*>(smem + a.off_mptr);
@@ -115,6 +111,12 @@ __global__ void __launch_bounds__((1024 / NT) * NT, 1) k1v4_eval_orders(const K1
   const int64_t cstride = int64_t(gridDim.x) * a.G;
   long long* xs_w = xs + (tid >> X::L) * X::STRIDE + (tid & (C - 1));
   const int n_edges = a.n_edges, n_pair = a.n_pair, n_gen = a.n_gen;
+  uint32_t em[QR];  // edge masks of this thread's chunks (ids 8q..8q+9)
+#pragma unroll
+  for (int r = 0; r < QR; ++r) {
+    const int q = tid + r * NT;
+    em[r] = (QFULL || q < Q) ? __ldg(a.em + q) : 0xff00ff00u;
+  }
   for (int i = tid; i < (SL + 8) / 2; i += NT) reinterpret_cast<uint32_t*>(pos)[i] = 0x80008000u;
   gbar(bar_id, NT);
 
@@ -142,20 +144,21 @@ __global__ void __launch_bounds__((1024 / NT) * NT, 1) k1v4_eval_orders(const K1
 #pragma unroll
     for (int r = 0; r < QR; ++r) {
       const int q = tid + r * NT;
-      if (QFULL || q < Q) {
-        const uint4 w = *reinterpret_cast<const uint4*>(pos + 8 * q);
-        const unsigned w4 = *reinterpret_cast<const uint32_t*>(pos + 8 * q + 8);
-        const uint4 m1 = nm1[q], m2 = nm2[q];
-        sent |= w.x | w.y | w.z | w.w;
-        ok &= simd_gt(__byte_perm(w.x, w.y, 0x5432), w.x, m1.x);
-        ok &= simd_gt(__byte_perm(w.y, w.z, 0x5432), w.y, m1.y);
-        ok &= simd_gt(__byte_perm(w.z, w.w, 0x5432), w.z, m1.z);
-        ok &= simd_gt(__byte_perm(w.w, w4, 0x5432), w.w, m1.w);
-        ok &= simd_gt(w.y, w.x, m2.x);
-        ok &= simd_gt(w.z, w.y, m2.y);
-        ok &= simd_gt(w.w, w.z, m2.z);
-        ok &= simd_gt(w4, w.w, m2.w);
-      }
+      // the next chunk's first word comes from the next lane (same round)
+      const uint4 w = (QFULL || q < Q) ? *reinterpret_cast<const uint4*>(pos + 8 * q)
+                                       : make_uint4(0, 0, 0, 0);
+      unsigned w4 = __shfl_down_sync(0xffffffffu, w.x, 1);
+      if (lane == 31 && (QFULL || q < Q)) w4 = *reinterpret_cast<const uint32_t*>(pos + 8 * q + 8);
+      const unsigned m = em[r];
+      sent |= w.x | w.y | w.z | w.w;
+      ok &= simd_gt(__byte_perm(w.x, w.y, 0x5432), w.x, m);
+      ok &= simd_gt(__byte_perm(w.y, w.z, 0x5432), w.y, m << 1);
+      ok &= simd_gt(__byte_perm(w.z, w.w, 0x5432), w.z, m << 2);
+      ok &= simd_gt(__byte_perm(w.w, w4, 0x5432), w.w, m << 3);
+      ok &= simd_gt(w.y, w.x, m << 4);
+      ok &= simd_gt(w.z, w.y, m << 5);
+      ok &= simd_gt(w.w, w.z, m << 6);
+      ok &= simd_gt(w4, w.w, m << 7);
     }
     // ---- P2a: the other checked edges (pv - pu - 1 < 0 marks a violation)
     int eacc = 0;
@@ -178,7 +181,7 @@ __global__ void __launch_bounds__((1024 / NT) * NT, 1) k1v4_eval_orders(const K1
     // (positions of a broken row may be the sentinel: clamp into the group)
     auto add_free = [&](unsigned kmax, unsigned units) {
       kmax = min(kmax, (unsigned)(SL - 1));
-      atomicAdd(reinterpret_cast<unsigned*>(xs + (kmax >> X::L) * X::STRIDE + (kmax & (C - 1))), units);
+      if (units) atomicAdd(reinterpret_cast<unsigned*>(xs + (kmax >> X::L) * X::STRIDE + (kmax & (C - 1))), units);
     };
     for (int m = tid; m < n_pair; m += NT) {
       const uint32_t w = mpair[m];
@@ -319,15 +322,14 @@ int launch_k1v4(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, in
                 uint8_t* valid, cudaStream_t s, bool u16_rows) {
   const K1V4Meta& m = g->k4v;
   if (!m.ok) return 1;
-  const int NT = m.NT, C = m.C, SL = m.SL, Q = SL / 8;
+  const int NT = m.NT, C = m.C, SL = m.SL;
   K1V4Args a{};
   a.orders = orders_dev;
   a.B = B;
   a.n = g->n;
   a.shift = g->k2v.shift;
   a.opv = g->k2v.opv.p;
-  a.nm1 = m.nm1.as<uint4>();
-  a.nm2 = m.nm2.as<uint4>();
+  a.em = m.em.as<uint32_t>();
   a.edges = m.edges.as<uint32_t>();
   a.n_edges = (int)m.n_edges;
   a.mpair = m.mpair.as<uint32_t>();
@@ -341,9 +343,7 @@ int launch_k1v4(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, in
   a.argmax = argmax;
   a.valid = valid;
   const int stride = C + 2;  // V4Geom<C>::STRIDE
-  a.off_nm1 = align16(8 * size_t(SL + 1));
-  a.off_nm2 = a.off_nm1 + 16 * size_t(Q);
-  a.off_edges = a.off_nm2 + 16 * size_t(Q);
+  a.off_edges = align16(8 * size_t(SL + 1));
   a.off_mpair = align16(a.off_edges + 4 * size_t(a.n_edges));
   a.off_mptr = align16(a.off_mpair + 4 * size_t(a.n_pair));
   a.off_mcons = align16(a.off_mptr + 4 * size_t(a.n_gen + 1));

@@ -181,22 +181,10 @@ static void build_k1v4_host(RmGraph& g) {
   const int SL = NT * C;
   if (SL + 8 > 32768) return;
   if (g.h2_opv.size() < 2 * size_t(SL + 1)) g.h2_opv.resize(2 * size_t(SL + 1), 0);
-  const int Q = SL / 8;
-  g.h4_nm1.assign(4 * size_t(Q), 0x80008000u);
-  g.h4_nm2.assign(4 * size_t(Q), 0x80008000u);
-  std::vector<uint32_t> gen;
+  std::vector<uint32_t> gen;  // edges the SIMD masks (build_k1_em) do not cover
   for (size_t e = 0; e < g.h_edge_u.size(); ++e) {
     const int u = g.h_edge_u[e], v = g.h_edge_v[e];
-    const int d = v - u;
-    const uint32_t bit = 1u << (15 + 16 * (u & 1));
-    const size_t word = size_t(u >> 3) * 4 + ((u & 7) >> 1);
-    if (d == 1) {
-      g.h4_nm1[word] &= ~bit;
-    } else if (d == 2) {
-      g.h4_nm2[word] &= ~bit;
-    } else {
-      gen.push_back((uint32_t)(2 * u) | ((uint32_t)(2 * v) << 16));
-    }
+    if (v - u != 1 && v - u != 2) gen.push_back((uint32_t)(2 * u) | ((uint32_t)(2 * v) << 16));
   }
   if (!gen.empty()) {
     const size_t pad = 4 * size_t(NT);
@@ -222,6 +210,24 @@ static void build_k1v4_host(RmGraph& g) {
   g.k4v.n_edges = (int64_t)g.h4_edges.size();
   g.k4v.n_pair = (int64_t)g.h4_mpair.size();
   g.k4v.ok = 1;
+}
+
+// SIMD edge-mask words of K1 v4, em[q] (one per 8-id chunk q, held in a
+// register by the thread owning the chunk): bit 15-m / 31-m = edge
+// (8q+2m, 8q+2m+1) / (8q+2m+1, 8q+2m+2) NOT checked, bit 11-m / 27-m = the
+// same for (8q+2m, 8q+2m+2) / (8q+2m+1, 8q+2m+3), so (em << m) and
+// (em << (m + 4)) put word m's masks on bits 15 and 31.  Sized for every
+// chunk either geometry reads.
+static void build_k1_em(RmGraph& g) {
+  const size_t chunks = g.k4v.ok ? size_t(g.k4v.SL / 8) : 0;
+  g.h4_em.assign(chunks, 0xff00ff00u);
+  if (!chunks) return;
+  for (size_t e = 0; e < g.h_edge_u.size(); ++e) {
+    const int u = g.h_edge_u[e], v = g.h_edge_v[e];
+    const int d = v - u, m = (u & 7) >> 1, hi = u & 1;
+    if (d == 1) g.h4_em[u >> 3] &= ~(1u << (15 - m + 16 * hi));
+    if (d == 2) g.h4_em[u >> 3] &= ~(1u << (11 - m + 16 * hi));
+  }
 }
 
 static int build_k1_host(RmGraph& g, bool allow_reduce) {
@@ -305,6 +311,7 @@ static int build_k1_host(RmGraph& g, bool allow_reduce) {
 
   build_k1v2_host(g, out, fs);
   build_k1v4_host(g);
+  build_k1_em(g);
 
   RmGraphInfo& I = g.info;
   I.k1_variant = g.k4v.ok ? 4 : g.k2v.ok ? (g.n <= 1024 ? 3 : 2) : 1;
@@ -490,11 +497,10 @@ int rm_graph_create(const RmGraphDesc* d, uint32_t flags, RmGraph** out) {
     if (!e && g->k2v.ok) e = up(g->k2v.mptr, g->h2_mptr);
     if (!e && g->k2v.ok) e = up(g->k2v.mcons, g->h2_mcons);
     if (!e && g->k2v.ok) e = up(g->k2v.msz, g->h2_msz);
-    if (!e && g->k4v.ok) e = up(g->k4v.nm1, g->h4_nm1);
-    if (!e && g->k4v.ok) e = up(g->k4v.nm2, g->h4_nm2);
     if (!e && g->k4v.ok) e = up(g->k4v.edges, g->h4_edges);
     if (!e && g->k4v.ok) e = up(g->k4v.mpair, g->h4_mpair);
     if (!e && g->k4v.ok) e = up(g->k4v.msz, g->h4_msz);
+    if (!e && g->k4v.ok) e = up(g->k4v.em, g->h4_em);
     if (!e) e = up(g->d_size, g->size);
     if (!e) e = up(g->d_producer, g->producer);
     if (!e) e = up(g->d_cons_ptr, g->cons_ptr);

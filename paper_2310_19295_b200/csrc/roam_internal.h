@@ -102,10 +102,8 @@ struct K1V2Meta {
 // multi-consumer CSR).  Geometry fixed per graph: NT threads per candidate,
 // C positions per thread, SL = NT * C slots (ids n..SL-1 are zero-byte
 // padding ops, id SL the sink for out-of-range row values).
-//   nm1/nm2 = per 8-id chunk q, four words each: the "not-checked" masks of
-//             the SIMD edge checks (u, u+1) and (u, u+2); word m covers the
-//             edges out of ids 8q+2m (low half) and 8q+2m+1 (high half), bit
-//             15/31 set = no such edge
+//   em      = one register word per 8-id chunk: the "not-checked" masks of the SIMD edge checks (u, u+1)
+//             and (u, u+2) (roam_graph.cpp build_k1_em)
 //   edges   = every other checked edge as byte offsets (2u | 2v << 16), padded
 //             with copies of the first one to a multiple of 4*NT
 //   mpair   = two-consumer tensors as byte offsets, padded to a multiple of NT
@@ -115,7 +113,7 @@ struct K1V4Meta {
   int ok = 0;
   int NT = 0, C = 0, SL = 0;
   int64_t n_edges = 0, n_pair = 0;
-  DevBuf nm1, nm2, edges, mpair, msz;
+  DevBuf em, edges, mpair, msz;
 };
 
 }  // namespace roam
@@ -142,7 +140,7 @@ struct RmGraph {
   std::vector<int32_t> h2_opv;     // 2n
   std::vector<uint32_t> h2_edges, h2_mpair, h2_mptr, h2_msz;
   std::vector<uint16_t> h2_mcons;
-  std::vector<uint32_t> h4_nm1, h4_nm2, h4_edges, h4_mpair, h4_msz;
+  std::vector<uint32_t> h4_em, h4_edges, h4_mpair, h4_msz;
   roam::DevBuf d_size, d_producer, d_cons_ptr, d_cons_idx, d_in_ptr, d_in_idx, d_out_ptr,
       d_out_idx, d_pred_ptr, d_pred_idx, d_succ_ptr, d_succ_idx;
 };
