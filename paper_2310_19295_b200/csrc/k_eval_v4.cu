@@ -82,7 +82,7 @@ __global__ void __launch_bounds__((1024 / NT) * NT, 1) k1v4_eval_orders(const K1
       for (size_t i = threadIdx.x; i < bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
     };
     cp16(a.opv, 0, align16(8 * size_t(SL + 1)));
-    cp16(a.edges, a.off_edges, 4 * size_t(a.n_edges));
+    if (a.n_edges != 4 * NT) cp16(a.edges, a.off_edges, 4 * size_t(a.n_edges));
     cp16(a.mpair, a.off_mpair, align16(4 * size_t(a.n_pair)));
     cp16(a.mptr, a.off_mptr, align16(4 * size_t(a.n_gen + 1)));
     cp16(a.mcons, a.off_mcons, align16(2 * size_t(a.n_mcons)));
@@ -111,6 +111,25 @@ __global__ void __launch_bounds__((1024 / NT) * NT, 1) k1v4_eval_orders(const K1
   const int64_t cstride = int64_t(gridDim.x) * a.G;
   long long* xs_w = xs + (tid >> X::L) * X::STRIDE + (tid & (C - 1));
   const int n_edges = a.n_edges, n_pair = a.n_pair, n_gen = a.n_gen;
+  // the generic edges stay in registers when there are exactly 4 per thread
+  const bool ereg = n_edges == 4 * NT;
+  uint32_t er[4] = {0u, 0u, 0u, 0u};
+  if (ereg) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) er[i] = __ldg(a.edges + tid + i * NT);
+  }
+  // likewise the two-consumer tensors when there are at most 4 per thread
+  const int pk = n_pair / NT;
+  const bool preg = pk <= 4;
+  uint32_t pw[4] = {0u, 0u, 0u, 0u}, pu[4] = {0u, 0u, 0u, 0u};
+  if (preg) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (i < pk) {
+        pw[i] = __ldg(a.mpair + tid + i * NT);
+        pu[i] = __ldg(a.msz + tid + i * NT);
+      }
+  }
   uint32_t em[QR];  // edge masks of this thread's chunks (ids 8q..8q+9)
 #pragma unroll
   for (int r = 0; r < QR; ++r) {
@@ -162,7 +181,13 @@ __global__ void __launch_bounds__((1024 / NT) * NT, 1) k1v4_eval_orders(const K1
     }
     // ---- P2a: the other checked edges (pv - pu - 1 < 0 marks a violation)
     int eacc = 0;
-    for (int e0 = tid; e0 < n_edges; e0 += 4 * NT) {
+    int e_first = tid;
+    if (ereg) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) eacc |= (int)lds_u16(posb, er[i] >> 16) - (int)lds_u16(posb, er[i] & 0xffffu) - 1;
+      e_first = n_edges;
+    }
+    for (int e0 = e_first; e0 < n_edges; e0 += 4 * NT) {
       uint32_t w[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) w[i] = edges[e0 + i * NT];
@@ -183,7 +208,14 @@ __global__ void __launch_bounds__((1024 / NT) * NT, 1) k1v4_eval_orders(const K1
       kmax = min(kmax, (unsigned)(SL - 1));
       if (units) atomicAdd(reinterpret_cast<unsigned*>(xs + (kmax >> X::L) * X::STRIDE + (kmax & (C - 1))), units);
     };
-    for (int m = tid; m < n_pair; m += NT) {
+    int m_first = tid;
+    if (preg) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (i < pk) add_free(max(lds_u16(posb, pw[i] & 0xffffu), lds_u16(posb, pw[i] >> 16)), pu[i]);
+      m_first = n_pair;
+    }
+    for (int m = m_first; m < n_pair; m += NT) {
       const uint32_t w = mpair[m];
       add_free(max(lds_u16(posb, w & 0xffffu), lds_u16(posb, w >> 16)), msz[m]);
     }
