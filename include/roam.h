@@ -241,6 +241,22 @@ int rm_greedy_windows(RmGraph* g, int32_t W, const int64_t* win_ptr, const int32
                       int32_t* order, int64_t* peak, int32_t* status, int32_t* bad_tensor,
                       void* stream);
 
+/* K5: batched exact window ordering (replaces ordering.py:183-286 exact_order
+ * for every window whose search provably stays under its node cap), one
+ * launch for all windows of a graph.  Same window CSR as rm_greedy_windows;
+ * node_cap[w] < 0 means no cap.  Per window: status 0 = exact answer in
+ * order[win_ptr[w]..] (global op ids) and peak[w]; 1 = the reference's
+ * ConfigError (bad_tensor[w] = the live-in tensor without a local consumer);
+ * 2 = no order exists; 3 = the window has more order ideals than
+ * node_cap + 1 (or more than 22 ops): the reference's DFS may stop at its cap
+ * and return the greedy incumbent, so the caller runs that search.
+ * nodes[w] = order ideals - 1 (an upper bound on the DFS's expansions). */
+int rm_exact_windows(RmGraph* g, int32_t W, const int64_t* win_ptr, const int32_t* win_ops,
+                     const int64_t* lin_ptr, const int32_t* lin_idx,
+                     const int64_t* lout_ptr, const int32_t* lout_idx, const int64_t* node_cap,
+                     int32_t* order, int64_t* peak, int64_t* nodes, int32_t* status,
+                     int32_t* bad_tensor, void* stream);
+
 /* ------------------------------------------------------------- misc */
 
 const char* rm_last_error(void);

@@ -381,3 +381,86 @@ def greedy_order(g, ops, live_in=(), live_out=()) -> tuple[tuple[int, ...], int]
         sched |= 1 << i
         order.append(v)
     return tuple(order), peak
+
+
+def _window_local(g, ops, live_in, live_out):
+    """ordering.py:78-123 (_Local) reduced to what the exact DP needs:
+    local op order, pred masks, out bytes, start_live, and the freeable
+    tensors as (consumer mask, size).  A tensor frees when its count of local
+    consumer ENTRIES reaches 0 with one decrement per distinct consuming op, so
+    an op listing an input twice keeps it live (hazard h1)."""
+    ops = tuple(sorted(ops))
+    inside = set(ops)
+    index = {v: i for i, v in enumerate(ops)}
+    live_in, live_out = set(live_in), set(live_out)
+    produced = {t for v in ops for t in g.ops[v].outputs}
+    freeable = []
+    for t in sorted(produced | live_in):
+        info = g.tensors[t]
+        local = sum(1 for c in info.consumers if c in inside)
+        if t in live_out or (t in produced and local == 0):
+            continue                                   # held
+        if t in live_in and local == 0:
+            raise OracleConfigError(f"live-in tensor {t} has no consumer in the window and is not live-out")
+        cons = {c for c in info.consumers if c in inside}
+        if len(cons) == local:                        # else never reaches 0 (duplicate entries)
+            m = 0
+            for c in cons:
+                m |= 1 << index[c]
+            freeable.append((m, info.size))
+    start = sum(g.tensors[t].size for t in sorted(live_in))
+    out_bytes = [sum(g.tensors[t].size for t in g.ops[v].outputs) for v in ops]
+    pred_mask = []
+    for v in ops:
+        m = 0
+        for t in g.ops[v].inputs:
+            p = g.tensors[t].producer
+            if p in inside and p != v:
+                m |= 1 << index[p]
+        pred_mask.append(m)
+    return ops, pred_mask, out_bytes, start, freeable
+
+
+def exact_order_dp(g, ops, live_in=(), live_out=(), node_cap=None):
+    """ordering.py:183-286 (exact_order) restated as a DP over the window's
+    order ideals (SURVEY §8 hazard h10):
+
+      V[full] = 0,  V[mask] = min over ready i of max(live(mask) + out[i], V[mask | i])
+
+    then the walk from mask 0 takes the smallest local index i (= ascending op
+    id) with max(live + out[i], V[mask | i]) <= V[mask]; peak = max(V[0],
+    start_live).  The reference's memoised DFS expands each order ideal at
+    most once, so when (#ideals - 1) <= node_cap it never hits its cap and
+    returns exactly this; otherwise its answer depends on how far its pruned
+    DFS gets, and this function returns None.  Returns (order, peak, #ideals)."""
+    ops, pred, out, start, freeable = _window_local(g, ops, live_in, live_out)
+    n = len(ops)
+    if n == 0:
+        return (), start, 1
+    full = (1 << n) - 1
+    down = [m for m in range(1 << n) if all(not (m >> i & 1) or not (pred[i] & ~m) for i in range(n))]
+    if node_cap is not None and len(down) - 1 > node_cap:
+        return None
+
+    def live(m):
+        s = start + sum(out[i] for i in range(n) if m >> i & 1)
+        return s - sum(sz for cm, sz in freeable if cm & m == cm)
+
+    V = {full: 0}
+    for m in sorted(down, key=lambda x: -bin(x).count("1")):
+        if m == full:
+            continue
+        lv = live(m)
+        V[m] = min(max(lv + out[i], V[m | 1 << i]) for i in range(n)
+                   if not (m >> i & 1) and not (pred[i] & ~m))
+    order, m = [], 0
+    while m != full:
+        lv = live(m)
+        for i in range(n):
+            if m >> i & 1 or pred[i] & ~m:
+                continue
+            if max(lv + out[i], V[m | 1 << i]) <= V[m]:
+                break
+        order.append(ops[i])
+        m |= 1 << i
+    return tuple(order), max(V[0], start), len(down)

@@ -75,12 +75,16 @@ def _translate(mp, fn):
     return wrapper
 
 
+def _raise(e):
+    raise e
+
+
 class _State:
     installed = None  # (memplan module, {(module, name): original})
 
 
 # dispatch counters since install(): how the planner's subtasks were served
-STATS = {"windows_k4": 0, "windows_ref_exact": 0, "leaves_k3_constrained": 0,
+STATS = {"windows_k4": 0, "windows_k5": 0, "windows_ref_exact": 0, "leaves_k3_constrained": 0,
          "leaves_k3_exact": 0, "leaves_ref_search": 0}
 
 
@@ -104,17 +108,41 @@ def install(mp=None):
                                 stats=lay.LayoutStats(m.stats.nodes, m.stats.wall_time))
 
     def solve_windows(jobs):
-        out = [None] * len(jobs)
+        """Every greedy window in one K4 launch and every exact window in one
+        K5 launch; a window with more order ideals than its node cap runs the
+        reference's capped DFS (its answer depends on where that search
+        stops).  Errors surface in job order, as the sequential map raises them."""
         greedy = [k for k, (p, limit) in enumerate(jobs) if len(p.ops) > limit]
-        sols = _ord.greedy_orders([jobs[k][0] for k in greedy], solution_type=ordm.OrderingSolution,
-                                  stats_type=ordm.SolverStats)
-        for k, s in zip(greedy, sols):
-            out[k] = s
-        STATS["windows_k4"] += len(greedy)
-        for k, (p, limit) in enumerate(jobs):
-            if out[k] is None:
-                out[k] = ref_exact_order(p)   # exact DFS stays the reference's
+        exact = [k for k, (p, limit) in enumerate(jobs) if len(p.ops) <= limit]
+        exact_keys = set(exact)
+        res = [None] * len(jobs)
+        for idx, batch in ((greedy, _ord.greedy_windows), (exact, _ord.exact_windows)):
+            groups = {}
+            for k in idx:
+                groups.setdefault(id(jobs[k][0].graph), []).append(k)
+            for ks in groups.values():
+                for k, r in zip(ks, batch([jobs[k][0] for k in ks])):
+                    res[k] = r
+        out = []
+        for k, ((p, limit), r) in enumerate(zip(jobs, res)):
+            T(_ord._check_problem)(p)
+            if isinstance(r, GraphError):
+                T(functools.partial(_raise, r))()
+            if isinstance(r, Exception):
+                raise r
+            if r is _ord.NEEDS_SEARCH:
+                out.append(ref_exact_order(p))
                 STATS["windows_ref_exact"] += 1
+            elif k in exact_keys:
+                order, peak, nodes = r
+                out.append(ordm.OrderingSolution(order=order, peak=peak, optimal=True,
+                                                  stats=ordm.SolverStats(nodes, 0.0)))
+                STATS["windows_k5"] += 1
+            else:
+                order, peak = r
+                out.append(ordm.OrderingSolution(order=order, peak=peak, optimal=False,
+                                                  stats=ordm.SolverStats(len(order), 0.0)))
+                STATS["windows_k4"] += 1
         return out
 
     def solve_layouts(jobs):

@@ -1,10 +1,14 @@
-"""Window greedy ordering on the GPU -- drop-in for the reference's
-``memplan.ordering.greedy_order`` plus its batch form.
+"""Window ordering on the GPU -- drop-ins for the reference's
+``memplan.ordering.greedy_order`` / ``exact_order`` plus their batch forms.
 
   OrderingProblem / OrderingSolution / SolverStats   ordering.py:35-66 (same fields)
   greedy_order(p)          ordering.py:126-180  -> rm_greedy_windows (K4), one window
   greedy_orders(problems)  the planner's _pool_map(_solve_window) over every
                            greedy window (planner.py:155-157) as ONE launch
+  exact_order(p)           ordering.py:183-286  -> rm_exact_windows (K5): the
+                           order-ideal DP, exact whenever the reference's
+                           search cannot reach its node cap
+  exact_orders(problems)   every exact window of the planner as ONE launch
 """
 
 from __future__ import annotations
@@ -54,16 +58,13 @@ def _check_problem(p) -> None:
         raise ConfigError("time budget must be positive")
 
 
-def greedy_windows(problems: Sequence) -> list[tuple[tuple[int, ...], int] | Exception]:
-    """K4 over windows that share one graph: [(order, peak) | exception]."""
-    if not problems:
-        return []
+def _window_csr(problems: Sequence, who: str):
+    """Device graph + window / live-in / live-out CSR of problems sharing one graph."""
     from .evaluator import device_graph
     _lib.require_device()
     g = problems[0].graph
     if any(p.graph is not g for p in problems):
-        raise ValueError("greedy_windows: every problem must share one graph")
-    dg = device_graph(g)
+        raise ValueError(f"{who}: every problem must share one graph")
     W = len(problems)
 
     def csr(lists):
@@ -73,9 +74,16 @@ def greedy_windows(problems: Sequence) -> list[tuple[tuple[int, ...], int] | Exc
         idx = np.fromiter((v for x in lists for v in x), np.int64, int(p[-1]))
         return p, idx.astype(np.int32)
 
-    win_ptr, win_ops = csr([sorted(p.ops) for p in problems])
-    lin_ptr, lin_idx = csr([sorted(p.live_in) for p in problems])
-    lout_ptr, lout_idx = csr([sorted(p.live_out) for p in problems])
+    return (device_graph(g), csr([sorted(p.ops) for p in problems]),
+            csr([sorted(p.live_in) for p in problems]), csr([sorted(p.live_out) for p in problems]))
+
+
+def greedy_windows(problems: Sequence) -> list[tuple[tuple[int, ...], int] | Exception]:
+    """K4 over windows that share one graph: [(order, peak) | exception]."""
+    if not problems:
+        return []
+    dg, (win_ptr, win_ops), (lin_ptr, lin_idx), (lout_ptr, lout_idx) = _window_csr(problems, "greedy_windows")
+    W = len(problems)
     order = np.empty(max(len(win_ops), 1), np.int32)
     peak = np.empty(W, np.int64)
     status = np.empty(W, np.int32)
@@ -125,3 +133,79 @@ def greedy_order(p) -> OrderingSolution:
     """Least-memory-increase list scheduling (ordering.py:126-180) on the GPU;
     always flagged non-optimal."""
     return greedy_orders([p])[0]
+
+
+# ------------------------------------------------------------------ exact
+
+NEEDS_SEARCH = object()   # rm_exact_windows status 3: the reference's DFS decides
+
+
+def exact_windows(problems: Sequence) -> list:
+    """K5 over windows that share one graph: per window (order, peak, nodes),
+    NEEDS_SEARCH, or the exception the reference raises."""
+    if not problems:
+        return []
+    dg, (win_ptr, win_ops), (lin_ptr, lin_idx), (lout_ptr, lout_idx) = _window_csr(problems, "exact_windows")
+    W = len(problems)
+    cap = np.array([-1 if p.node_cap is None else int(p.node_cap) for p in problems], np.int64)
+    order = np.empty(max(len(win_ops), 1), np.int32)
+    peak = np.zeros(W, np.int64)
+    nodes = np.zeros(W, np.int64)
+    status = np.empty(W, np.int32)
+    bad = np.empty(W, np.int32)
+    check(lib().rm_exact_windows(dg.handle, W, ptr(win_ptr), ptr(win_ops), ptr(lin_ptr), ptr(lin_idx),
+                                 ptr(lout_ptr), ptr(lout_idx), ptr(cap), ptr(order), ptr(peak),
+                                 ptr(nodes), ptr(status), ptr(bad), None), "rm_exact_windows")
+    out: list = []
+    for w in range(W):
+        if status[w] == 1:
+            out.append(ConfigError(f"live-in tensor {int(bad[w])} has no consumer in the window "
+                                   f"and is not live-out"))
+        elif status[w] == 2:
+            out.append(AssertionError("window precedence contains a cycle"))
+        elif status[w] == 3:
+            out.append(NEEDS_SEARCH)
+        else:
+            a, b = int(win_ptr[w]), int(win_ptr[w + 1])
+            out.append((tuple(order[a:b].tolist()), int(peak[w]), int(nodes[w])))
+    return out
+
+
+def exact_orders(problems: Sequence, search=None, solution_type=OrderingSolution,
+                 stats_type=SolverStats) -> list:
+    """exact_order over many windows (one K5 launch per graph).  Windows whose
+    order ideals outnumber their node cap go to ``search`` (the reference's
+    exact_order when called through the planner plug-in); without one they
+    raise RoamError -- there is no CPU path here.  ``stats.nodes`` is the
+    number of order ideals minus one, an upper bound on the reference DFS's
+    expansions (the plan documents never contain it)."""
+    t0 = time.monotonic()
+    for p in problems:
+        _check_problem(p)
+    res: list = [None] * len(problems)
+    groups: dict[int, list[int]] = {}
+    for k, p in enumerate(problems):
+        groups.setdefault(id(p.graph), []).append(k)
+    for idx in groups.values():
+        for k, r in zip(idx, exact_windows([problems[k] for k in idx])):
+            res[k] = r
+    wall = time.monotonic() - t0
+    out = []
+    for p, r in zip(problems, res):
+        if isinstance(r, Exception):
+            raise r
+        if r is NEEDS_SEARCH:
+            if search is None:
+                raise _lib.RoamError("exact_order: the window has more order ideals than its node cap; "
+                                     "the reference's capped search decides it (pass search=)")
+            out.append(search(p))
+            continue
+        order, peak, nodes = r
+        out.append(solution_type(order=order, peak=peak, optimal=True,
+                                 stats=stats_type(nodes=nodes, wall_time=wall)))
+    return out
+
+
+def exact_order(p, search=None) -> OrderingSolution:
+    """Minimum-peak window order (ordering.py:183-286) on the GPU (K5)."""
+    return exact_orders([p], search=search)[0]

@@ -358,6 +358,84 @@ def make_greedy():
     dump("greedy.json", {"cases": out, "graphs": graphs})
 
 
+# ---------------------------------------------------------------- exact
+
+def random_window(g, rng):
+    """A random op subset of g with its boundary liveness (live_in = consumed
+    inside, produced outside; live_out = produced inside, consumed outside,
+    plus a few extra held outputs)."""
+    n = g.n_ops
+    k = rng.randint(1, min(n, 14))
+    ops = sorted(rng.sample(range(n), k))
+    inside = set(ops)
+    live_in, live_out = set(), set()
+    for t in g.tensors:
+        cons = set(t.consumers)
+        if t.producer not in inside and cons & inside:
+            live_in.add(t.id)
+        if t.producer in inside and cons - inside:
+            live_out.add(t.id)
+        if t.producer in inside and rng.random() < 0.1:
+            live_out.add(t.id)
+    return ops, sorted(live_in), sorted(live_out)
+
+
+def make_exact():
+    """exact_order (ordering.py:183-286) on whole random DAGs, random windows
+    with boundary liveness, the hazard fixtures and the planner's own windows
+    (node_limit 20, node_cap 500k); plus cases whose node cap the search hits
+    (the reference then returns the greedy incumbent, optimal=False)."""
+    out, graphs = [], {}
+
+    def case(name, g, ops, live_in, live_out, node_cap=500_000, doc=None):
+        prob = ro.OrderingProblem(graph=g, ops=tuple(ops), live_in=frozenset(live_in),
+                                  live_out=frozenset(live_out), node_cap=node_cap)
+        sol = ro.exact_order(prob)
+        ent = {"graph": name, "ops": list(ops), "live_in": list(live_in), "live_out": list(live_out),
+               "node_cap": node_cap, "order": list(sol.order), "peak": sol.peak,
+               "optimal": sol.optimal, "nodes": sol.stats.nodes}
+        if doc is not None:
+            ent["doc"] = doc
+        out.append(ent)
+
+    rng = random.Random(7)
+    for k in range(60):
+        g = gen_random_dag(2 + k % 13, density=0.15 + 0.05 * (k % 8), seed=2000 + k)
+        case(f"rand{k}", g, range(g.n_ops), (), (), doc=rg.graph_to_doc(g))
+    for k in range(60):
+        g = gen_random_dag(8 + k % 12, density=0.2 + 0.05 * (k % 6), seed=3000 + k)
+        ops, li, lo = random_window(g, rng)
+        case(f"win{k}", g, ops, li, lo, doc=rg.graph_to_doc(g))
+    for name, doc in edge_docs().items():
+        g = rg.load_graph(doc)
+        case(name, g, range(g.n_ops), (), (), doc=doc)
+    trap = gen_greedy_trap(0)
+    case("greedy_trap0", trap, range(trap.n_ops), (), (), doc=rg.graph_to_doc(trap))
+    # caps the search hits: a 12-op antichain, and a random DAG under a tiny cap
+    anti = {"ops": [{"id": i, "name": f"a{i}", "kind": "forward", "inputs": [], "outputs": [i]}
+                    for i in range(12)] + [{"id": 12, "name": "z", "kind": "forward",
+                                            "inputs": list(range(12)), "outputs": []}],
+            "tensors": [{"id": i, "size_bytes": (i % 5 + 1) * MB} for i in range(12)]}
+    g = rg.load_graph(anti)
+    case("antichain12_cap100", g, range(g.n_ops), (), (), node_cap=100, doc=anti)
+    case("antichain12_nocap", g, range(g.n_ops), (), (), node_cap=None, doc=anti)
+    g = gen_random_dag(14, density=0.2, seed=77)
+    case("rand14_cap20", g, range(g.n_ops), (), (), node_cap=20, doc=rg.graph_to_doc(g))
+    # the planner's exact windows
+    for arch in ("mlp", "residual", "transformer_block"):
+        for blocks in (2, 4):
+            g = gen_training_graph(arch, blocks, optimizer="adam")
+            name = f"{arch}{blocks}"
+            graphs[name] = rg.graph_to_doc(g)
+            tree = rp.build_subgraph_tree(g, 20)
+            lin = rp.linearize(g, tree)
+            wu = rp.place_weight_updates(g, tree, 2.0)
+            for w, prob in ro.build_window_problems(g, lin, wu):
+                if len(prob.ops) <= 20:
+                    case(name, g, sorted(prob.ops), sorted(prob.live_in), sorted(prob.live_out))
+    dump("exact.json", {"cases": out, "graphs": graphs})
+
+
 def make_plans():
     docs = {"diamond": diamond_doc()}
     for arch in ("mlp", "residual", "transformer_block"):
@@ -372,7 +450,7 @@ def make_plans():
 
 
 if __name__ == "__main__":
-    which = set(sys.argv[1:]) or {"peaks", "schedules", "layouts", "greedy", "plans"}
-    for w in ("peaks", "schedules", "layouts", "greedy", "plans"):
+    which = set(sys.argv[1:]) or {"peaks", "schedules", "layouts", "greedy", "exact", "plans"}
+    for w in ("peaks", "schedules", "layouts", "greedy", "exact", "plans"):
         if w in which:
             globals()[f"make_{w}"]()

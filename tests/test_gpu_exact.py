@@ -1,0 +1,120 @@
+"""K5 (batched exact window ordering, the order-ideal DP) against the
+reference's golden exact_order vectors (tests/golden/exact.json: whole random
+DAGs, random windows with boundary liveness, the hazard fixtures, the greedy
+trap, the planner's own exact windows, and windows whose node cap the
+reference's search hits) and against the oracle DP on larger windows."""
+
+from __future__ import annotations
+
+import random
+
+import pytest
+
+from conftest import golden
+from oracle import memplan_oracle as O
+from paper_2310_19295_b200 import graphgen as gg
+from paper_2310_19295_b200._lib import RoamError
+from paper_2310_19295_b200.graph import ConfigError, load_graph
+from paper_2310_19295_b200.ordering import (NEEDS_SEARCH, OrderingProblem, exact_order, exact_orders,
+                                            exact_windows)
+
+pytestmark = pytest.mark.gpu
+
+
+def _cases():
+    G = golden("exact")
+    graphs = {}
+    for c in G["cases"]:
+        key = c["graph"] if "doc" not in c else id(c)
+        if key not in graphs:
+            graphs[key] = load_graph(c["doc"] if "doc" in c else G["graphs"][c["graph"]])
+        yield graphs[key], c
+
+
+def _problem(g, c):
+    return OrderingProblem(g, tuple(c["ops"]), frozenset(c["live_in"]), frozenset(c["live_out"]),
+                           node_cap=c["node_cap"])
+
+
+def test_golden_windows():
+    decided = 0
+    for g, c in _cases():
+        r = exact_windows([_problem(g, c)])[0]
+        if r is NEEDS_SEARCH:
+            # only when the reference's DFS could reach its cap
+            assert c["node_cap"] is not None and len(c["ops"]) > 0
+            continue
+        decided += 1
+        assert c["optimal"], c["graph"]
+        order, peak, nodes = r
+        assert (list(order), peak) == (c["order"], c["peak"]), c["graph"]
+        assert c["nodes"] <= max(nodes, 0)
+    assert decided >= 185
+
+
+def test_cap_hit_windows_go_back_to_the_search():
+    hit = [(g, c) for g, c in _cases() if not c["optimal"]]
+    assert hit
+    for g, c in hit:
+        assert exact_windows([_problem(g, c)])[0] is NEEDS_SEARCH
+        with pytest.raises(RoamError):
+            exact_order(_problem(g, c))
+        # with the reference's search as the fallback the answer is its own
+        sol = exact_order(_problem(g, c), search=lambda p: ("searched", p.node_cap))
+        assert sol == ("searched", c["node_cap"])
+
+
+def test_golden_batched_one_launch_per_graph():
+    cases = list(_cases())
+    sols = exact_orders([_problem(g, c) for g, c in cases], search=lambda p: None)
+    for (g, c), s in zip(cases, sols):
+        if s is None:
+            assert not c["optimal"] or c["node_cap"] is not None
+            continue
+        assert (list(s.order), s.peak, s.optimal) == (c["order"], c["peak"], True), c["graph"]
+
+
+def _random_window(g, rng, k):
+    ops = sorted(rng.sample(range(len(g.ops)), k))
+    inside = set(ops)
+    li, lo = set(), set()
+    for t in g.tensors:
+        cons = set(t.consumers)
+        if t.producer not in inside and cons & inside:
+            li.add(t.id)
+        if t.producer in inside and cons - inside:
+            lo.add(t.id)
+    return ops, li, lo
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_large_windows_vs_oracle_dp(seed):
+    """14..18-op windows (V in global memory past 2^13 masks) of the config
+    graphs and of dense random DAGs."""
+    rng = random.Random(seed)
+    graphs = [load_graph(gg.config_doc("gpt2-small")), load_graph(gg.config_doc("layered"))]
+    probs, want = [], []
+    for g in graphs:
+        for _ in range(6):
+            k = rng.randint(14, 18)
+            start = rng.randrange(0, len(g.ops) - 40)
+            ops = sorted(rng.sample(range(start, start + 40), k))   # nearby ops: real precedence
+            inside = set(ops)
+            li = {t.id for t in g.tensors if t.producer not in inside and set(t.consumers) & inside}
+            lo = {t.id for t in g.tensors if t.producer in inside and set(t.consumers) - inside}
+            probs.append(OrderingProblem(g, tuple(ops), frozenset(li), frozenset(lo)))
+            want.append(O.exact_order_dp(g, ops, li, lo))
+    got = exact_windows([p for p in probs if p.graph is graphs[0]]) + \
+        exact_windows([p for p in probs if p.graph is graphs[1]])
+    for r, w in zip(got, want):
+        assert r is not NEEDS_SEARCH
+        assert (r[0], r[1], r[2] + 1) == w
+
+
+def test_config_error_and_empty_window():
+    g = load_graph(golden("peaks")["fixtures"]["diamond"])
+    # live-in tensor 0 with no consumer inside window {2..3}? tensor 0 is consumed by op 2
+    with pytest.raises(ConfigError):
+        exact_order(OrderingProblem(g, (3,), frozenset({0}), frozenset()))
+    sol = exact_order(OrderingProblem(g, (), frozenset({1}), frozenset({1})))
+    assert (sol.order, sol.peak, sol.optimal) == ((), 20 << 20, True)

@@ -45,6 +45,11 @@ def test_device_entry_points_fail_loudly_without_gpu():
         evaluate_orders(g, np.array([[0, 2, 1, 3]], np.int32))
     with pytest.raises(_lib.RoamError):
         peak_memory(g, Schedule((0, 2, 1, 3), (0, 2, 1, 3)))
+    from paper_2310_19295_b200.ordering import OrderingProblem, exact_order, greedy_order
+    with pytest.raises(_lib.RoamError):
+        exact_order(OrderingProblem(g, (0, 1, 2, 3)))
+    with pytest.raises(_lib.RoamError):
+        greedy_order(OrderingProblem(g, (0, 1, 2, 3)))
 
 
 def k1_numpy(meta: dict, n: int, order) -> tuple[int, int, bool]:

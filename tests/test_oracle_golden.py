@@ -163,3 +163,27 @@ def test_greedy_matches_reference():
 def test_first_strict_min():
     assert O.first_strict_min([5, 3, 3, 1], [True, True, True, False]) == (3, 1)
     assert O.first_strict_min([5], [False]) == (None, -1)
+
+
+def exact_cases():
+    G = golden("exact")
+    graphs = {k: load_graph(v) for k, v in G["graphs"].items()}
+    for c in G["cases"]:
+        yield (load_graph(c["doc"]) if "doc" in c else graphs[c["graph"]]), c
+
+
+def test_exact_dp_matches_reference():
+    """The order-ideal DP reproduces exact_order wherever the
+    reference's search cannot hit its node cap (#ideals - 1 <= cap), and every
+    case where the reference did hit it has more ideals than the cap."""
+    decided = 0
+    for g, c in exact_cases():
+        dp = O.exact_order_dp(g, c["ops"], c["live_in"], c["live_out"], c["node_cap"])
+        if dp is None:
+            assert c["node_cap"] is not None
+            continue
+        decided += 1
+        assert c["optimal"], c["graph"]
+        assert (list(dp[0]), dp[1]) == (c["order"], c["peak"]), c["graph"]
+        assert c["nodes"] <= dp[2] - 1            # each ideal expanded at most once
+    assert decided >= 185
