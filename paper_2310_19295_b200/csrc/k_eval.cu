@@ -20,6 +20,9 @@
 //          readback pos[o_k] == k (permutation), running max/first argmax,
 //          group exclusive scan of chunk totals, (max, min-index) reduction.
 #include <climits>
+#include <cstring>
+
+#include <cstdlib>
 
 #include "k_common.cuh"
 
@@ -630,76 +633,113 @@ static int eval_impl(RmGraph* g, const void* orders, int64_t B, uint32_t flags, 
     return launch_argmin(peak, valid, B, id_base, best, s);
   }
 
-  // Host buffers: chunked pipeline -- H2D of chunk i+1 on a copy stream
-  // overlaps K1 on chunk i; results come back with one D2H per chunk.
+  // Host buffers: chunked pipeline -- every chunk's H2D is queued back to back
+  // on a copy stream (device rows for the whole batch, no buffer reuse waits),
+  // K1 on chunk i waits only for chunk i's copy; results come back through a
+  // pinned staging buffer in one D2H each.
   const int64_t n = g->n;
   const int64_t esz = u16 ? 2 : 4;
   const int64_t row_bytes = std::max<int64_t>(esz * n, 4);
-  // ~8 MB chunks: the copy engine streams chunk i+1 while K1 runs on chunk i
-  int64_t chunk = std::max<int64_t>(1, (int64_t(8) << 20) / row_bytes);
-  chunk = std::min(chunk, std::max<int64_t>(B, 1));
-  // per-thread copy stream and events, created once (re-entrant: calls on
-  // different threads never share them)
+  // chunks of ~16 MB, halving towards the end of the batch so that the K1
+  // launch left after the last copy is short (ROAM_STAGE_CHUNK_KB overrides
+  // the first size, for measurement)
+  static const int64_t chunk_bytes = [] {
+    const char* e = std::getenv("ROAM_STAGE_CHUNK_KB");
+    const long long kb = e ? std::atoll(e) : 0;
+    return kb > 0 ? int64_t(kb) << 10 : int64_t(16) << 20;
+  }();
+  std::vector<std::pair<int64_t, int64_t>> chunks;  // (first row, rows)
+  {
+    int64_t cur = std::max<int64_t>(1, chunk_bytes / row_bytes);
+    const int64_t floor_rows = std::max<int64_t>(1, (int64_t(1) << 20) / row_bytes);
+    for (int64_t b0 = 0; b0 < B;) {
+      const int64_t rem = B - b0;
+      while (rem < 2 * cur && cur > floor_rows) cur = std::max(floor_rows, cur / 2);
+      const int64_t nb = std::min(cur, rem);
+      chunks.emplace_back(b0, nb);
+      b0 += nb;
+    }
+  }
+  const int64_t n_chunks = (int64_t)chunks.size();
+  // per-thread copy stream, events and pinned result staging, created once
+  // (re-entrant: calls on different threads never share them)
   struct CopyCtx {
     int dev = -1;
     cudaStream_t cs = nullptr;
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    std::vector<cudaEvent_t> ev;
+    unsigned char* pinned = nullptr;
+    size_t pinned_bytes = 0;
   };
   static thread_local CopyCtx ctx;
   if (ctx.dev != g->device) {
     RM_CUDA(cudaStreamCreateWithFlags(&ctx.cs, cudaStreamNonBlocking));
-    for (auto& e : ctx.ev) RM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx.ev.clear();
     ctx.dev = g->device;
+  }
+  while ((int64_t)ctx.ev.size() < n_chunks + 1) {
+    cudaEvent_t e;
+    RM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx.ev.push_back(e);
+  }
+  const size_t res_bytes = size_t(B) * 13 + 16;  // peak, argmax, valid, best
+  if (ctx.pinned_bytes < res_bytes) {
+    if (ctx.pinned) cudaFreeHost(ctx.pinned);
+    ctx.pinned = nullptr;
+    ctx.pinned_bytes = 0;
+    RM_CUDA(cudaMallocHost(&ctx.pinned, res_bytes));
+    ctx.pinned_bytes = res_bytes;
   }
   cudaStream_t cs = ctx.cs;
   Scratch sc(s);
-  unsigned char* d_ord[2];
+  unsigned char* d_ord;
   int64_t* d_peak;
   int32_t* d_arg;
   uint8_t* d_val;
-  RM_CUDA(sc.alloc(&d_ord[0], size_t(chunk * n * esz)));
-  RM_CUDA(sc.alloc(&d_ord[1], size_t(chunk * n * esz)));
+  RM_CUDA(sc.alloc(&d_ord, size_t(std::max<int64_t>(B, 1) * n * esz)));
   RM_CUDA(sc.alloc(&d_peak, size_t(B)));
   RM_CUDA(sc.alloc(&d_arg, size_t(B)));
   RM_CUDA(sc.alloc(&d_val, size_t(B)));
   int64_t* d_best;
   RM_CUDA(sc.alloc(&d_best, 2));
-  cudaEvent_t copied[2] = {ctx.ev[0], ctx.ev[1]}, consumed[2] = {ctx.ev[2], ctx.ev[3]};
   // the allocations above are ordered on s; the copy stream must see them
-  RM_CUDA(cudaEventRecord(consumed[0], s));
-  RM_CUDA(cudaEventRecord(consumed[1], s));
+  RM_CUDA(cudaEventRecord(ctx.ev[n_chunks], s));
+  RM_CUDA(cudaStreamWaitEvent(cs, ctx.ev[n_chunks], 0));
+  for (int64_t k = 0; k < n_chunks; ++k) {
+    const int64_t b0 = chunks[k].first, nb = chunks[k].second;
+    RM_CUDA(cudaMemcpyAsync(d_ord + b0 * n * esz, static_cast<const unsigned char*>(orders) + b0 * n * esz,
+                            size_t(nb * n * esz), cudaMemcpyHostToDevice, cs));
+    RM_CUDA(cudaEventRecord(ctx.ev[k], cs));
+  }
   int rc = RM_OK;
-  int64_t k = 0;
-  for (int64_t b0 = 0; b0 < B && rc == RM_OK; b0 += chunk, ++k) {
-    const int64_t nb = std::min(chunk, B - b0);
-    const int i = int(k & 1);
-    cudaStreamWaitEvent(cs, consumed[i], 0);
-    cudaMemcpyAsync(d_ord[i], static_cast<const unsigned char*>(orders) + b0 * n * esz,
-                    size_t(nb * n * esz), cudaMemcpyHostToDevice, cs);
-    cudaEventRecord(copied[i], cs);
-    cudaStreamWaitEvent(s, copied[i], 0);
-    rc = launch_k1(g, d_ord[i], nb, d_peak + b0, d_arg + b0, d_val + b0, s, u16);
-    cudaEventRecord(consumed[i], s);
+  for (int64_t k = 0; k < n_chunks && rc == RM_OK; ++k) {
+    const int64_t b0 = chunks[k].first, nb = chunks[k].second;
+    cudaStreamWaitEvent(s, ctx.ev[k], 0);
+    rc = launch_k1(g, d_ord + b0 * n * esz, nb, d_peak + b0, d_arg + b0, d_val + b0, s, u16);
   }
-  if (rc == RM_OK && best) {
-    if (B > 0) {
-      rc = launch_argmin(d_peak, d_val, B, id_base, d_best, s);
-      if (rc == RM_OK) cudaMemcpyAsync(best, d_best, 16, cudaMemcpyDeviceToHost, s);
-    } else {
-      best[0] = INT64_MAX;
-      best[1] = -1;
-    }
+  unsigned char* hp = ctx.pinned;
+  if (rc == RM_OK && best && B > 0) {
+    rc = launch_argmin(d_peak, d_val, B, id_base, d_best, s);
+    if (rc == RM_OK) cudaMemcpyAsync(hp + size_t(B) * 13, d_best, 16, cudaMemcpyDeviceToHost, s);
   }
-  if (rc == RM_OK) {
-    cudaMemcpyAsync(peak, d_peak, size_t(B) * 8, cudaMemcpyDeviceToHost, s);
-    cudaMemcpyAsync(argmax, d_arg, size_t(B) * 4, cudaMemcpyDeviceToHost, s);
-    cudaMemcpyAsync(valid, d_val, size_t(B), cudaMemcpyDeviceToHost, s);
+  if (rc == RM_OK && B > 0) {
+    cudaMemcpyAsync(hp, d_peak, size_t(B) * 8, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(hp + size_t(B) * 8, d_arg, size_t(B) * 4, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(hp + size_t(B) * 12, d_val, size_t(B), cudaMemcpyDeviceToHost, s);
   }
   cudaError_t e = cudaStreamSynchronize(s);
   cudaError_t e2 = cudaStreamSynchronize(cs);
   if (e == cudaSuccess) e = e2;
   if (rc != RM_OK) return rc;
   if (e != cudaSuccess) return cuda_fail(e, "rm_eval_orders");
+  if (B > 0) {
+    std::memcpy(peak, hp, size_t(B) * 8);
+    std::memcpy(argmax, hp + size_t(B) * 8, size_t(B) * 4);
+    std::memcpy(valid, hp + size_t(B) * 12, size_t(B));
+    if (best) std::memcpy(best, hp + size_t(B) * 13, 16);
+  } else if (best) {
+    best[0] = INT64_MAX;
+    best[1] = -1;
+  }
   return RM_OK;
 }
 
