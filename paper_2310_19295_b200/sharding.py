@@ -93,9 +93,11 @@ class ShardResult:
     local_valid: int
 
 
-def evaluate_sharded(g, total: int, seed: int = 0, group=None, stream=None) -> ShardResult:
+def evaluate_sharded(g, total: int, seed: int = 0, group=None, stream=None,
+                     chunk: int = 1 << 16) -> ShardResult:
     """Generate this rank's candidate ids on its device (counter-RNG Kahn),
-    evaluate them with K1, take the local first strict minimum on device and
+    evaluate them with K1 and keep the first strict minimum on the device,
+    ``chunk`` candidates at a time (rows never exceed chunk x n in HBM), then
     exchange it: the 8-GPU candidate search of BASELINE config 5."""
     import torch
     import torch.distributed as dist
@@ -105,10 +107,18 @@ def evaluate_sharded(g, total: int, seed: int = 0, group=None, stream=None) -> S
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     lo, hi = shard_range(total, world, rank)
     dev = torch.device("cuda", torch.cuda.current_device())
-    orders = ev.generate_orders(g, seed, lo, hi - lo, device=dev, stream=stream)
-    peak, _, valid = ev.evaluate_orders(g, orders, stream=stream)
-    best = ev.select_device(peak, valid, id_base=lo, stream=stream)
+    best = torch.tensor([NONE_PEAK, -1], dtype=torch.int64, device=dev)
+    n_valid = torch.zeros((), dtype=torch.int64, device=dev)
+    for c0 in range(lo, hi, max(1, chunk)):
+        nb = min(chunk, hi - c0)
+        orders = ev.generate_orders(g, seed, c0, nb, device=dev, stream=stream)
+        peak, _, valid = ev.evaluate_orders(g, orders, stream=stream)
+        cb = ev.select_device(peak, valid, id_base=c0, stream=stream)
+        n_valid += valid.sum()
+        # chunks arrive in id order: a later chunk wins only with a strictly smaller peak
+        take = (cb[1] >= 0) & ((best[1] < 0) | (cb[0] < best[0]))
+        best = torch.where(take, cb, best)
     if world > 1:
         best = allgather_best(best, group)
     b = [int(x) for x in best.cpu().tolist()]
-    return ShardResult(b[0], b[1], (lo, hi), int(valid.sum().item()))
+    return ShardResult(b[0], b[1], (lo, hi), int(n_valid.item()))
