@@ -49,7 +49,7 @@ struct K1V4Args {
 
 template <int C>
 struct V4Geom {
-  static constexpr int L = C == 4 ? 2 : C == 8 ? 3 : 4;
+  static constexpr int L = C == 4 ? 2 : C == 8 ? 3 : C == 16 ? 4 : C == 32 ? 5 : 6;
   static constexpr int STRIDE = C + 2;  // (STRIDE / 2) odd: conflict-free LDS.128 rows
 };
 
@@ -63,8 +63,30 @@ __device__ __forceinline__ unsigned simd_gt(unsigned v, unsigned u, unsigned nm)
   return ((v | 0x80008000u) - u - 0x00010001u) | nm;
 }
 
+// C = 32 instances cap the CTA at 512 threads: 128 registers hold the
+// 32-position row and the other register-resident lists
+__host__ __device__ constexpr int v4_cta_cap(int c) { return c == 64 ? 256 : c == 32 ? 512 : 1024; }
+
+// scan-layout word offset of position tid + j*NT relative to that of tid
+// (NT a multiple of C, or C a multiple of NT)
+template <int NT, int C>
+__device__ constexpr int v4_xs_off(int j) {
+  return ((j * NT) >> V4Geom<C>::L) * V4Geom<C>::STRIDE + ((j * NT) & (C - 1));
+}
+
+// group barrier; a one-warp group only needs the warp's own
+template <int NT>
+__device__ __forceinline__ void v4_bar(int id) {
+  if constexpr (NT == 32) __syncwarp(); else gbar(id, NT);
+}
+template <int NT>
+__device__ __forceinline__ unsigned v4_bar_or(int id, unsigned p) {
+  if constexpr (NT == 32) return __any_sync(0xffffffffu, p) ? 1u : 0u;
+  else return (unsigned)gbar_or(id, NT, (int)p);
+}
+
 template <typename RowT, int NT, int C>
-__global__ void __launch_bounds__((1024 / NT) * NT, 1) k1v4_eval_orders(const K1V4Args a) {
+__global__ void __launch_bounds__((v4_cta_cap(C) / NT) * NT, 1) k1v4_eval_orders(const K1V4Args a) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int SL = NT * C;
   constexpr int Q = SL / 8;                 // 8-id chunks
@@ -72,7 +94,6 @@ __global__ void __launch_bounds__((1024 / NT) * NT, 1) k1v4_eval_orders(const K1
   constexpr bool QFULL = (Q % NT) == 0;
   constexpr int NWARPS = NT / 32;
   using X = V4Geom<C>;
-  constexpr int XS_STEP = (NT / C) * X::STRIDE;
   const int n = a.n;
   const RowT* orders = static_cast<const RowT*>(a.orders);
   {
@@ -82,7 +103,7 @@ __global__ void __launch_bounds__((1024 / NT) * NT, 1) k1v4_eval_orders(const K1
       for (size_t i = threadIdx.x; i < bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
     };
     cp16(a.opv, 0, align16(8 * size_t(SL + 1)));
-    if (a.n_edges != 4 * NT) cp16(a.edges, a.off_edges, 4 * size_t(a.n_edges));
+    if (a.n_edges > (C / 4) * NT) cp16(a.edges, a.off_edges, 4 * size_t(a.n_edges));
     cp16(a.mpair, a.off_mpair, align16(4 * size_t(a.n_pair)));
     cp16(a.mptr, a.off_mptr, align16(4 * size_t(a.n_gen + 1)));
     cp16(a.mcons, a.off_mcons, align16(2 * size_t(a.n_mcons)));
@@ -112,23 +133,20 @@ __global__ void __launch_bounds__((1024 / NT) * NT, 1) k1v4_eval_orders(const K1
   long long* xs_w = xs + (tid >> X::L) * X::STRIDE + (tid & (C - 1));
   const int n_edges = a.n_edges, n_pair = a.n_pair, n_gen = a.n_gen;
   // the generic edges stay in registers when there are exactly 4 per thread
-  const bool ereg = n_edges == 4 * NT;
-  uint32_t er[4] = {0u, 0u, 0u, 0u};
-  if (ereg) {
+  constexpr int ER = C / 4;  // list entries per thread kept in registers
+  const int ek = n_edges / NT;         // a multiple of 4
+  const bool ereg = ek <= ER;
+  uint32_t er[ER];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) er[i] = __ldg(a.edges + tid + i * NT);
-  }
+  for (int i = 0; i < ER; ++i) er[i] = (ereg && i < ek) ? __ldg(a.edges + tid + i * NT) : 0u;
   // likewise the two-consumer tensors when there are at most 4 per thread
   const int pk = n_pair / NT;
-  const bool preg = pk <= 4;
-  uint32_t pw[4] = {0u, 0u, 0u, 0u}, pu[4] = {0u, 0u, 0u, 0u};
-  if (preg) {
+  const bool preg = pk <= ER;
+  uint32_t pw[ER], pu[ER];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (i < pk) {
-        pw[i] = __ldg(a.mpair + tid + i * NT);
-        pu[i] = __ldg(a.msz + tid + i * NT);
-      }
+  for (int i = 0; i < ER; ++i) {
+    pw[i] = (preg && i < pk) ? __ldg(a.mpair + tid + i * NT) : 0u;
+    pu[i] = (preg && i < pk) ? __ldg(a.msz + tid + i * NT) : 0u;
   }
   uint32_t em[QR];  // edge masks of this thread's chunks (ids 8q..8q+9)
 #pragma unroll
@@ -137,7 +155,7 @@ __global__ void __launch_bounds__((1024 / NT) * NT, 1) k1v4_eval_orders(const K1
     em[r] = (QFULL || q < Q) ? __ldg(a.em + q) : 0xff00ff00u;
   }
   for (int i = tid; i < (SL + 8) / 2; i += NT) reinterpret_cast<uint32_t*>(pos)[i] = 0x80008000u;
-  gbar(bar_id, NT);
+  v4_bar<NT>(bar_id);
 
   uint32_t v[C];
   auto load_row = [&](int64_t cc) {
@@ -157,7 +175,7 @@ __global__ void __launch_bounds__((1024 / NT) * NT, 1) k1v4_eval_orders(const K1
       v[j] = min(v[j], (uint32_t)SL);
       pos[v[j]] = (uint16_t)(tid + j * NT);
     }
-    gbar(bar_id, NT);
+    v4_bar<NT>(bar_id);
     // ---- P2a (id-major): missing ids (sentinel) and the (u, u+1), (u, u+2) edges
     unsigned sent = 0, ok = 0xffffffffu;
 #pragma unroll
@@ -184,7 +202,8 @@ __global__ void __launch_bounds__((1024 / NT) * NT, 1) k1v4_eval_orders(const K1
     int e_first = tid;
     if (ereg) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) eacc |= (int)lds_u16(posb, er[i] >> 16) - (int)lds_u16(posb, er[i] & 0xffffu) - 1;
+      for (int i = 0; i < ER; ++i)
+        if (i < ek) eacc |= (int)lds_u16(posb, er[i] >> 16) - (int)lds_u16(posb, er[i] & 0xffffu) - 1;
       e_first = n_edges;
     }
     for (int e0 = e_first; e0 < n_edges; e0 += 4 * NT) {
@@ -196,12 +215,12 @@ __global__ void __launch_bounds__((1024 / NT) * NT, 1) k1v4_eval_orders(const K1
     }
     // ---- P2a (position-major): {fs, out} units of the op at each position
 #pragma unroll
-    for (int j = 0; j < C; ++j) xs_w[j * XS_STEP] = opv[v[j]];
+    for (int j = 0; j < C; ++j) xs_w[v4_xs_off<NT, C>(j)] = opv[v[j]];
     unsigned bad = ((sent & 0x80008000u) != 0) | ((ok & 0x80008000u) != 0x80008000u) | (eacc < 0);
     // prefetch the next candidate's row; it lands while P2b / P3 run
     const int64_t cn = c + cstride;
     if (cn < a.B) load_row(cn);
-    gbar(bar_id, NT);
+    v4_bar<NT>(bar_id);
     // ---- P2b: multi-consumer tensors free after their latest maximal consumer
     // (positions of a broken row may be the sentinel: clamp into the group)
     auto add_free = [&](unsigned kmax, unsigned units) {
@@ -211,7 +230,7 @@ __global__ void __launch_bounds__((1024 / NT) * NT, 1) k1v4_eval_orders(const K1
     int m_first = tid;
     if (preg) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < ER; ++i)
         if (i < pk) add_free(max(lds_u16(posb, pw[i] & 0xffffu), lds_u16(posb, pw[i] >> 16)), pu[i]);
       m_first = n_pair;
     }
@@ -225,7 +244,7 @@ __global__ void __launch_bounds__((1024 / NT) * NT, 1) k1v4_eval_orders(const K1
       for (int q = q0; q < q1; ++q) kmax = max(kmax, (unsigned)pos[mcons[q]]);
       add_free(kmax, msz[n_pair + m]);
     }
-    gbar(bar_id, NT);
+    v4_bar<NT>(bar_id);
     // ---- P3: reset this thread's ids to the sentinel for the next candidate
 #pragma unroll
     for (int r = 0; r < QR; ++r) {
@@ -262,7 +281,7 @@ __global__ void __launch_bounds__((1024 / NT) * NT, 1) k1v4_eval_orders(const K1
       if (lane >= d) incl += t;
     }
     if (lane == 31) red_t[warp] = incl;
-    bad = gbar_or(bar_id, NT, bad);
+    bad = v4_bar_or<NT>(bar_id, bad);
     long long off = incl - run;
 #pragma unroll
     for (int w = 0; w < NWARPS - 1; ++w)
@@ -279,7 +298,7 @@ __global__ void __launch_bounds__((1024 / NT) * NT, 1) k1v4_eval_orders(const K1
       red_c[warp] = (long long)(((unsigned long long)(unsigned)mh << 32) | ml);
       red_i[warp] = (int)mi;
     }
-    gbar(bar_id, NT);
+    v4_bar<NT>(bar_id);
     if (tid == 0) {
       long long bv = red_c[0];
       int bk = red_i[0];
@@ -346,6 +365,13 @@ static int launch_k1v4_nt(K1V4Args& a, int NT, int C, int grid, size_t smem, cud
   RM_K1V4_CASE(640, 16)
   RM_K1V4_CASE(768, 16)
   RM_K1V4_CASE(1024, 16)
+  RM_K1V4_CASE(32, 32)
+  RM_K1V4_CASE(64, 32)
+  RM_K1V4_CASE(128, 32)
+  RM_K1V4_CASE(256, 32)
+  RM_K1V4_CASE(32, 64)
+  RM_K1V4_CASE(64, 64)
+  RM_K1V4_CASE(128, 64)
 #undef RM_K1V4_CASE
   return 1;
 }
@@ -389,7 +415,7 @@ int launch_k1v4(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, in
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   const size_t avail = max_smem > (int)a.off_groups ? size_t(max_smem) - a.off_groups : 0;
   int G = (int)(avail / a.group_bytes);
-  G = std::min(G, 1024 / NT);
+  G = std::min(G, (C == 64 ? 256 : C == 32 ? 512 : 1024) / NT);
   G = std::min(G, 15);
   if (G < 1) return 1;
   const int64_t sms = sm_count(dev);

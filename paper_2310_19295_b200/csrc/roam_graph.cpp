@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <atomic>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <unordered_map>
@@ -146,9 +147,26 @@ static void build_k1v2_host(RmGraph& g, const std::vector<int64_t>& out,
 }
 
 // K1 v4 geometry: the smallest slot count SL = NT * C >= n among the compiled
-// instances (k_eval_v4.cu launch table); C = 8 positions per thread up to 1k
-// ops, 16 beyond.
+// instances (k_eval_v4.cu launch table).  C positions per thread: 8 up to 1k
+// ops, 32 up to 2k (two-warp groups, 128 registers: measured fastest on
+// GPT-2 small, 0.084 vs 0.090 ms per 16k candidates), 16 beyond (32 would
+// halve the resident warps once a group's shared memory grows).
+// ROAM_K1_C=16|32|64 forces C where an instance exists (A/B runs).
 static bool k1v4_geometry(int n, int& NT, int& C) {
+  static const int cenv = [] {
+    const char* e = std::getenv("ROAM_K1_C");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int want = cenv ? cenv : (n > 1024 && n <= 2048 ? 32 : 0);
+  if (want == 32 || want == 64) {
+    static const int nts[] = {32, 64, 128, 256};
+    for (int nt : nts)
+      if (nt * want >= n && (want == 32 || nt <= 128)) {
+        NT = nt;
+        C = want;
+        return true;
+      }
+  }
   static const int nt8[] = {32, 64, 96, 128};
   static const int nt16[] = {64, 96, 128, 160, 192, 256, 320, 384, 512, 640, 768, 1024};
   if (n <= 128) {
