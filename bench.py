@@ -4,8 +4,9 @@ One step = one pass of the hot path over one batch: K1 evaluates B candidate
 operator orders of the named training graph (peak memory of each, as
 reference peak_memory(g, sequential_schedule(g, o)) -- graph.py:401-468) and
 selects the first strict minimum (planner.py:209-216); with N>1 GPUs each rank
-evaluates its own contiguous id range (weak scaling) and the per-rank best
-(peak, id) is exchanged with one NCCL all_gather.
+evaluates its own contiguous id range (weak scaling) and the per-rank best is
+exchanged with one 8-byte NCCL all_reduce(MIN) of a packed (peak, id) key on a
+side stream, overlapping the next step's K1 (which leaves one SM idle for it).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config gpt2-small]
   python bench.py --impl reference ...   # the reference algorithm on host cores
@@ -13,8 +14,11 @@ evaluates its own contiguous id range (weak scaling) and the per-rank best
 Default workload: BASELINE config 2, GPT-2 small fwd+bwd+Adam training graph
 (batch 8, seq 1024), 16,384 candidates per GPU.  Candidates are counter-RNG
 Kahn orders (seed 0, ids rank*B ...), generated on device before timing
-(generation timed separately).  L2 is flushed (512 MiB write) between timed
-steps; each step is timed with CUDA events on the launching stream.
+(generation timed separately).  Three copies of the batch rotate between
+steps (inputs larger than L2, no flush needed); the K steps are one CUDA-event
+interval on the launching stream, from after the barrier to after the last
+exchange, max over ranks; K1's own launches are timed per step for the
+roofline.
 """
 
 from __future__ import annotations
@@ -221,62 +225,82 @@ def main() -> None:
     g1.record()
     torch.cuda.synchronize()
     gen_ms = g0.elapsed_time(g1)
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    # three copies of the batch rotate between steps (3 x B*n*4 bytes, 372 MB
+    # for GPT-2 small, against a 126 MB L2): every step reads its rows from
+    # HBM, with no L2 flush inside the timed region
+    bufs = [orders] + [orders.clone() for _ in range(2)]
+    l2_note = (f"inputs larger than L2: {len(bufs)} copies of the batch "
+               f"({len(bufs) * B * n * 4 / 1e6:.0f} MB) rotate between steps")
 
     # selection: packed (peak << id_bits) | id key + ONE 8-byte all_reduce(MIN)
     # when the bits fit (they do for every config graph), else the 16-byte
-    # all_gather of {peak, id}
+    # all_gather of {peak, id}.  With N > 1 the exchange runs on a side stream
+    # while the next step's K1 runs; K1 leaves one SM idle for its kernel.
     id_bits = key_bits(world * B)
     use_key = info["total_bytes"] < (1 << (63 - id_bits))
+    side = torch.cuda.Stream(device=dev) if world > 1 else None
+    if world > 1:
+        ev.set_sm_reserve(1)
 
-    def select(peak, val):
-        if use_key:
-            key = ev.select_key_device(g, peak, val, first_id, id_bits)  # argmin kernel
-            if world > 1:
-                allreduce_key(key)
-            return key
-        best = ev.select_device(peak, val, first_id)                    # argmin kernel
-        if world > 1:
-            best = allgather_best(best)                                 # 16 B per rank
-        return best
+    def exchange(local):
+        if world == 1:
+            return local
+        done = torch.cuda.Event()
+        done.record(stream)
+        side.wait_event(done)
+        with torch.cuda.stream(side):
+            local.record_stream(side)
+            return allreduce_key(local) if use_key else allgather_best(local)   # 8 / 16 B per rank
 
     def to_pair(best) -> list[int]:
         v = [int(x) for x in best.cpu().tolist()]
         return list(decode_key(v[0], id_bits)) if use_key else v
 
-    def step():
-        peak, arg, val = ev.evaluate_orders(g, orders)          # K1
-        return select(peak, val)
+    def evaluate(i):
+        """K1 over batch i with the rank's first strict minimum: the packed key
+        reduced inside the K1 launch, else K1 + the argmin kernel."""
+        rows = bufs[i % len(bufs)]
+        if use_key:
+            peak, arg, val, local = ev.evaluate_select_key(g, rows, first_id, id_bits)
+        else:
+            peak, arg, val = ev.evaluate_orders(g, rows)
+            local = ev.select_device(peak, val, first_id)
+        return peak, val, local
 
-    for _ in range(args.warmup):
-        step()
+    def step(i):
+        return exchange(evaluate(i)[2])
+
+    for i in range(args.warmup):
+        step(i)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
 
     K = args.steps
-    ev_s = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
-    ev_k1 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
-    ev_e = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ev_k1s = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ev_k1e = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ev_start, ev_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sampler = ClockSampler(local)
     launches0 = ev.launch_count()
     with sampler:
+        ev_start.record(stream)
         for i in range(K):
-            flush.zero_()                                        # untimed: L2 flush
-            ev_s[i].record(stream)
-            peak, arg, val = ev.evaluate_orders(g, orders)
-            ev_k1[i].record(stream)
-            best = select(peak, val)
-            ev_e[i].record(stream)
+            ev_k1s[i].record(stream)
+            peak, val, local = evaluate(i)
+            ev_k1e[i].record(stream)
+            best = exchange(local)
+        if side is not None:
+            stream.wait_stream(side)
+        ev_end.record(stream)
         torch.cuda.synchronize()
     launches = ev.launch_count() - launches0
     if world > 1:
         dist.barrier()
+        ev.set_sm_reserve(0)
     torch.cuda.synchronize()
-    step_ms = [ev_s[i].elapsed_time(ev_e[i]) for i in range(K)]
-    k1_ms = [ev_s[i].elapsed_time(ev_k1[i]) for i in range(K)]
-    tot_ms = sum(step_ms)
+    k1_ms = [ev_k1s[i].elapsed_time(ev_k1e[i]) for i in range(K)]
+    tot_ms = ev_start.elapsed_time(ev_end)
     if world > 1:
         tot_ms = max_over_ranks(tot_ms)
     ms_per_step = tot_ms / K
@@ -385,7 +409,7 @@ def main() -> None:
             "config": {"workload": f"{WORKLOAD[args.config]}: {B} per GPU", "graph": args.config,
                        "n_ops": n, "n_tensors": info["n_tensors"], "candidates_per_gpu": B,
                        "candidate_ids": f"rank r evaluates [r*{B}, (r+1)*{B})",
-                       "l2": "flushed between timed steps (512 MiB write, outside the events)",
+                       "l2": l2_note,
                        "parallelism": f"candidate-sharded dp{world}" + (
                            (f" + {args.dist_backend} all_reduce(MIN) of a packed (peak, id) key" if use_key
                             else f" + {args.dist_backend} all_gather of (peak, id)") if world > 1 else ""),

@@ -136,6 +136,14 @@ int rm_argmin(const int64_t* peak, const uint8_t* valid, int64_t B, int64_t id_b
 int rm_argmin_key(const int64_t* peak, const uint8_t* valid, int64_t B, int64_t id_base,
                   int32_t id_bits, int64_t max_peak, int64_t* out_key, void* stream);
 
+/* K1 + selection in one pass (device pointers only, RM_DEVICE_PTRS): the
+ * rm_eval_orders outputs plus out_key = rm_argmin_key's packed key over them
+ * (max_peak = the graph's total bytes), reduced inside the K1 launch where the
+ * default evaluator runs -- no separate selection kernel. */
+int rm_eval_select_key(RmGraph* g, const void* orders, int64_t B, int64_t id_base, int32_t id_bits,
+                       uint32_t flags, int64_t* peak, int32_t* argmax, uint8_t* valid,
+                       int64_t* out_key, void* stream);
+
 /* Counter-RNG candidate generator: row c is the Kahn topological order that
  * breaks ties by the smallest (splitmix64(seed ^ splitmix64(id)) ^ op, op)
  * key with id = first_id + c (oracle: oracle/memplan_oracle.py kahn_candidate).
@@ -272,6 +280,10 @@ int rm_set_timing(int enable);
  * edge checks); unsupported choices fall back.  For tests and A/B
  * measurement. */
 int rm_set_k1_variant(int variant);
+/* Leave `sms` SMs idle in every K1 launch of this process (default 0), so a
+ * collective issued on another stream (the multi-GPU selection exchange) runs
+ * concurrently with the next batch's evaluation instead of after it. */
+int rm_set_sm_reserve(int sms);
 double rm_last_kernel_ms(void);
 
 #ifdef __cplusplus

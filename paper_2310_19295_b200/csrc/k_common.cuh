@@ -9,6 +9,7 @@
 namespace roam {
 
 extern thread_local bool g_timing;     // rm_set_timing
+extern int g_sm_reserve;               // rm_set_sm_reserve: SMs K1 leaves free
 extern thread_local double g_last_ms;  // rm_last_kernel_ms
 
 __device__ __forceinline__ void gbar(int id, int nt) {
@@ -42,6 +43,10 @@ inline int sm_count(int dev) {
 
 
 
+// SMs the persistent K1 grids use: all but rm_set_sm_reserve()'s count, so a
+// collective launched on another stream finds an idle SM while K1 runs
+inline int64_t k1_sms(int dev) { return std::max<int64_t>(1, sm_count(dev) - g_sm_reserve); }
+
 // K1 v2/v3 (k_eval_v2.cu): returns 1 when the graph does not fit the layout
 // (the caller falls back to the generic evaluator).  u16_rows: orders are
 // uint16[B, n] instead of int32[B, n].
@@ -49,7 +54,19 @@ int launch_k1v2(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, in
                 uint8_t* valid, cudaStream_t s, bool pairs, bool u16_rows);
 
 // K1 v4 (k_eval_v4.cu): same contract; returns 1 when g->k4v.ok == 0.
+// Fused selection: K1 v4 also reduces the packed key (peak << id_bits) |
+// (id_base + c) of the first strict minimum over valid candidates into
+// *key_out (INT64_MAX when none is valid), via per-group partials and a
+// last-group reduction; partial / counter are per-thread scratch (counter
+// zero between launches, reset by the last group).
+struct K1KeySel {
+  int64_t* key_out;
+  long long* partial;
+  unsigned* counter;
+  int64_t id_base;
+  int id_bits;
+};
 int launch_k1v4(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, int32_t* argmax,
-                uint8_t* valid, cudaStream_t s, bool u16_rows);
+                uint8_t* valid, cudaStream_t s, bool u16_rows, const K1KeySel* sel = nullptr);
 
 }  // namespace roam

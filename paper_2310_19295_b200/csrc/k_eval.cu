@@ -29,6 +29,7 @@
 namespace roam {
 
 thread_local bool g_timing = false;
+int g_sm_reserve = 0;
 thread_local double g_last_ms = -1.0;
 
 struct K1Args {
@@ -487,11 +488,16 @@ static int launch_k1_int32(RmGraph* g, const int32_t* orders_dev, int64_t B, int
 
 // orders_dev: int32[B, n], or uint16[B, n] with u16_rows (n < 65536).
 int launch_k1(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, int32_t* argmax,
-              uint8_t* valid, cudaStream_t s, bool u16_rows) {
+              uint8_t* valid, cudaStream_t s, bool u16_rows, const K1KeySel* sel = nullptr,
+              bool* fused = nullptr) {
+  if (fused) *fused = false;
   if (B <= 0) return RM_OK;
   if (g->k4v.ok && (t_force_variant == 0 || t_force_variant >= 4)) {
-    const int rc = launch_k1v4(g, orders_dev, B, peak, argmax, valid, s, u16_rows);
-    if (rc != 1) return rc;
+    const int rc = launch_k1v4(g, orders_dev, B, peak, argmax, valid, s, u16_rows, sel);
+    if (rc != 1) {
+      if (fused) *fused = sel != nullptr && rc == RM_OK;
+      return rc;
+    }
   }
   if (g->k2v.ok && t_force_variant != 1) {
     // v3 (pairs) wins on small graphs; from ~1k ops its doubled per-group
@@ -563,7 +569,7 @@ static int launch_k1_int32(RmGraph* g, const int32_t* orders_dev, int64_t B, int
   G = std::min(G, 15);  // named barriers 1..15
   if (G < 1) return fail(RM_ERR_CAPACITY, "K1: graph metadata does not fit in shared memory");
   // don't launch more groups than candidates
-  const int64_t sms = sm_count(dev);
+  const int64_t sms = k1_sms(dev);
   if (int64_t(G) * sms > B) G = (int)std::max<int64_t>(1, (B + sms - 1) / sms);
   a.G = G;
   const size_t smem = a.off_groups + size_t(G) * a.group_bytes;
@@ -601,6 +607,11 @@ extern "C" {
 
 int rm_set_timing(int enable) {
   g_timing = enable != 0;
+  return RM_OK;
+}
+int rm_set_sm_reserve(int sms) {
+  if (sms < 0 || sms > 64) return fail(RM_ERR_INVALID_ARG, "SM reserve must be 0..64");
+  g_sm_reserve = sms;
   return RM_OK;
 }
 int rm_set_k1_variant(int variant) {
@@ -808,6 +819,48 @@ int rm_argmin_key(const int64_t* peak, const uint8_t* valid, int64_t B, int64_t 
     RM_CUDA(cudaStreamSynchronize(s));
     return RM_OK;
   }
+  return launch_argmin(peak, valid, B, id_base, nullptr, s, out_key, id_bits);
+}
+
+int rm_eval_select_key(RmGraph* g, const void* orders, int64_t B, int64_t id_base, int32_t id_bits,
+                       uint32_t flags, int64_t* peak, int32_t* argmax, uint8_t* valid,
+                       int64_t* out_key, void* stream) {
+  int st = need_device(g);
+  if (st) return st;
+  if (!(flags & RM_DEVICE_PTRS)) return fail(RM_ERR_INVALID_ARG, "rm_eval_select_key takes device pointers");
+  if (B < 0 || !out_key || (B > 0 && ((!orders && g->n > 0) || !peak || !argmax || !valid)) ||
+      id_bits < 1 || id_bits > 62 || id_base < 0)
+    return fail(RM_ERR_INVALID_ARG, "bad rm_eval_select_key arguments");
+  const bool u16 = (flags & RM_ORDERS_U16) != 0;
+  if (u16 && g->n > 65535) return fail(RM_ERR_INVALID_ARG, "uint16 rows need n_ops <= 65535");
+  if ((id_base + B) > (int64_t(1) << id_bits))
+    return fail(RM_ERR_OVERFLOW, "candidate ids do not fit id_bits");
+  if (g->info.total_bytes >= (int64_t(1) << (63 - id_bits)))
+    return fail(RM_ERR_OVERFLOW, "peak bytes do not fit beside the id bits");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (B == 0) {
+    const int64_t none = INT64_MAX;
+    RM_CUDA(cudaMemcpyAsync(out_key, &none, 8, cudaMemcpyHostToDevice, s));
+    RM_CUDA(cudaStreamSynchronize(s));
+    return RM_OK;
+  }
+  // per-thread, per-device partials and a counter the kernel leaves at zero
+  struct SelCtx {
+    int dev = -1;
+    long long* partial = nullptr;
+    unsigned* counter = nullptr;
+  };
+  static thread_local SelCtx ctx;
+  if (ctx.dev != g->device) {
+    RM_CUDA(cudaMalloc(&ctx.partial, sizeof(long long) * 4096));
+    RM_CUDA(cudaMalloc(&ctx.counter, sizeof(unsigned)));
+    RM_CUDA(cudaMemset(ctx.counter, 0, sizeof(unsigned)));
+    ctx.dev = g->device;
+  }
+  const K1KeySel sel{out_key, ctx.partial, ctx.counter, id_base, id_bits};
+  bool fused = false;
+  int rc = launch_k1(g, orders, B, peak, argmax, valid, s, u16, &sel, &fused);
+  if (rc != RM_OK || fused) return rc;
   return launch_argmin(peak, valid, B, id_base, nullptr, s, out_key, id_bits);
 }
 

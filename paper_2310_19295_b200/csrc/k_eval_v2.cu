@@ -616,7 +616,7 @@ int launch_k1v2(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, in
   G = std::min(G, 1024 / NT);
   G = std::min(G, 15);
   if (G < 1) return 1;
-  const int64_t sms = sm_count(dev);
+  const int64_t sms = k1_sms(dev);
   const int64_t units = pairs ? (B + 1) / 2 : B;  // what one group evaluates at a time
   if (int64_t(G) * sms > units) G = (int)std::max<int64_t>(1, (units + sms - 1) / sms);
   a.G = G;

@@ -43,6 +43,7 @@ struct K1V4Args {
   int64_t* peak;
   int32_t* argmax;
   uint8_t* valid;
+  K1KeySel sel;  // sel.key_out == nullptr: no fused selection
   size_t off_edges, off_mpair, off_mptr, off_mcons, off_msz;
   size_t off_groups, group_bytes, off_xs, off_red;
 };
@@ -166,6 +167,7 @@ __global__ void __launch_bounds__((v4_cta_cap(C) / NT) * NT, 1) k1v4_eval_orders
       v[j] = k < n ? (uint32_t)__ldcs(row + k) : (uint32_t)k;
     }
   };
+  long long kbest = LLONG_MAX;  // fused selection: this group's best key (thread 0)
   int64_t c = int64_t(blockIdx.x) * a.G + gid;
   if (c < a.B) load_row(c);
   for (; c < a.B; c += cstride) {
@@ -315,6 +317,33 @@ __global__ void __launch_bounds__((v4_cta_cap(C) / NT) * NT, 1) k1v4_eval_orders
       a.peak[c] = (int64_t)bv << a.shift;
       a.argmax[c] = bk;
       a.valid[c] = bad ? 0 : 1;
+      if (!bad) kbest = min(kbest, (((long long)bv << a.shift) << a.sel.id_bits) | (a.sel.id_base + c));
+    }
+  }
+  if (a.sel.key_out) {
+    // fused selection: each group leaves its best key; the last group to
+    // finish reduces them all (threadfence + counter), then resets the counter
+    int* s_last = red_i + NWARPS;
+    if (tid == 0) {
+      a.sel.partial[blockIdx.x * a.G + gid] = kbest;
+      __threadfence();
+      *s_last = atomicAdd(a.sel.counter, 1u) == gridDim.x * (unsigned)a.G - 1u;
+    }
+    v4_bar<NT>(bar_id);
+    if (*s_last) {
+      __threadfence();
+      const int total = gridDim.x * a.G;
+      long long m = LLONG_MAX;
+      for (int i = tid; i < total; i += NT) m = min(m, ((volatile long long*)a.sel.partial)[i]);
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, d));
+      if (lane == 0) red_c[warp] = m;
+      v4_bar<NT>(bar_id);
+      if (tid == 0) {
+        for (int w = 1; w < NWARPS; ++w) m = min(m, red_c[w]);
+        *a.sel.key_out = m;
+        *a.sel.counter = 0u;
+      }
     }
   }
 }
@@ -377,7 +406,7 @@ static int launch_k1v4_nt(K1V4Args& a, int NT, int C, int grid, size_t smem, cud
 }
 
 int launch_k1v4(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, int32_t* argmax,
-                uint8_t* valid, cudaStream_t s, bool u16_rows) {
+                uint8_t* valid, cudaStream_t s, bool u16_rows, const K1KeySel* sel) {
   const K1V4Meta& m = g->k4v;
   if (!m.ok) return 1;
   const int NT = m.NT, C = m.C, SL = m.SL;
@@ -400,6 +429,7 @@ int launch_k1v4(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, in
   a.peak = peak;
   a.argmax = argmax;
   a.valid = valid;
+  if (sel) a.sel = *sel;
   const int stride = C + 2;  // V4Geom<C>::STRIDE
   a.off_edges = align16(8 * size_t(SL + 1));
   a.off_mpair = align16(a.off_edges + 4 * size_t(a.n_edges));
@@ -409,7 +439,7 @@ int launch_k1v4(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, in
   a.off_groups = align16(a.off_msz + 4 * size_t(a.n_pair + a.n_gen));
   a.off_xs = align16(2 * size_t(SL + 8));
   a.off_red = align16(a.off_xs + 8 * size_t(SL / C) * stride);
-  a.group_bytes = align16(a.off_red + 3 * 8 * size_t(NT / 32));
+  a.group_bytes = align16(a.off_red + 3 * 8 * size_t(NT / 32) + 16);
   int dev = g->device;
   int max_smem = 0;
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
@@ -418,7 +448,7 @@ int launch_k1v4(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, in
   G = std::min(G, (C == 64 ? 256 : C == 32 ? 512 : 1024) / NT);
   G = std::min(G, 15);
   if (G < 1) return 1;
-  const int64_t sms = sm_count(dev);
+  const int64_t sms = k1_sms(dev);
   if (int64_t(G) * sms > B) G = (int)std::max<int64_t>(1, (B + sms - 1) / sms);
   a.G = G;
   const size_t smem = a.off_groups + size_t(G) * a.group_bytes;

@@ -310,6 +310,29 @@ def select_key_device(g, peak, valid, id_base: int, id_bits: int, stream=None):
     return out
 
 
+def evaluate_select_key(g, orders, id_base: int, id_bits: int, stream=None):
+    """K1 over device rows with the packed-key selection fused into the same
+    launch (rm_eval_select_key): (peak, argmax, valid, key) CUDA tensors, key
+    = (peak << id_bits) | (id + id_base) of the first strict minimum, INT64_MAX
+    if no row is valid -- select_key_device(evaluate_orders(...)) in one pass."""
+    import torch
+    dg = device_graph(g)
+    n = dg.n_ops
+    kind, flags = _row_kind(orders)
+    if kind != "dev":
+        raise ValueError("evaluate_select_key takes CUDA rows")
+    if orders.dim() != 2 or orders.shape[1] != n:
+        raise ValueError(f"orders must be [B, {n}]")
+    orders = orders.contiguous()
+    B = orders.shape[0]
+    peak, arg, val = _device_outputs(orders, B)
+    key = torch.empty(1, dtype=torch.int64, device=orders.device)
+    check(lib().rm_eval_select_key(dg.handle, ptr(orders), B, id_base, id_bits, flags, ptr(peak),
+                                   ptr(arg), ptr(val), ptr(key), _stream_handle(stream)),
+          "rm_eval_select_key")
+    return peak, arg, val.view(torch.bool), key
+
+
 def argmin_orders(peak, valid, id_base: int = 0, stream=None) -> tuple[int, int]:
     """First strict minimum (lexicographic (peak, id)) over valid candidates.
 
@@ -341,6 +364,12 @@ def generate_orders(g, seed: int, first_id: int, B: int, device=None, stream=Non
 
 def set_kernel_timing(enable: bool) -> None:
     lib().rm_set_timing(1 if enable else 0)
+
+
+def set_sm_reserve(sms: int) -> None:
+    """K1 leaves ``sms`` SMs idle (rm_set_sm_reserve), for a collective that
+    overlaps the next batch's evaluation on another stream."""
+    check(lib().rm_set_sm_reserve(int(sms)), "rm_set_sm_reserve")
 
 
 def set_k1_variant(variant: int) -> None:

@@ -282,3 +282,35 @@ def test_random_hazard_graphs_vs_oracle(seed):
                 assert bool(val[k]) == want[2], (seed, trial, variant, row)
                 if want[2]:
                     assert (int(peak[k]), int(arg[k])) == want[:2], (seed, trial, variant, row)
+
+
+@pytest.mark.parametrize("variant", [0, 2])
+@pytest.mark.parametrize("name", ["layered", "gpt2-small", "bert-large", "gpt2-xl"])
+def test_fused_key_selection(name, variant):
+    """K1 with the packed-key selection fused into the launch (v4) or chained
+    (other variants) equals evaluate_orders + select_key_device, including
+    invalid rows, an id base, and a batch with no valid row."""
+    import torch
+    from paper_2310_19295_b200.evaluator import evaluate_select_key, select_key_device, set_k1_variant
+    from paper_2310_19295_b200.sharding import decode_key, key_bits
+    g = load_graph(gg.config_doc(name))
+    orders = generate_orders(g, 5, 0, 2500)
+    host = orders.cpu().numpy()
+    host[::3] = host[::3][:, ::-1]
+    dev = torch.from_numpy(host).cuda()
+    bits = key_bits(1 << 22)
+    set_k1_variant(variant)
+    try:
+        for base in (0, 123_456):
+            p, a, v, key = evaluate_select_key(g, dev, base, bits)
+            p2, a2, v2 = evaluate_orders(g, dev)
+            want = int(select_key_device(g, p2, v2, base, bits).item())
+            assert int(key.item()) == want
+            assert torch.equal(v, v2) and torch.equal(p[v], p2[v2]) and torch.equal(a[v], a2[v2])
+            b = O.first_strict_min(p2.cpu().tolist(), v2.cpu().tolist())
+            assert decode_key(int(key.item()), bits) == (b[0], b[1] + base)
+        bad = torch.flip(orders[1::3], dims=[1]).contiguous()   # every row reversed: none valid
+        *_, key = evaluate_select_key(g, bad, 0, bits)
+        assert int(key.item()) == 2**63 - 1
+    finally:
+        set_k1_variant(0)
