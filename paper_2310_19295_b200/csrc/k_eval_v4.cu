@@ -31,6 +31,10 @@ struct K1V4Args {
   int64_t B;
   int n, G, shift;
   const void* opv;  // int2 {fs, out} units per id [SL + 1]
+  const uint8_t* cls;  // CLS mode: class per id [SL + 1] ...
+  const void* tab;     // ... and int2 {fs, out} units per class [ncls]
+  int ncls;
+  size_t off_tab;
   const uint32_t* em;  // SIMD edge-mask word per 8-id chunk (roam_graph.cpp build_k1_em)
   const uint32_t* edges;
   int n_edges;  // multiple of 4 * NT
@@ -86,7 +90,11 @@ __device__ __forceinline__ unsigned v4_bar_or(int id, unsigned p) {
   else return (unsigned)gbar_or(id, NT, (int)p);
 }
 
-template <typename RowT, int NT, int C>
+// CLS: per-op {fs, out} as a one-byte class into a small table (graphs with
+// at most 255 distinct {out, fs} pairs): the per-id table shrinks 8x, which
+// buys a second resident group on large graphs at the cost of a dependent
+// table lookup per position
+template <typename RowT, int NT, int C, bool CLS = false>
 __global__ void __launch_bounds__((v4_cta_cap(C) / NT) * NT, 1) k1v4_eval_orders(const K1V4Args a) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int SL = NT * C;
@@ -103,7 +111,12 @@ __global__ void __launch_bounds__((v4_cta_cap(C) / NT) * NT, 1) k1v4_eval_orders
       uint4* dst = reinterpret_cast<uint4*>(smem + off);
       for (size_t i = threadIdx.x; i < bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
     };
-    cp16(a.opv, 0, align16(8 * size_t(SL + 1)));
+    if (CLS) {
+      cp16(a.cls, 0, align16(size_t(SL + 1)));
+      cp16(a.tab, a.off_tab, align16(8 * size_t(a.ncls)));
+    } else {
+      cp16(a.opv, 0, align16(8 * size_t(SL + 1)));
+    }
     if (a.n_edges > (C / 4) * NT) cp16(a.edges, a.off_edges, 4 * size_t(a.n_edges));
     cp16(a.mpair, a.off_mpair, align16(4 * size_t(a.n_pair)));
     cp16(a.mptr, a.off_mptr, align16(4 * size_t(a.n_gen + 1)));
@@ -112,6 +125,8 @@ __global__ void __launch_bounds__((v4_cta_cap(C) / NT) * NT, 1) k1v4_eval_orders
   }
   __syncthreads();
   const long long* opv = reinterpret_cast<const long long*>(smem);  // fs | out << 32
+  const uint8_t* cls8 = smem;                                         // CLS: class per id
+  const long long* tab = reinterpret_cast<const long long*>(smem + a.off_tab);
   const uint32_t* edges = reinterpret_cast<const uint32_t*>(smem + a.off_edges);
   const uint32_t* mpair = reinterpret_cast<const uint32_t*>(smem + a.off_mpair);
   const uint32_t* mptr = reinterpret_cast<const uint32_t*>(smem + a.off_mptr);
@@ -217,7 +232,7 @@ __global__ void __launch_bounds__((v4_cta_cap(C) / NT) * NT, 1) k1v4_eval_orders
     }
     // ---- P2a (position-major): {fs, out} units of the op at each position
 #pragma unroll
-    for (int j = 0; j < C; ++j) xs_w[v4_xs_off<NT, C>(j)] = opv[v[j]];
+    for (int j = 0; j < C; ++j) xs_w[v4_xs_off<NT, C>(j)] = CLS ? tab[cls8[v[j]]] : opv[v[j]];
     unsigned bad = ((sent & 0x80008000u) != 0) | ((ok & 0x80008000u) != 0x80008000u) | (eacc < 0);
     // prefetch the next candidate's row; it lands while P2b / P3 run
     const int64_t cn = c + cstride;
@@ -348,9 +363,9 @@ __global__ void __launch_bounds__((v4_cta_cap(C) / NT) * NT, 1) k1v4_eval_orders
   }
 }
 
-template <typename RowT, int NT, int C>
+template <typename RowT, int NT, int C, bool CLS = false>
 static int launch_k1v4_t(K1V4Args& a, int grid, size_t smem, cudaStream_t s) {
-  auto kern = k1v4_eval_orders<RowT, NT, C>;
+  auto kern = k1v4_eval_orders<RowT, NT, C, CLS>;
   RM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (g_timing) {
@@ -374,7 +389,20 @@ static int launch_k1v4_t(K1V4Args& a, int grid, size_t smem, cudaStream_t s) {
 
 // the instance table must list every (NT, C) k1v4_geometry (roam_graph.cpp) picks
 template <typename RowT>
-static int launch_k1v4_nt(K1V4Args& a, int NT, int C, int grid, size_t smem, cudaStream_t s) {
+static int launch_k1v4_nt(K1V4Args& a, int NT, int C, bool cls, int grid, size_t smem, cudaStream_t s) {
+#define RM_K1V4_CLS(nt, cc) \
+  if (cls && NT == nt && C == cc) return launch_k1v4_t<RowT, nt, cc, true>(a, grid, smem, s);
+  RM_K1V4_CLS(256, 16)
+  RM_K1V4_CLS(320, 16)
+  RM_K1V4_CLS(384, 16)
+  RM_K1V4_CLS(512, 16)
+  RM_K1V4_CLS(640, 16)
+  RM_K1V4_CLS(768, 16)
+  RM_K1V4_CLS(1024, 16)
+  RM_K1V4_CLS(128, 32)
+  RM_K1V4_CLS(256, 32)
+#undef RM_K1V4_CLS
+  if (cls) return 1;
 #define RM_K1V4_CASE(nt, cc) \
   if (NT == nt && C == cc) return launch_k1v4_t<RowT, nt, cc>(a, grid, smem, s);
   RM_K1V4_CASE(32, 4)
@@ -430,31 +458,52 @@ int launch_k1v4(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, in
   a.argmax = argmax;
   a.valid = valid;
   if (sel) a.sel = *sel;
+  a.cls = m.cls.as<uint8_t>();
+  a.tab = m.tab.p;
+  a.ncls = m.ncls;
   const int stride = C + 2;  // V4Geom<C>::STRIDE
-  a.off_edges = align16(8 * size_t(SL + 1));
-  a.off_mpair = align16(a.off_edges + 4 * size_t(a.n_edges));
-  a.off_mptr = align16(a.off_mpair + 4 * size_t(a.n_pair));
-  a.off_mcons = align16(a.off_mptr + 4 * size_t(a.n_gen + 1));
-  a.off_msz = align16(a.off_mcons + 2 * size_t(a.n_mcons));
-  a.off_groups = align16(a.off_msz + 4 * size_t(a.n_pair + a.n_gen));
-  a.off_xs = align16(2 * size_t(SL + 8));
-  a.off_red = align16(a.off_xs + 8 * size_t(SL / C) * stride);
-  a.group_bytes = align16(a.off_red + 3 * 8 * size_t(NT / 32) + 16);
   int dev = g->device;
   int max_smem = 0;
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  const size_t avail = max_smem > (int)a.off_groups ? size_t(max_smem) - a.off_groups : 0;
-  int G = (int)(avail / a.group_bytes);
-  G = std::min(G, (C == 64 ? 256 : C == 32 ? 512 : 1024) / NT);
-  G = std::min(G, 15);
+  const int cap = (C == 64 ? 256 : C == 32 ? 512 : 1024) / NT;
+  // layout with the per-id table (cls = false) or the class form; the class
+  // form is used only where it fits more groups per SM
+  auto layout = [&](bool cls) {
+    K1V4Args b = a;
+    const size_t table = cls ? align16(size_t(SL + 1)) + align16(8 * size_t(a.ncls)) : align16(8 * size_t(SL + 1));
+    b.off_tab = align16(size_t(SL + 1));
+    b.off_edges = table;
+    b.off_mpair = align16(b.off_edges + 4 * size_t(b.n_edges));
+    b.off_mptr = align16(b.off_mpair + 4 * size_t(b.n_pair));
+    b.off_mcons = align16(b.off_mptr + 4 * size_t(b.n_gen + 1));
+    b.off_msz = align16(b.off_mcons + 2 * size_t(b.n_mcons));
+    b.off_groups = align16(b.off_msz + 4 * size_t(b.n_pair + b.n_gen));
+    b.off_xs = align16(2 * size_t(SL + 8));
+    b.off_red = align16(b.off_xs + 8 * size_t(SL / C) * stride);
+    b.group_bytes = align16(b.off_red + 3 * 8 * size_t(NT / 32) + 16);
+    const size_t avail = max_smem > (int)b.off_groups ? size_t(max_smem) - b.off_groups : 0;
+    b.G = std::min({(int)(avail / b.group_bytes), cap, 15});
+    return b;
+  };
+  K1V4Args plain = layout(false);
+  bool use_cls = false;
+  if (m.ncls > 0 && ((C == 16 && NT >= 256) || (C == 32 && NT >= 128))) {
+    K1V4Args c = layout(true);
+    if (c.G > plain.G) {
+      plain = c;
+      use_cls = true;
+    }
+  }
+  a = plain;
+  int G = a.G;
   if (G < 1) return 1;
   const int64_t sms = k1_sms(dev);
   if (int64_t(G) * sms > B) G = (int)std::max<int64_t>(1, (B + sms - 1) / sms);
   a.G = G;
   const size_t smem = a.off_groups + size_t(G) * a.group_bytes;
   const int grid = (int)std::min<int64_t>(sms, (B + G - 1) / G);
-  return u16_rows ? launch_k1v4_nt<uint16_t>(a, NT, C, grid, smem, s)
-                  : launch_k1v4_nt<int32_t>(a, NT, C, grid, smem, s);
+  return u16_rows ? launch_k1v4_nt<uint16_t>(a, NT, C, use_cls, grid, smem, s)
+                  : launch_k1v4_nt<int32_t>(a, NT, C, use_cls, grid, smem, s);
 }
 
 }  // namespace roam

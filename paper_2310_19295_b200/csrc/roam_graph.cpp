@@ -148,16 +148,17 @@ static void build_k1v2_host(RmGraph& g, const std::vector<int64_t>& out,
 
 // K1 v4 geometry: the smallest slot count SL = NT * C >= n among the compiled
 // instances (k_eval_v4.cu launch table).  C positions per thread: 8 up to 1k
-// ops, 32 up to 2k (two-warp groups, 128 registers: measured fastest on
-// GPT-2 small, 0.084 vs 0.090 ms per 16k candidates), 16 beyond (32 would
-// halve the resident warps once a group's shared memory grows).
+// ops; 32 up to 2k (two-warp groups, 128 registers: GPT-2 small 0.082 vs
+// 0.090 ms per 16k candidates at C = 16) and up to 8k when the per-op table
+// has a class form (GPT2-XL 0.197 vs 0.209 ms per 8k); 16 otherwise (32
+// would halve the resident warps once a group's shared memory grows).
 // ROAM_K1_C=16|32|64 forces C where an instance exists (A/B runs).
-static bool k1v4_geometry(int n, int& NT, int& C) {
+static bool k1v4_geometry(int n, bool classes, int& NT, int& C) {
   static const int cenv = [] {
     const char* e = std::getenv("ROAM_K1_C");
     return e ? std::atoi(e) : 0;
   }();
-  const int want = cenv ? cenv : (n > 1024 && n <= 2048 ? 32 : 0);
+  const int want = cenv ? cenv : (n > 1024 && (n <= 2048 || (classes && n <= 8192)) ? 32 : 0);
   if (want == 32 || want == 64) {
     static const int nts[] = {32, 64, 128, 256};
     for (int nt : nts)
@@ -195,7 +196,7 @@ static void build_k1v4_host(RmGraph& g) {
   g.k4v.ok = 0;
   const int n = g.n;
   int NT = 0, C = 0;
-  if (!g.k2v.ok || !k1v4_geometry(n, NT, C)) return;
+  if (!g.k2v.ok || !k1v4_geometry(n, g.h_out.size() < 255, NT, C)) return;
   const int SL = NT * C;
   if (SL + 8 > 32768) return;
   if (g.h2_opv.size() < 2 * size_t(SL + 1)) g.h2_opv.resize(2 * size_t(SL + 1), 0);
@@ -222,6 +223,26 @@ static void build_k1v4_host(RmGraph& g) {
     g.h4_msz.push_back(0);
   }
   g.h4_msz.insert(g.h4_msz.end(), g.h2_msz.begin() + g.h2_mpair.size(), g.h2_msz.end());
+  // class form: one byte per id into a table of {fs, out} units
+  g.k4v.ncls = 0;
+  g.h4_cls.clear();
+  g.h4_tab.clear();
+  if (g.h_out.size() < 255) {
+    int zero = -1;
+    for (size_t c = 0; c < g.h_out.size(); ++c) {
+      g.h4_tab.push_back((int32_t)(g.h_fs[c] >> g.k2v.shift));
+      g.h4_tab.push_back((int32_t)(g.h_out[c] >> g.k2v.shift));
+      if (g.h_out[c] == 0 && g.h_fs[c] == 0) zero = (int)c;
+    }
+    if (zero < 0) {
+      zero = (int)g.h_out.size();
+      g.h4_tab.push_back(0);
+      g.h4_tab.push_back(0);
+    }
+    g.h4_cls.assign(size_t(SL + 1), (uint8_t)zero);
+    for (int v = 0; v < n; ++v) g.h4_cls[v] = (uint8_t)g.h_vidx[v];
+    g.k4v.ncls = (int)(g.h4_tab.size() / 2);
+  }
   g.k4v.NT = NT;
   g.k4v.C = C;
   g.k4v.SL = SL;
@@ -519,6 +540,8 @@ int rm_graph_create(const RmGraphDesc* d, uint32_t flags, RmGraph** out) {
     if (!e && g->k4v.ok) e = up(g->k4v.mpair, g->h4_mpair);
     if (!e && g->k4v.ok) e = up(g->k4v.msz, g->h4_msz);
     if (!e && g->k4v.ok) e = up(g->k4v.em, g->h4_em);
+    if (!e && g->k4v.ok && g->k4v.ncls) e = up(g->k4v.cls, g->h4_cls);
+    if (!e && g->k4v.ok && g->k4v.ncls) e = up(g->k4v.tab, g->h4_tab);
     if (!e) e = up(g->d_size, g->size);
     if (!e) e = up(g->d_producer, g->producer);
     if (!e) e = up(g->d_cons_ptr, g->cons_ptr);

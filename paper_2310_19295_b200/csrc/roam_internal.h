@@ -114,6 +114,11 @@ struct K1V4Meta {
   int NT = 0, C = 0, SL = 0;
   int64_t n_edges = 0, n_pair = 0;
   DevBuf em, edges, mpair, msz;
+  // class form (ncls > 0 when the graph has <= 255 distinct {out, fs} pairs):
+  // cls = class per id [SL + 1] (padding ids: a zero class), tab = int2
+  // {fs, out} units per class
+  int ncls = 0;
+  DevBuf cls, tab;
 };
 
 }  // namespace roam
@@ -141,6 +146,8 @@ struct RmGraph {
   std::vector<uint32_t> h2_edges, h2_mpair, h2_mptr, h2_msz;
   std::vector<uint16_t> h2_mcons;
   std::vector<uint32_t> h4_em, h4_edges, h4_mpair, h4_msz;
+  std::vector<uint8_t> h4_cls;
+  std::vector<int32_t> h4_tab;
   roam::DevBuf d_size, d_producer, d_cons_ptr, d_cons_idx, d_in_ptr, d_in_idx, d_out_ptr,
       d_out_idx, d_pred_ptr, d_pred_idx, d_succ_ptr, d_succ_idx;
 };
