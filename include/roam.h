@@ -98,6 +98,12 @@ int rm_graph_k1_export(const RmGraph* g, int32_t* vidx, int32_t* slot, int64_t* 
                        int64_t* fs_tab, int32_t* edge_u, int32_t* edge_v, int32_t* mptr,
                        int32_t* mcons, int64_t* msize);
 
+/* Schedule bounds (replaces graph.py:365-372 asap_alap): asap[v] = number of
+ * transitive predecessors, alap[v] = n-1 - number of transitive successors,
+ * from closure bitsets in C++.  Host-only (no device needed); control-plane
+ * code the planner's weight-update placement calls (ordering.py:405). */
+int rm_graph_asap_alap(const RmGraph* g, int32_t* asap, int32_t* alap);
+
 /* ----------------------------------------------------- K1: order batches */
 
 /* Evaluate B candidate orders (orders is int32[B, n_ops], row-major), each as

@@ -593,4 +593,31 @@ int rm_graph_k1_export(const RmGraph* g, int32_t* vidx, int32_t* slot, int64_t* 
   return RM_OK;
 }
 
+int rm_graph_asap_alap(const RmGraph* g, int32_t* asap, int32_t* alap) {
+  // graph.py:365-372: asap(v) = |transitive predecessors|, alap(v) = n-1 -
+  // |transitive successors|; transitive closure as bitsets in topological
+  // order (descendants) and reverse topological order (ancestors), popcounts
+  if (!g || (g->n > 0 && (!asap || !alap))) return fail(RM_ERR_INVALID_ARG, "NULL argument");
+  const int n = g->n;
+  if (n == 0) return RM_OK;
+  if (n > 60000) return fail(RM_ERR_CAPACITY, "asap_alap: closure bitsets above 60k ops");
+  std::vector<uint64_t> desc;
+  size_t words = 0;
+  if (!descendants(*g, desc, words)) return fail(RM_ERR_INVALID_ARG, "graph contains a cycle");
+  for (int v = 0; v < n; ++v) {
+    int c = 0;
+    for (size_t i = 0; i < words; ++i) c += __builtin_popcountll(desc[size_t(v) * words + i]);
+    alap[v] = n - 1 - c;
+  }
+  // ancestors: column counts of the descendant matrix
+  std::vector<int32_t> cnt(n, 0);
+  for (int u = 0; u < n; ++u) {
+    const uint64_t* du = &desc[size_t(u) * words];
+    for (size_t i = 0; i < words; ++i)
+      for (uint64_t w = du[i]; w; w &= w - 1) ++cnt[i * 64 + __builtin_ctzll(w)];
+  }
+  std::memcpy(asap, cnt.data(), sizeof(int32_t) * size_t(n));
+  return RM_OK;
+}
+
 }  // extern "C"

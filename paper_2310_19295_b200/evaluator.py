@@ -366,6 +366,17 @@ def set_kernel_timing(enable: bool) -> None:
     lib().rm_set_timing(1 if enable else 0)
 
 
+def asap_alap(g) -> tuple[tuple[int, ...], tuple[int, ...]]:
+    """Schedule bounds (graph.py:365-372) from closure bitsets in libroam's
+    C++ host code: (asap, alap) tuples."""
+    dg = device_graph(g)
+    n = dg.n_ops
+    asap = np.zeros(n, np.int32)
+    alap = np.zeros(n, np.int32)
+    check(lib().rm_graph_asap_alap(dg.handle, ptr(asap), ptr(alap)), "rm_graph_asap_alap")
+    return tuple(asap.tolist()), tuple(alap.tolist())
+
+
 def set_sm_reserve(sms: int) -> None:
     """K1 leaves ``sms`` SMs idle (rm_set_sm_reserve), for a collective that
     overlaps the next batch's evaluation on another stream."""

@@ -42,6 +42,7 @@ from . import evaluator as _ev
 from . import layout as _lay
 from . import ordering as _ord
 from . import windows as _win
+from ._lib import RoamError
 from .graph import GraphError
 
 ROOT = Path(__file__).resolve().parents[1]
@@ -77,6 +78,21 @@ def _translate(mp, fn):
 
 def _raise(e):
     raise e
+
+
+def _asap_alap_factory(mp):
+    """graph.py:365-372 asap_alap (called by place_weight_updates,
+    ordering.py:405) from libroam's C++ closure bitsets; the reference's own
+    function where the closure would be too large."""
+    ref = mp.graph.asap_alap
+
+    def asap_alap(g):
+        try:
+            asap, alap = _ev.asap_alap(g)
+        except RoamError:
+            return ref(g)
+        return mp.graph.ScheduleBounds(asap=asap, alap=alap)
+    return asap_alap
 
 
 class _State:
@@ -192,6 +208,7 @@ def install(mp=None):
     patches = {
         (pl, "build_window_problems"): build_window_problems,
         (ordm, "weight_update_cost"): _weight_update_cost_factory(mp),
+        (ordm, "asap_alap"): _asap_alap_factory(mp),
         (pl, "peak_memory"): T(_ev.peak_memory),
         (pl, "tensor_lifetimes"): T(_ev.tensor_lifetimes),
         (pl, "live_bytes_by_timestep"): T(_ev.live_bytes_by_timestep),

@@ -18,7 +18,8 @@ def test_install_uninstall_roundtrip():
     names = [(mp.planner, n) for n in ("peak_memory", "tensor_lifetimes", "live_bytes_by_timestep",
                                        "_pool_map", "repair_conflicts", "validate_layout")]
     names += [(mp.layout, "layout_violations"), (mp.simulator, "layout_violations"),
-              (mp.ordering, "weight_update_cost"), (mp.planner, "build_window_problems"),
+              (mp.ordering, "weight_update_cost"), (mp.ordering, "asap_alap"),
+              (mp.planner, "build_window_problems"),
               (mp.simulator, "peak_memory")]
     before = {k: getattr(*k) for k in names}
     plug.install(mp)
@@ -129,3 +130,19 @@ def test_window_problems_interval_rule_matches_reference(monkeypatch):
         for opt in ("sgd", "adam"):
             mp.planner.plan(rgen.gen_training_graph(arch, 4, optimizer=opt))
     assert sum(n_calls) > 20
+
+
+@pytest.mark.skipif(mp is None, reason="reference memplan not importable")
+def test_asap_alap_matches_reference():
+    """graph.py:365-372 from libroam's C++ closure bitsets (host-only)."""
+    rg = mp.graph
+    gen_random_dag, gen_training_graph = mp.graphgen.gen_random_dag, mp.graphgen.gen_training_graph
+    from paper_2310_19295_b200 import evaluator as ev
+    from paper_2310_19295_b200 import graphgen as gg
+    graphs = [rg.load_graph(gg.config_doc(name)) for name in ("layered", "gpt2-small")]
+    graphs += [gen_random_dag(5 + k, density=0.1 + 0.05 * (k % 6), seed=40 + k) for k in range(20)]
+    graphs += [gen_training_graph("transformer_block", 3, optimizer="adam")]
+    for g in graphs:
+        want = rg.asap_alap(g)
+        asap, alap = ev.asap_alap(g)
+        assert (asap, alap) == (want.asap, want.alap)
