@@ -98,6 +98,12 @@ int rm_graph_k1_export(const RmGraph* g, int32_t* vidx, int32_t* slot, int64_t* 
                        int64_t* fs_tab, int32_t* edge_u, int32_t* edge_v, int32_t* mptr,
                        int32_t* mcons, int64_t* msize);
 
+/* Transitive predecessors of every op as bitsets (graph.py:335-347
+ * predecessor_masks): rows[v * words + i] bit j set iff op 64*i+j precedes v,
+ * words = ceil(n_ops / 64).  Host-only; feeds the vectorised control-plane
+ * helpers of the planner plug-in (region filters, linearisation ranks). */
+int rm_graph_ancestors(const RmGraph* g, uint64_t* rows);
+
 /* Schedule bounds (replaces graph.py:365-372 asap_alap): asap[v] = number of
  * transitive predecessors, alap[v] = n-1 - number of transitive successors,
  * from closure bitsets in C++.  Host-only (no device needed); control-plane

@@ -593,6 +593,39 @@ int rm_graph_k1_export(const RmGraph* g, int32_t* vidx, int32_t* slot, int64_t* 
   return RM_OK;
 }
 
+int rm_graph_ancestors(const RmGraph* g, uint64_t* rows) {
+  // rows[v * words + i]: bit j of word i set iff op 64*i+j is a transitive
+  // predecessor of v (graph.py:335-347 predecessor_masks as bitsets), words =
+  // ceil(n / 64); ancestors accumulate over direct_preds in topological order
+  if (!g || (g->n > 0 && !rows)) return fail(RM_ERR_INVALID_ARG, "NULL argument");
+  const int n = g->n;
+  if (n == 0) return RM_OK;
+  if (n > 60000) return fail(RM_ERR_CAPACITY, "ancestors: closure bitsets above 60k ops");
+  const size_t words = (size_t(n) + 63) / 64;
+  std::vector<int32_t> indeg(n), topo;
+  topo.reserve(n);
+  for (int v = 0; v < n; ++v) indeg[v] = g->pred_ptr[v + 1] - g->pred_ptr[v];
+  for (int v = 0; v < n; ++v)
+    if (!indeg[v]) topo.push_back(v);
+  for (size_t h = 0; h < topo.size(); ++h) {
+    const int u = topo[h];
+    for (int k = g->succ_ptr[u]; k < g->succ_ptr[u + 1]; ++k)
+      if (--indeg[g->succ_idx[k]] == 0) topo.push_back(g->succ_idx[k]);
+  }
+  if ((int)topo.size() != n) return fail(RM_ERR_INVALID_ARG, "graph contains a cycle");
+  std::memset(rows, 0, sizeof(uint64_t) * words * size_t(n));
+  for (const int v : topo) {
+    uint64_t* rv = rows + size_t(v) * words;
+    for (int k = g->pred_ptr[v]; k < g->pred_ptr[v + 1]; ++k) {
+      const int p = g->pred_idx[k];
+      const uint64_t* rp = rows + size_t(p) * words;
+      for (size_t i = 0; i < words; ++i) rv[i] |= rp[i];
+      rv[p >> 6] |= 1ull << (p & 63);
+    }
+  }
+  return RM_OK;
+}
+
 int rm_graph_asap_alap(const RmGraph* g, int32_t* asap, int32_t* alap) {
   // graph.py:365-372: asap(v) = |transitive predecessors|, alap(v) = n-1 -
   // |transitive successors|; transitive closure as bitsets in topological

@@ -12,8 +12,9 @@ Dispatch points rebound (reference file:line of the call site):
   planner.tensor_lifetimes       planner.py:227    layout item lifetimes
   planner.live_bytes_by_timestep planner.py:264    boundary peaks
   planner._pool_map              planner.py:155-157, 250-252  the batch dispatch:
-        _solve_window jobs -> every greedy window in ONE K4 launch, exact
-                              windows stay on the reference's exact_order
+        _solve_window jobs -> every greedy window in ONE K4 launch, every
+                              exact window in ONE K5 launch (the reference's
+                              exact_order DFS only where its node cap can bind)
         _solve_layout jobs -> every leaf in ONE K3 launch per mode
                               (constrained LLFB for big leaves, exact_layout's
                               incumbent+bound for small ones; the reference's
@@ -21,6 +22,10 @@ Dispatch points rebound (reference file:line of the call site):
   planner.repair_conflicts       planner.py:259    K2 detection + mover placement
   planner.validate_layout        planner.py:260    K2
   ordering.weight_update_cost    ordering.py:310   event sweep once per (graph, bounds)
+  ordering.asap_alap             ordering.py:405   C++ closure bitsets (graph.py:365-372)
+  segmentation._region_between / _format_ig_ok / linearize (+ planner.linearize,
+  ordering.linearize)            segmentation.py:174-201, 500-572: numpy over the
+                                 C++ ancestor bit matrix (control.py)
   planner.build_window_problems  planner.py:141-149 interval stabbing on slot positions
                                                    (windows.py)
   layout.layout_violations / simulator.layout_violations / simulator.peak_memory
@@ -38,6 +43,7 @@ import sys
 import time
 from pathlib import Path
 
+from . import control as _ctl
 from . import evaluator as _ev
 from . import layout as _lay
 from . import ordering as _ord
@@ -205,10 +211,16 @@ def install(mp=None):
         except _win.Unsupported:
             return ref_bwp(g, lin, wu_plan, ops_per_step, time_budget, node_cap)
 
+    fast_linearize = _ctl.linearize_factory(mp)
     patches = {
+        (mp.segmentation, "linearize"): fast_linearize,
+        (pl, "linearize"): fast_linearize,
+        (ordm, "linearize"): fast_linearize,
         (pl, "build_window_problems"): build_window_problems,
         (ordm, "weight_update_cost"): _weight_update_cost_factory(mp),
         (ordm, "asap_alap"): _asap_alap_factory(mp),
+        (mp.segmentation, "_region_between"): _ctl.region_between_factory(mp.segmentation._region_between),
+        (mp.segmentation, "_format_ig_ok"): _ctl.format_ig_ok_factory(mp, mp.segmentation._format_ig_ok),
         (pl, "peak_memory"): T(_ev.peak_memory),
         (pl, "tensor_lifetimes"): T(_ev.tensor_lifetimes),
         (pl, "live_bytes_by_timestep"): T(_ev.live_bytes_by_timestep),

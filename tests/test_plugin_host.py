@@ -146,3 +146,41 @@ def test_asap_alap_matches_reference():
         want = rg.asap_alap(g)
         asap, alap = ev.asap_alap(g)
         assert (asap, alap) == (want.asap, want.alap)
+
+
+@pytest.mark.skipif(mp is None, reason="reference memplan not importable")
+def test_control_plane_dropins_match_reference():
+    """control.py restatements == the reference functions on the subgraph
+    trees of training graphs (every _region_between / _format_ig_ok call the
+    tree build makes, and linearize) -- host-only."""
+    from paper_2310_19295_b200 import control
+    seg = mp.segmentation
+    ref_rb, ref_ok, ref_lin = seg._region_between, seg._format_ig_ok, seg.linearize
+    fast_rb = control.region_between_factory(ref_rb)
+    fast_ok = control.format_ig_ok_factory(mp, ref_ok)
+    fast_lin = control.linearize_factory(mp)
+    calls = {"rb": 0, "ok": 0}
+
+    def rb(build, core, lo, hi):
+        calls["rb"] += 1
+        want = ref_rb(build, core, lo, hi)
+        assert fast_rb(build, core, lo, hi) == want
+        return want
+
+    def ok(build, members, boundary):
+        calls["ok"] += 1
+        want = ref_ok(build, members, boundary)
+        assert fast_ok(build, members, boundary) == want
+        return want
+
+    seg._region_between, seg._format_ig_ok = rb, ok
+    try:
+        for arch, blocks, opt in (("transformer_block", 4, "adam"), ("mlp", 3, "sgd"),
+                                  ("residual", 5, "adam"), ("transformer_block", 12, "adam")):
+            g = mp.graphgen.gen_training_graph(arch, blocks, optimizer=opt)
+            for limit in (6, 20):
+                tree = seg.build_subgraph_tree(g, limit)
+                assert fast_lin(g, tree) == ref_lin(g, tree)
+    finally:
+        seg._region_between, seg._format_ig_ok = ref_rb, ref_ok
+    assert calls["rb"] > 20 and calls["ok"] > 5
