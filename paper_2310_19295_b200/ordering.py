@@ -14,6 +14,7 @@
 from __future__ import annotations
 
 import ctypes as C
+import itertools
 import time
 from dataclasses import dataclass
 from typing import Sequence
@@ -59,7 +60,9 @@ def _check_problem(p) -> None:
 
 
 def _window_csr(problems: Sequence, who: str):
-    """Device graph + window / live-in / live-out CSR of problems sharing one graph."""
+    """Device graph + window / live-in / live-out CSR of problems sharing one
+    graph.  Entry order within a window is free: libroam sorts the ops and
+    treats the tensor lists as sets."""
     from .evaluator import device_graph
     _lib.require_device()
     g = problems[0].graph
@@ -68,14 +71,14 @@ def _window_csr(problems: Sequence, who: str):
     W = len(problems)
 
     def csr(lists):
-        lens = np.fromiter((len(x) for x in lists), np.int64, W)
+        lens = np.fromiter(map(len, lists), np.int64, W)
         p = np.zeros(W + 1, np.int64)
         np.cumsum(lens, out=p[1:])
-        idx = np.fromiter((v for x in lists for v in x), np.int64, int(p[-1]))
-        return p, idx.astype(np.int32)
+        idx = np.fromiter(itertools.chain.from_iterable(lists), np.int32, int(p[-1]))
+        return p, idx
 
-    return (device_graph(g), csr([sorted(p.ops) for p in problems]),
-            csr([sorted(p.live_in) for p in problems]), csr([sorted(p.live_out) for p in problems]))
+    return (device_graph(g), csr([p.ops for p in problems]),
+            csr([p.live_in for p in problems]), csr([p.live_out for p in problems]))
 
 
 def greedy_windows(problems: Sequence) -> list[tuple[tuple[int, ...], int] | Exception]:
