@@ -133,7 +133,158 @@ def format_ig_ok_factory(mp, ref):
     return format_ig_ok
 
 
+def _floating_closed(g, fl: set) -> bool:
+    """Every successor of a floating op is floating, so no core-to-core path
+    runs through a floating op and the core's induced closure (what
+    predecessor_masks(g, core) computes) is the global closure on core rows."""
+    return all(s in fl for f in fl for s in g.direct_succs[f])
+
+
+def subgraph_tree_factory(mp):
+    """Drop-in for segmentation.build_subgraph_tree (segmentation.py:343-448).
+
+    The reference spends most of this function on bookkeeping, not on the
+    tree: the core list tests membership in a set rebuilt for every op
+    (O(n * |floating|)), ``_mi_over`` popcounts induced big-int masks, and the
+    residual grouping tests ``before`` bit by bit.  Here those three come from
+    the C++ ancestor bit matrix; the steps that shape the tree -- the
+    inside-out independent-subgraph pairing, the residual runs and
+    ``_split_if_oversized`` -- are the reference's own helpers, called in the
+    same order on the reference's ``_TreeBuild`` (node ids come out the
+    same).  Where the core's induced closure could differ from the global one
+    the reference function runs instead."""
+    seg, gr = mp.segmentation, mp.graph
+    ref = seg.build_subgraph_tree
+
+    def build_subgraph_tree(g, node_limit):
+        if node_limit < 2:
+            raise gr.ConfigError("node_limit must be >= 2")
+        if not any(op.kind is gr.OpKind.BACKWARD for op in g.ops):
+            raise gr.StructuralError("graph has no backward pass; segment it as an inference graph")
+        branches = seg.weight_update_branches(g)
+        floating = sorted(v for b in branches for v in b.ops)
+        fl = set(floating)
+        if not _floating_closed(g, fl):
+            return ref(g, node_limit)
+        c = closure(g)
+        n, anc = c["n"], c["anc"]
+        is_core = np.ones(n, bool)
+        if floating:
+            is_core[np.asarray(floating, np.int64)] = False
+        core = np.nonzero(is_core)[0].tolist()
+        # the reference's predecessor masks (graph.py:335-348) as big ints
+        preds = [int.from_bytes(anc[v].tobytes(), "little") for v in range(n)]
+        build = seg._TreeBuild(g=g, node_limit=node_limit, preds=preds,
+                               categories=seg.classify_tensors(g), branches=branches)
+        # _mi_over(g, core) (segmentation.py:108-117): ancestors within the core
+        # + descendants within the core == |core| - 1, ordered by position
+        cbytes = np.packbits(np.append(is_core, np.zeros(anc.shape[1] * 8 - n, bool)), bitorder="little")
+        n_anc = np.bitwise_count(anc & cbytes).sum(axis=1, dtype=np.int64)
+        # descendants within the core = all descendants (n-1-alap, libroam C++)
+        # minus the floating ones (column sums over the few floating rows)
+        from .evaluator import asap_alap
+        n_desc = n - 1 - np.asarray(asap_alap(g)[1], np.int64)
+        if floating:
+            blk = np.unpackbits(anc[np.asarray(floating, np.int64)], axis=1, bitorder="little")[:, :n]
+            n_desc -= blk.sum(axis=0, dtype=np.int64)
+        mi_mask = is_core & (n_anc + n_desc == len(core) - 1)
+        mi_core = sorted(np.nonzero(mi_mask)[0].tolist(), key=lambda v: int(n_anc[v]))
+        fwd_mi = [v for v in mi_core if g.ops[v].kind is gr.OpKind.FORWARD]
+        bwd_mi = [v for v in mi_core if g.ops[v].kind is gr.OpKind.BACKWARD]
+
+        igs, used = [], []
+        inner = None          # (inner_f, inner_b) of the last accepted pair
+        for of, ob in zip(reversed(fwd_mi), bwd_mi):
+            if inner is None:
+                members = seg._region_between(build, core, of, ob)
+                boundary = {of, ob}
+            else:
+                members = sorted(seg._region_between(build, core, of, inner[0])
+                                 + seg._region_between(build, core, inner[1], ob))
+                boundary = {of, ob, inner[0], inner[1]}
+            if seg._format_ig_ok(build, set(members), boundary):
+                igs.append(build.new_node(kind="independent", outer_fwd=of,
+                                          inner_fwd=None if inner is None else inner[0],
+                                          inner_bwd=None if inner is None else inner[1],
+                                          outer_bwd=ob, members=tuple(members),
+                                          tag="middle" if inner is None else ""))
+                used += [of, ob]
+                inner = (of, ob)
+
+        covered = np.zeros(n, bool)
+        if used:
+            covered[np.asarray(used, np.int64)] = True
+        for node in igs:
+            if node.members:
+                covered[np.asarray(node.members, np.int64)] = True
+        unc = np.nonzero(is_core & ~covered)[0]
+        residuals = []
+        if len(unc):
+            # residual runs: uncovered ops grouped by how many pair boundaries
+            # precede them (segmentation.py:408-418)
+            sorted_used = sorted(set(used), key=lambda v: int(c["count"][v]))
+            umask = np.zeros(anc.shape[1] * 8, bool)
+            if sorted_used:
+                umask[np.asarray(sorted_used, np.int64)] = True
+            rank = np.bitwise_count(anc[unc] & np.packbits(umask, bitorder="little")).sum(axis=1)
+            for r in np.unique(rank).tolist():
+                lo = sorted_used[r - 1] if r > 0 else None
+                hi = sorted_used[r] if r < len(sorted_used) else None
+                residuals.append(build.new_node(kind="independent", outer_fwd=lo, outer_bwd=hi,
+                                                members=tuple(unc[rank == r].tolist()), tag="residual"))
+
+        for node in igs + residuals:
+            seg._split_if_oversized(build, node, mi_core)
+        children = igs + residuals
+        if not children:
+            children.append(build.new_node(kind="independent", tag="catchall"))
+        children.append(build.new_node(kind="independent", tag="tail"))
+        pinned = set()
+        for node in children:
+            pinned.update(node.boundary_ops())
+            for ch in node.children:
+                pinned.update(ch.boundary_ops())
+        return seg.SubgraphNode(id=0, kind="root", members=(), children=tuple(children),
+                                floating_ops=tuple(floating), pinned_ops=tuple(sorted(pinned)))
+    return build_subgraph_tree
+
+
+def weight_update_branches_factory(mp):
+    """graph.py:513-557 weight_update_branches, computed once per graph (the
+    planner asks seven times per plan: tree build, each linearisation, each
+    weight-update placement); every call gets its own list of the
+    reference's frozen WeightUpdateBranch records."""
+    ref = mp.graph.weight_update_branches
+
+    def weight_update_branches(g):
+        ent = graph_cache(g)
+        hit = ent.get("wu_branches")
+        if hit is None:
+            hit = ent["wu_branches"] = tuple(ref(g))
+        return list(hit)
+    return weight_update_branches
+
+
 def linearize_factory(mp):
+    seg = mp.segmentation
+    build = _linearize_factory(mp)
+
+    def linearize(g, root):
+        """Computed once per (graph, tree): the planner linearises the same
+        tree four times per plan (planner.py:198, ordering.py:404 twice,
+        segmentation.py:608).  Callers get a fresh leaf_of_op dict each time."""
+        ent = graph_cache(g)
+        hit = ent.get("linearize")
+        if hit is None or hit[0]() is not root:
+            import weakref
+            hit = ent["linearize"] = (weakref.ref(root), build(g, root))
+        lin = hit[1]
+        return seg.Linearization(slots=lin.slots, windows=lin.windows, leaf_of_op=dict(lin.leaf_of_op),
+                                 tail_window=lin.tail_window)
+    return linearize
+
+
+def _linearize_factory(mp):
     seg, gr = mp.segmentation, mp.graph
 
     def linearize(g, root):

@@ -368,13 +368,18 @@ def set_kernel_timing(enable: bool) -> None:
 
 def asap_alap(g) -> tuple[tuple[int, ...], tuple[int, ...]]:
     """Schedule bounds (graph.py:365-372) from closure bitsets in libroam's
-    C++ host code: (asap, alap) tuples."""
-    dg = device_graph(g)
-    n = dg.n_ops
-    asap = np.zeros(n, np.int32)
-    alap = np.zeros(n, np.int32)
-    check(lib().rm_graph_asap_alap(dg.handle, ptr(asap), ptr(alap)), "rm_graph_asap_alap")
-    return tuple(asap.tolist()), tuple(alap.tolist())
+    C++ host code: (asap, alap) tuples, computed once per graph (the planner
+    asks from the tree build and from weight-update placement)."""
+    ent = graph_cache(g)
+    hit = ent.get("asap_alap")
+    if hit is None:
+        dg = device_graph(g)
+        n = dg.n_ops
+        asap = np.zeros(n, np.int32)
+        alap = np.zeros(n, np.int32)
+        check(lib().rm_graph_asap_alap(dg.handle, ptr(asap), ptr(alap)), "rm_graph_asap_alap")
+        hit = ent["asap_alap"] = (tuple(asap.tolist()), tuple(alap.tolist()))
+    return hit
 
 
 def set_sm_reserve(sms: int) -> None:

@@ -26,6 +26,9 @@ Dispatch points rebound (reference file:line of the call site):
   segmentation._region_between / _format_ig_ok / linearize (+ planner.linearize,
   ordering.linearize)            segmentation.py:174-201, 500-572: numpy over the
                                  C++ ancestor bit matrix (control.py)
+  segmentation.build_subgraph_tree (+ planner's)  segmentation.py:343-448: core,
+                                 _mi_over and residual ranks from the same matrix
+  graph/segmentation/ordering.weight_update_branches  graph.py:513: once per graph
   planner.build_window_problems  planner.py:141-149 interval stabbing on slot positions
                                                    (windows.py)
   layout.layout_violations / simulator.layout_violations / simulator.peak_memory
@@ -212,7 +215,14 @@ def install(mp=None):
             return ref_bwp(g, lin, wu_plan, ops_per_step, time_budget, node_cap)
 
     fast_linearize = _ctl.linearize_factory(mp)
+    fast_tree = _ctl.subgraph_tree_factory(mp)
+    wu_branches = _ctl.weight_update_branches_factory(mp)
     patches = {
+        (mp.segmentation, "build_subgraph_tree"): fast_tree,
+        (pl, "build_subgraph_tree"): fast_tree,
+        (gr, "weight_update_branches"): wu_branches,
+        (mp.segmentation, "weight_update_branches"): wu_branches,
+        (ordm, "weight_update_branches"): wu_branches,
         (mp.segmentation, "linearize"): fast_linearize,
         (pl, "linearize"): fast_linearize,
         (ordm, "linearize"): fast_linearize,

@@ -18,6 +18,8 @@ def test_install_uninstall_roundtrip():
     names = [(mp.planner, n) for n in ("peak_memory", "tensor_lifetimes", "live_bytes_by_timestep",
                                        "_pool_map", "repair_conflicts", "validate_layout")]
     names += [(mp.layout, "layout_violations"), (mp.simulator, "layout_violations"),
+              (mp.segmentation, "build_subgraph_tree"), (mp.planner, "build_subgraph_tree"),
+              (mp.ordering, "weight_update_branches"),
               (mp.ordering, "weight_update_cost"), (mp.ordering, "asap_alap"),
               (mp.planner, "build_window_problems"),
               (mp.simulator, "peak_memory")]
@@ -184,3 +186,44 @@ def test_control_plane_dropins_match_reference():
     finally:
         seg._region_between, seg._format_ig_ok = ref_rb, ref_ok
     assert calls["rb"] > 20 and calls["ok"] > 5
+
+
+def _tree_key(node):
+    return (node.id, node.kind, node.outer_fwd, node.inner_fwd, node.inner_bwd, node.outer_bwd,
+            node.members, node.owned_tensors, node.unsplittable, node.tag, node.floating_ops,
+            node.pinned_ops, tuple(_tree_key(c) for c in node.children))
+
+
+@pytest.mark.skipif(mp is None, reason="reference memplan not importable")
+def test_subgraph_tree_dropin_matches_reference():
+    """build_subgraph_tree over the C++ ancestor matrix returns the reference's
+    tree node for node (ids, boundaries, members, split flags) on the config
+    graphs and the reference's own generators, across node limits; the
+    weight-update-branch and linearize caches hand out equal, independent
+    results (host-only)."""
+    from paper_2310_19295_b200 import control
+    from paper_2310_19295_b200 import graphgen as gg
+    seg = mp.segmentation
+    ref_tree, ref_lin, ref_wu = seg.build_subgraph_tree, seg.linearize, mp.graph.weight_update_branches
+    fast_tree = control.subgraph_tree_factory(mp)
+    fast_lin = control.linearize_factory(mp)
+    fast_wu = control.weight_update_branches_factory(mp)
+    graphs = [mp.graph.load_graph(gg.config_doc(name)) for name in ("gpt2-small", "bert-large")]
+    for arch, blocks, opt in (("transformer_block", 6, "adam"), ("mlp", 5, "sgd"),
+                              ("residual", 7, "adam"), ("transformer_block", 1, "sgd")):
+        graphs.append(mp.graphgen.gen_training_graph(arch, blocks, optimizer=opt))
+    for g in graphs:
+        assert fast_wu(g) == ref_wu(g) and fast_wu(g) is not fast_wu(g)
+        for limit in (2, 7, 20, 10**6):
+            want = ref_tree(g, limit)
+            got = fast_tree(g, limit)
+            assert _tree_key(got) == _tree_key(want), (len(g.ops), limit)
+            lin = fast_lin(g, got)
+            assert lin == ref_lin(g, want)
+            assert fast_lin(g, got).leaf_of_op is not lin.leaf_of_op
+    inference = mp.graph.load_graph(gg.config_doc("layered"))
+    for fn in (ref_tree, fast_tree):
+        with pytest.raises(mp.graph.StructuralError, match="no backward pass"):
+            fn(inference, 20)
+        with pytest.raises(mp.graph.ConfigError, match="node_limit"):
+            fn(graphs[0], 1)
