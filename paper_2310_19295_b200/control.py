@@ -265,6 +265,51 @@ def weight_update_branches_factory(mp):
     return weight_update_branches
 
 
+def assign_shared_tensors_factory(mp):
+    """Drop-in for segmentation.assign_shared_tensors (segmentation.py:598-639).
+
+    The reference places every floating weight-update op at the last window
+    slot of its leaf by rescanning the whole slot sequence once per floating
+    op (O(floating x slots): 0.4 s on the reference's 600-block graph); here
+    one pass over the slots records each leaf's last window position.  The
+    ownership rule itself (backward / weight-update / consumer-less tensors
+    stay with their producer's leaf, the rest go to the leaf of their last
+    consumer by (slot, id)) is unchanged, as is the owned_tensors side effect."""
+    seg, gr = mp.segmentation, mp.graph
+
+    def assign_shared_tensors(tree, g, leaf_of=None):
+        lin = seg.linearize(g, tree)
+        if leaf_of is None:
+            leaf_of = lin.leaf_of_op
+        slot_pos: dict[int, int] = {}
+        last_win: dict[int, int] = {}
+        for pos, (kind, ref) in enumerate(lin.slots):
+            if kind == "op":
+                slot_pos[ref] = pos
+            else:
+                w = lin.windows[ref]
+                for v in w.ops:
+                    slot_pos[v] = pos
+                last_win[w.leaf] = pos
+        for v in range(g.n_ops):
+            if v not in slot_pos:
+                slot_pos[v] = last_win.get(leaf_of[v], len(lin.slots))
+        late = (gr.OpKind.BACKWARD, gr.OpKind.WEIGHT_UPDATE)
+        ownership: dict[int, int] = {}
+        owned: dict[int, list[int]] = {}
+        for t in g.tensors:
+            if not t.consumers or g.ops[t.producer].kind in late:
+                leaf = leaf_of[t.producer]
+            else:
+                leaf = leaf_of[max(t.consumers, key=lambda c: (slot_pos[c], c))]
+            ownership[t.id] = leaf
+            owned.setdefault(leaf, []).append(t.id)
+        for leaf in tree.leaves():
+            leaf.owned_tensors = tuple(sorted(owned.get(leaf.id, [])))
+        return ownership
+    return assign_shared_tensors
+
+
 def linearize_factory(mp):
     seg = mp.segmentation
     build = _linearize_factory(mp)

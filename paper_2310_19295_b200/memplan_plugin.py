@@ -29,6 +29,8 @@ Dispatch points rebound (reference file:line of the call site):
   segmentation.build_subgraph_tree (+ planner's)  segmentation.py:343-448: core,
                                  _mi_over and residual ranks from the same matrix
   graph/segmentation/ordering.weight_update_branches  graph.py:513: once per graph
+  segmentation.assign_shared_tensors (+ planner's)  segmentation.py:598-639: one
+                                 slot pass instead of one per floating op
   planner.build_window_problems  planner.py:141-149 interval stabbing on slot positions
                                                    (windows.py)
   layout.layout_violations / simulator.layout_violations / simulator.peak_memory
@@ -217,8 +219,11 @@ def install(mp=None):
     fast_linearize = _ctl.linearize_factory(mp)
     fast_tree = _ctl.subgraph_tree_factory(mp)
     wu_branches = _ctl.weight_update_branches_factory(mp)
+    fast_assign = _ctl.assign_shared_tensors_factory(mp)
     patches = {
         (mp.segmentation, "build_subgraph_tree"): fast_tree,
+        (mp.segmentation, "assign_shared_tensors"): fast_assign,
+        (pl, "assign_shared_tensors"): fast_assign,
         (pl, "build_subgraph_tree"): fast_tree,
         (gr, "weight_update_branches"): wu_branches,
         (mp.segmentation, "weight_update_branches"): wu_branches,

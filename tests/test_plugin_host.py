@@ -19,7 +19,7 @@ def test_install_uninstall_roundtrip():
                                        "_pool_map", "repair_conflicts", "validate_layout")]
     names += [(mp.layout, "layout_violations"), (mp.simulator, "layout_violations"),
               (mp.segmentation, "build_subgraph_tree"), (mp.planner, "build_subgraph_tree"),
-              (mp.ordering, "weight_update_branches"),
+              (mp.ordering, "weight_update_branches"), (mp.planner, "assign_shared_tensors"),
               (mp.ordering, "weight_update_cost"), (mp.ordering, "asap_alap"),
               (mp.planner, "build_window_problems"),
               (mp.simulator, "peak_memory")]
@@ -208,6 +208,7 @@ def test_subgraph_tree_dropin_matches_reference():
     fast_tree = control.subgraph_tree_factory(mp)
     fast_lin = control.linearize_factory(mp)
     fast_wu = control.weight_update_branches_factory(mp)
+    ref_assign, fast_assign = seg.assign_shared_tensors, control.assign_shared_tensors_factory(mp)
     graphs = [mp.graph.load_graph(gg.config_doc(name)) for name in ("gpt2-small", "bert-large")]
     for arch, blocks, opt in (("transformer_block", 6, "adam"), ("mlp", 5, "sgd"),
                               ("residual", 7, "adam"), ("transformer_block", 1, "sgd")):
@@ -221,6 +222,15 @@ def test_subgraph_tree_dropin_matches_reference():
             lin = fast_lin(g, got)
             assert lin == ref_lin(g, want)
             assert fast_lin(g, got).leaf_of_op is not lin.leaf_of_op
+            # tensor routing on two copies of the tree (it records owned_tensors)
+            leaf_of = dict(lin.leaf_of_op)
+            if limit == 20:   # a routing that moves weight-update ops, as plan() does
+                for v in want.floating_ops[::2]:
+                    leaf_of[v] = want.leaves()[-1].id
+            for lo in (None, leaf_of):
+                t_ref, t_fast = ref_tree(g, limit), ref_tree(g, limit)
+                assert fast_assign(t_fast, g, lo) == ref_assign(t_ref, g, lo)
+                assert [x.owned_tensors for x in t_fast.leaves()] == [x.owned_tensors for x in t_ref.leaves()]
     inference = mp.graph.load_graph(gg.config_doc("layered"))
     for fn in (ref_tree, fast_tree):
         with pytest.raises(mp.graph.StructuralError, match="no backward pass"):
