@@ -218,9 +218,13 @@ __global__ void __launch_bounds__((v4_cta_cap(C) / NT) * NT, 1) k1v4_eval_orders
     int eacc = 0;
     int e_first = tid;
     if (ereg) {
+      // every slot loads (unused ones read pos[0]: a broadcast) so the loads
+      // issue back to back; unused slots are masked out of the result
 #pragma unroll
-      for (int i = 0; i < ER; ++i)
-        if (i < ek) eacc |= (int)lds_u16(posb, er[i] >> 16) - (int)lds_u16(posb, er[i] & 0xffffu) - 1;
+      for (int i = 0; i < ER; ++i) {
+        const int d = (int)lds_u16(posb, er[i] >> 16) - (int)lds_u16(posb, er[i] & 0xffffu) - 1;
+        eacc |= i < ek ? d : 0;
+      }
       e_first = n_edges;
     }
     for (int e0 = e_first; e0 < n_edges; e0 += 4 * NT) {
@@ -240,15 +244,22 @@ __global__ void __launch_bounds__((v4_cta_cap(C) / NT) * NT, 1) k1v4_eval_orders
     v4_bar<NT>(bar_id);
     // ---- P2b: multi-consumer tensors free after their latest maximal consumer
     // (positions of a broken row may be the sentinel: clamp into the group)
+    // unconditional shared reduction: the zero-size padding pairs add 0 to a
+    // real slot, which is cheaper than branching around their atomics
     auto add_free = [&](unsigned kmax, unsigned units) {
       kmax = min(kmax, (unsigned)(SL - 1));
-      if (units) atomicAdd(reinterpret_cast<unsigned*>(xs + (kmax >> X::L) * X::STRIDE + (kmax & (C - 1))), units);
+      atomicAdd(reinterpret_cast<unsigned*>(xs + (kmax >> X::L) * X::STRIDE + (kmax & (C - 1))), units);
     };
     int m_first = tid;
     if (preg) {
+      // gathers first (independent, back to back), then the atomics of the
+      // slots in use (pk is uniform)
+      unsigned km[ER];
+#pragma unroll
+      for (int i = 0; i < ER; ++i) km[i] = max(lds_u16(posb, pw[i] & 0xffffu), lds_u16(posb, pw[i] >> 16));
 #pragma unroll
       for (int i = 0; i < ER; ++i)
-        if (i < pk) add_free(max(lds_u16(posb, pw[i] & 0xffffu), lds_u16(posb, pw[i] >> 16)), pu[i]);
+        if (i < pk) add_free(km[i], pu[i]);
       m_first = n_pair;
     }
     for (int m = m_first; m < n_pair; m += NT) {
@@ -273,24 +284,36 @@ __global__ void __launch_bounds__((v4_cta_cap(C) / NT) * NT, 1) k1v4_eval_orders
     // carry zero bytes: they never raise the running max above a real slot)
     const int k0 = tid * C;
     const long long* xr = xs + tid * X::STRIDE;
-    long long run = 0, best = LLONG_MIN;
-    int bi = 0;
+    // the running sum is one dependent chain; the (max, first index) over the
+    // C live values is a pairwise tree (depth log2 C instead of C)
+    long long run = 0;
+    long long lv[C];
 #pragma unroll
     for (int i = 0; i < C; i += 2) {
       const longlong2 pr = *reinterpret_cast<const longlong2*>(xr + i);
-      long long live = run + (long long)((unsigned long long)pr.x >> 32);
-      if (live > best) {
-        best = live;
-        bi = i;
-      }
-      run = live - (long long)(unsigned)pr.x;
-      live = run + (long long)((unsigned long long)pr.y >> 32);
-      if (live > best) {
-        best = live;
-        bi = i + 1;
-      }
-      run = live - (long long)(unsigned)pr.y;
+      lv[i] = run + (long long)((unsigned long long)pr.x >> 32);
+      run = lv[i] - (long long)(unsigned)pr.x;
+      lv[i + 1] = run + (long long)((unsigned long long)pr.y >> 32);
+      run = lv[i + 1] - (long long)(unsigned)pr.y;
     }
+    int ix[C / 2];
+#pragma unroll
+    for (int p = 0; p < C / 2; ++p) {  // strict >: ties keep the earlier position
+      const bool t = lv[2 * p + 1] > lv[2 * p];
+      lv[p] = t ? lv[2 * p + 1] : lv[2 * p];
+      ix[p] = 2 * p + (t ? 1 : 0);
+    }
+#pragma unroll
+    for (int w = C / 2; w > 1; w >>= 1) {
+#pragma unroll
+      for (int p = 0; p < w / 2; ++p) {
+        const bool t = lv[2 * p + 1] > lv[2 * p];
+        lv[p] = t ? lv[2 * p + 1] : lv[2 * p];
+        ix[p] = t ? ix[2 * p + 1] : ix[2 * p];
+      }
+    }
+    const long long best = lv[0];
+    const int bi = ix[0];
     long long incl = run;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
