@@ -74,6 +74,9 @@ def _window_csr(problems: Sequence, who: str):
         lens = np.fromiter(map(len, lists), np.int64, W)
         p = np.zeros(W + 1, np.int64)
         np.cumsum(lens, out=p[1:])
+        arrs = [getattr(x, "arr", None) for x in lists]
+        if W and all(a is not None for a in arrs):   # windows.LiveSet: ids already as arrays
+            return p, np.concatenate(arrs).astype(np.int32, copy=False)
         idx = np.fromiter(itertools.chain.from_iterable(lists), np.int32, int(p[-1]))
         return p, idx
 

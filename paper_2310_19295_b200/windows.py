@@ -24,6 +24,19 @@ import numpy as np
 from .graph import graph_arrays
 
 
+class LiveSet(frozenset):
+    """The reference's frozenset of tensor ids, also carrying them as an
+    int32 array (``arr``) so the K4/K5 marshalling (ordering._window_csr) does
+    not walk the set element by element."""
+    __slots__ = ("arr",)
+
+
+def live_set(idx: np.ndarray) -> LiveSet:
+    s = LiveSet(idx.tolist())
+    s.arr = idx.astype(np.int32)
+    return s
+
+
 class Unsupported(Exception):
     """The linearisation lists an op in two windows; use the reference builder."""
 
@@ -79,7 +92,7 @@ def build_window_problems(g, lin, wu_plan=None, ops_per_step: int = 1, time_budg
         live_out = np.flatnonzero((b <= p) & (p < L))
         ops = final_ops[w.index]
         out.append((window_type(index=w.index, leaf=w.leaf, ops=ops),
-                    problem_type(graph=g, ops=ops, live_in=frozenset(live_in.tolist()),
-                                 live_out=frozenset(live_out.tolist()), ops_per_step=ops_per_step,
+                    problem_type(graph=g, ops=ops, live_in=live_set(live_in),
+                                 live_out=live_set(live_out), ops_per_step=ops_per_step,
                                  time_budget=time_budget, node_cap=node_cap)))
     return out

@@ -201,6 +201,8 @@ def test_subgraph_tree_dropin_matches_reference():
     graphs and the reference's own generators, across node limits; the
     weight-update-branch and linearize caches hand out equal, independent
     results (host-only)."""
+    import memplan.graphgen  # noqa: F401  (mp.graphgen)
+
     from paper_2310_19295_b200 import control
     from paper_2310_19295_b200 import graphgen as gg
     seg = mp.segmentation
