@@ -288,6 +288,114 @@ __global__ void __launch_bounds__(NT) k3_llfb(const K3Args a) {
 
   // ---- sequential placement, parallel _lowest_fit
   long long cap_rest = LLONG_MIN;
+  if constexpr (NT * MAXC <= 8192) {
+    // Placed list in registers: thread t owns list slots [t*MAXC, (t+1)*MAXC)
+    // as {lo, hi, start, end}; empty slots never overlap and sort last.  An
+    // insertion shifts the suffix with lo > res one slot right: within a
+    // thread by register selects, across threads by one shuffle (lane 0
+    // reads the previous warp's last slot, double-buffered by item parity).
+    // NT = 512: start | end << 16 in one register (the host routes problems
+    // with timesteps >= 65535 elsewhere), so the list fits 128 registers
+    constexpr bool PK = NT > 256;
+    __shared__ long long s_plo[2][NT / 32], s_phi[2][NT / 32];
+    __shared__ int s_pst[2][NT / 32], s_pen[2][NT / 32];
+    const int lane = tid & 31, w = tid >> 5;
+    long long rlo[MAXC], rhi[MAXC];
+    int rst[MAXC], ren[PK ? 1 : MAXC];
+    auto t_st = [&](int m) { return PK ? (rst[m] & 0xffff) : rst[m]; };
+    auto t_en = [&](int m) { return PK ? ((unsigned)rst[m] >> 16) : ren[PK ? 0 : m]; };
+#pragma unroll
+    for (int m = 0; m < MAXC; ++m) {
+      const int j = tid * MAXC + m;
+      int a0 = INT_MAX, a1 = INT_MIN;
+      if (j < P) {
+        const int q = ord[j];
+        rlo[m] = off[q];
+        rhi[m] = off[q] + sz[q];
+        a0 = st[q];
+        a1 = en[q];
+      } else {
+        rlo[m] = LLONG_MAX;
+        rhi[m] = LLONG_MIN;
+      }
+      if (PK) {
+        rst[m] = j < P ? (a0 | (a1 << 16)) : 0xffff;  // empty: start 65535 > every end
+      } else {
+        rst[m] = a0;
+        ren[PK ? 0 : m] = a1;
+      }
+    }
+    for (int k = A; k < N; ++k) {
+      const int i = ord[k];
+      const int si = st[i], ei = en[i];
+      const long long szi = sz[i], fl = flo[i];
+      const int buf = k & 1;
+      if (lane == 31) {
+        s_plo[buf][w] = rlo[MAXC - 1];
+        s_phi[buf][w] = rhi[MAXC - 1];
+        s_pst[buf][w] = rst[MAXC - 1];
+        if (!PK) s_pen[buf][w] = ren[PK ? 0 : MAXC - 1];
+      }
+      long long mx = LLONG_MIN;
+#pragma unroll
+      for (int m = 0; m < MAXC; ++m)
+        if (t_st(m) <= ei && si <= t_en(m)) mx = max(mx, rhi[m]);
+      long long all_mx;
+      long long M = max(fl, blk.excl_max(mx, &all_mx));
+      int brk = INT_MAX;
+      long long at = 0;
+#pragma unroll
+      for (int m = 0; m < MAXC; ++m) {
+        if (t_st(m) <= ei && si <= t_en(m) && brk == INT_MAX) {
+          if (M + szi <= rlo[m]) {
+            brk = tid * MAXC + m;
+            at = M;
+          } else {
+            M = max(M, rhi[m]);
+          }
+        }
+      }
+      long long res;
+      if (blk.min_key(brk, at, &res) == INT_MAX) res = max(fl, all_mx);
+      // the slot before this thread's first one
+      long long plo = __shfl_up_sync(0xffffffffu, rlo[MAXC - 1], 1);
+      long long phi = __shfl_up_sync(0xffffffffu, rhi[MAXC - 1], 1);
+      int pst = __shfl_up_sync(0xffffffffu, rst[MAXC - 1], 1);
+      int pen = PK ? 0 : __shfl_up_sync(0xffffffffu, ren[PK ? 0 : MAXC - 1], 1);
+      if (lane == 0) {
+        if (w == 0) {
+          plo = LLONG_MIN;  // list start: the item goes first if slot 0 moves
+        } else {
+          plo = s_plo[buf][w - 1];
+          phi = s_phi[buf][w - 1];
+          pst = s_pst[buf][w - 1];
+          if (!PK) pen = s_pen[buf][w - 1];
+        }
+      }
+      const int ist = PK ? (si | (ei << 16)) : si;
+#pragma unroll
+      for (int m = 0; m < MAXC; ++m) {
+        // slots with lo <= res stay; the first other slot takes the item, the
+        // rest take their predecessor
+        const long long olo = rlo[m], ohi = rhi[m];
+        const int ost = rst[m], oen = PK ? 0 : ren[PK ? 0 : m];
+        if (olo > res) {
+          const bool first = plo <= res;
+          rlo[m] = first ? res : plo;
+          rhi[m] = first ? res + szi : phi;
+          rst[m] = first ? ist : pst;
+          if (!PK) ren[PK ? 0 : m] = first ? ei : pen;
+        }
+        plo = olo;
+        phi = ohi;
+        pst = ost;
+        pen = oen;
+      }
+      if (tid == 0) off[i] = res;
+      cap_rest = max(cap_rest, res + szi);
+    }
+    __syncthreads();
+  } else {
   for (int k = A; k < N; ++k) {
     const int i = ord[k];
     const int si = st[i], ei = en[i];
@@ -341,6 +449,7 @@ __global__ void __launch_bounds__(NT) k3_llfb(const K3Args a) {
     cap_rest = max(cap_rest, res + szi);
     ++P;
     __syncthreads();
+  }
   }
   if (tid == 0) {
     // capacity starts at the activation block (layout.py:127, 199)
@@ -512,9 +621,16 @@ extern "C" int rm_llfb_batch(int32_t P, const int64_t* item_ptr, const int32_t* 
   }
   K3Args a{P, d_ptr, d_t, d_s, d_e, d_sz, d_act, mode, d_off, d_cap, d_met, d_comp, d_ccap, d_g,
            d_goff};
+  // NT = 512 packs start | end << 16 per placed item
+  bool times16 = true;
+  for (int64_t k = 0; k < NI && times16; ++k)
+    times16 = start[k] >= 0 && end[k] >= 0 && start[k] < 65535 && end[k] < 65535;
   int rc;
-  if (maxN <= 255 * 16 + 15 && maxN < 4096)
+  // the register-resident placed list holds NT * 16 - 1 placed items
+  if (maxN < 4096)
     rc = launch_k3_t<256, 16>(a, P, smem, s);
+  else if (maxN < 8192 && times16)
+    rc = launch_k3_t<512, 16>(a, P, smem, s);
   else
     rc = launch_k3_t<1024, 16>(a, P, smem, s);
   if (rc) return rc;

@@ -87,7 +87,7 @@ def _rand_rows(rng, n, horizon, act_p):
     return rows
 
 
-@pytest.mark.parametrize("n", [1, 2, 31, 255, 256, 257, 1000, 3000])
+@pytest.mark.parametrize("n", [1, 2, 31, 255, 256, 257, 1000, 3000, 4095, 4096])
 def test_random_vs_oracle(n):
     rng = random.Random(1000 + n)
     rows = _rand_rows(rng, n, max(4, n // 3), 0.3)
@@ -105,6 +105,17 @@ def test_large_problem_global_scratch():
     rows = _rand_rows(rng, 6000, 2000, 0.2)
     items = _items(rows)
     b = pack_batch([items], CONSTRAINED)[0]
+    assert (b.offsets, b.capacity) == O.constrained_llfb_layout(rows)
+
+
+@pytest.mark.parametrize("n,horizon", [(5000, 1500), (8191, 3000), (8192, 3000), (6000, 70000)])
+def test_register_list_geometries(n, horizon):
+    """Placed lists of 4k-8k items (512 threads, start | end packed in 16 bits),
+    the first size past it (1024 threads, shared-memory list) and timesteps
+    beyond 16 bits (routed to the 1024-thread path)."""
+    rng = random.Random(n + horizon)
+    rows = _rand_rows(rng, n, horizon, 0.2)
+    b = pack_batch([_items(rows)], CONSTRAINED)[0]
     assert (b.offsets, b.capacity) == O.constrained_llfb_layout(rows)
 
 
