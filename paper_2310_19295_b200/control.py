@@ -383,6 +383,21 @@ def assign_shared_tensors_factory(mp):
     return assign_shared_tensors
 
 
+def classify_tensors_factory(mp):
+    """graph.py:471-492 classify_tensors, computed once per graph (the planner
+    asks from the tree build, the weight-update cost table, plan() itself and
+    validate_layout); every call gets its own dict of the reference's enums."""
+    ref = mp.graph.classify_tensors
+
+    def classify_tensors(g):
+        ent = graph_cache(g)
+        hit = ent.get("ref_categories")
+        if hit is None:
+            hit = ent["ref_categories"] = ref(g)
+        return dict(hit)
+    return classify_tensors
+
+
 def linearize_factory(mp):
     seg = mp.segmentation
     build = _linearize_factory(mp)

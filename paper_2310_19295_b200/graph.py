@@ -282,7 +282,16 @@ def validate_graph(g) -> ValidationReport:
 
 
 def classify_tensors(g) -> dict[int, TensorCategory]:
-    """Activation / gradient / temporary taxonomy (reference graph.py:471-492)."""
+    """Activation / gradient / temporary taxonomy (reference graph.py:471-492),
+    computed once per graph; each call returns its own dict."""
+    ent = graph_cache(g)
+    hit = ent.get("categories")
+    if hit is None:
+        hit = ent["categories"] = _classify(g)
+    return dict(hit)
+
+
+def _classify(g) -> dict[int, TensorCategory]:
     out: dict[int, TensorCategory] = {}
     for t in g.tensors:
         if TensorCategory(t.category) in _PINNED:

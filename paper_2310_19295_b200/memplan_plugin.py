@@ -29,6 +29,7 @@ Dispatch points rebound (reference file:line of the call site):
   segmentation.build_subgraph_tree (+ planner's)  segmentation.py:343-448: core,
                                  _mi_over and residual ranks from the same matrix
   graph/segmentation/ordering.weight_update_branches  graph.py:513: once per graph
+  graph/planner/ordering/segmentation.classify_tensors  graph.py:471: once per graph
   segmentation.assign_shared_tensors (+ planner's)  segmentation.py:598-639: one
                                  slot pass instead of one per floating op
   planner.build_window_problems  planner.py:141-149 interval stabbing on slot positions
@@ -151,8 +152,9 @@ def install(mp=None):
                 for k, r in zip(ks, batch([jobs[k][0] for k in ks])):
                     res[k] = r
         out = []
+        check_problem = T(_ord._check_problem)   # wrap once, not per window
         for k, ((p, limit), r) in enumerate(zip(jobs, res)):
-            T(_ord._check_problem)(p)
+            check_problem(p)
             if isinstance(r, GraphError):
                 T(functools.partial(_raise, r))()
             if isinstance(r, Exception):
@@ -220,8 +222,13 @@ def install(mp=None):
     fast_tree = _ctl.subgraph_tree_factory(mp)
     wu_branches = _ctl.weight_update_branches_factory(mp)
     fast_assign = _ctl.assign_shared_tensors_factory(mp)
+    cats = _ctl.classify_tensors_factory(mp)
     patches = {
         (mp.segmentation, "build_subgraph_tree"): fast_tree,
+        (gr, "classify_tensors"): cats,
+        (pl, "classify_tensors"): cats,
+        (ordm, "classify_tensors"): cats,
+        (mp.segmentation, "classify_tensors"): cats,
         (mp.segmentation, "assign_shared_tensors"): fast_assign,
         (pl, "assign_shared_tensors"): fast_assign,
         (pl, "build_subgraph_tree"): fast_tree,

@@ -20,6 +20,7 @@ def test_install_uninstall_roundtrip():
     names += [(mp.layout, "layout_violations"), (mp.simulator, "layout_violations"),
               (mp.segmentation, "build_subgraph_tree"), (mp.planner, "build_subgraph_tree"),
               (mp.ordering, "weight_update_branches"), (mp.planner, "assign_shared_tensors"),
+              (mp.planner, "classify_tensors"), (mp.graph, "classify_tensors"),
               (mp.ordering, "weight_update_cost"), (mp.ordering, "asap_alap"),
               (mp.planner, "build_window_problems"),
               (mp.simulator, "peak_memory")]
@@ -215,8 +216,10 @@ def test_subgraph_tree_dropin_matches_reference():
     for arch, blocks, opt in (("transformer_block", 6, "adam"), ("mlp", 5, "sgd"),
                               ("residual", 7, "adam"), ("transformer_block", 1, "sgd")):
         graphs.append(mp.graphgen.gen_training_graph(arch, blocks, optimizer=opt))
+    fast_cats = control.classify_tensors_factory(mp)
     for g in graphs:
         assert fast_wu(g) == ref_wu(g) and fast_wu(g) is not fast_wu(g)
+        assert fast_cats(g) == mp.graph.classify_tensors(g) and fast_cats(g) is not fast_cats(g)
         for limit in (2, 7, 20, 10**6):
             want = ref_tree(g, limit)
             got = fast_tree(g, limit)
