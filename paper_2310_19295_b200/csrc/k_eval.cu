@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(1024) k_live_scan(int steps, const long long* 
 template <class IdxT, int MAXC>
 static int launch_k1_t(K1Args& a, int grid, size_t smem, cudaStream_t s) {
   auto kern = k1_eval_orders<IdxT, MAXC>;
-  RM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  RM_CUDA(smem_optin(kern));
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (g_timing) {
     cudaEventCreate(&e0);

@@ -519,7 +519,7 @@ __global__ void __launch_bounds__(1024, 1) k1v3_eval_orders(const K1V2Args a) {
 template <bool PAIRS, typename RowT, int NT, int MAXC>
 static int launch_k1v2_t(K1V2Args& a, int grid, size_t smem, cudaStream_t s) {
   auto kern = PAIRS ? k1v3_eval_orders<RowT, NT, MAXC> : k1v2_eval_orders<RowT, NT, MAXC>;
-  RM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  RM_CUDA(smem_optin(kern));
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (g_timing) {
     cudaEventCreate(&e0);

@@ -389,7 +389,7 @@ __global__ void __launch_bounds__((v4_cta_cap(C) / NT) * NT, 1) k1v4_eval_orders
 template <typename RowT, int NT, int C, bool CLS = false>
 static int launch_k1v4_t(K1V4Args& a, int grid, size_t smem, cudaStream_t s) {
   auto kern = k1v4_eval_orders<RowT, NT, C, CLS>;
-  RM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  RM_CUDA(smem_optin(kern));
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (g_timing) {
     cudaEventCreate(&e0);

@@ -349,7 +349,7 @@ extern "C" int rm_exact_windows(RmGraph* g, int32_t W, const int64_t* win_ptr,
            d_ord, d_peak, d_nodes, d_st, d_v, gmax, max_ten};
   const size_t smem = (8u << K5_SMEM_N) + 8 * size_t(K5_MAX_N + max_ten) + 4 * size_t(K5_MAX_N + max_ten);
   constexpr int NT = 512;
-  RM_CUDA(cudaFuncSetAttribute(k5_exact<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  RM_CUDA(smem_optin(k5_exact<NT>));
   k5_exact<NT><<<grid, NT, smem, s>>>(a);
   RM_LAUNCH_CHECK("k5_exact launch");
   std::vector<int32_t> ord(gop.size()), st(W);

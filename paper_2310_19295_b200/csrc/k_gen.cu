@@ -120,14 +120,12 @@ int launch_gen(RmGraph* g, uint64_t seed, int64_t first_id, int64_t B, int32_t* 
   const int64_t blocks_needed = (B + wpb - 1) / wpb;
   const int grid = (int)std::min<int64_t>(blocks_needed, int64_t(sms) * 8);
   if (wide) {
-    RM_CUDA(cudaFuncSetAttribute(k_gen_orders<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
+    RM_CUDA(smem_optin(k_gen_orders<int32_t>));
     k_gen_orders<int32_t><<<grid, 32 * wpb, smem, s>>>(
         n, seed, first_id, B, g->d_pred_ptr.as<int32_t>(), g->d_succ_ptr.as<int32_t>(),
         g->d_succ_idx.as<int32_t>(), out, wpb);
   } else {
-    RM_CUDA(cudaFuncSetAttribute(k_gen_orders<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
+    RM_CUDA(smem_optin(k_gen_orders<uint16_t>));
     k_gen_orders<uint16_t><<<grid, 32 * wpb, smem, s>>>(
         n, seed, first_id, B, g->d_pred_ptr.as<int32_t>(), g->d_succ_ptr.as<int32_t>(),
         g->d_succ_idx.as<int32_t>(), out, wpb);

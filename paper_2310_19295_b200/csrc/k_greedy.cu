@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(NT) k4_greedy(const K4Args a) {
 template <int NT>
 static int launch_k4_t(const K4Args& a, size_t smem, cudaStream_t s) {
   auto kern = k4_greedy<NT>;
-  RM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  RM_CUDA(smem_optin(kern));
   kern<<<a.W, NT, smem, s>>>(a);
   RM_LAUNCH_CHECK("k4_greedy launch");
   return RM_OK;

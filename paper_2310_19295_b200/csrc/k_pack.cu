@@ -533,7 +533,7 @@ static int sm_max_smem(int dev) {
 template <int NT, int MAXC>
 static int launch_k3_t(const K3Args& a, int grid, size_t smem, cudaStream_t s) {
   auto kern = k3_llfb<NT, MAXC>;
-  RM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  RM_CUDA(smem_optin(kern));
   kern<<<grid, NT, smem, s>>>(a);
   RM_LAUNCH_CHECK("k3_llfb launch");
   return RM_OK;

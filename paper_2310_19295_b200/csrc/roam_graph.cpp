@@ -13,6 +13,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
+#include <set>
 #include <unordered_map>
 
 #include "roam_internal.h"
@@ -32,6 +34,24 @@ int cuda_fail(cudaError_t e, const char* what) {
   return RM_ERR_CUDA;
 }
 void note_launch(int64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+cudaError_t smem_optin_raw(const void* kern) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({dev, kern})) return cudaSuccess;
+  int optin = 0;
+  e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaFuncAttributes fa{};
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, kern);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
+  if (e == cudaSuccess) done.insert({dev, kern});
+  return e;
+}
 
 DevBuf::~DevBuf() {
   if (p) cudaFree(p);

@@ -30,6 +30,18 @@ void note_launch(int64_t k = 1);
     if (e_ != cudaSuccess) return ::roam::cuda_fail(e_, what); \
   } while (0)
 
+// ---- dynamic shared memory opt-in -------------------------------------------
+// Always the largest value the kernel can take (device opt-in limit minus its
+// static shared memory), never the size of the launch at hand: the library is
+// re-entrant, and a per-launch value set by one host thread could shrink the
+// limit between another thread's set and launch ("too many resources").
+// Done once per (device, kernel); later calls are a locked set lookup.
+cudaError_t smem_optin_raw(const void* kern);
+template <class Kern>
+inline cudaError_t smem_optin(Kern kern) {
+  return smem_optin_raw(reinterpret_cast<const void*>(kern));
+}
+
 // ---- device buffer owned by a handle --------------------------------------
 struct DevBuf {
   void* p = nullptr;

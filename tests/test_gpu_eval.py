@@ -314,3 +314,39 @@ def test_fused_key_selection(name, variant):
         assert int(key.item()) == 2**63 - 1
     finally:
         set_k1_variant(0)
+
+
+def test_host_staged_calls_from_two_threads():
+    """libroam is re-entrant: host-buffer calls of different batch sizes (so
+    different K1 launch geometries and shared-memory sizes) from two threads on
+    their own streams return what the same calls return one at a time."""
+    import threading
+
+    import torch
+    from paper_2310_19295_b200.evaluator import evaluate_and_select
+    g = load_graph(gg.config_doc("gpt2-small"))
+    orders = generate_orders(g, 5, 0, 6000).cpu().numpy().astype(np.uint16)
+    sizes = [6000, 37, 1500, 129, 4096, 5]
+    want = [evaluate_and_select(g, orders[:b], id_base=b) for b in sizes]
+    got = [None] * len(sizes)
+    errors = []
+
+    def worker(j):
+        try:
+            torch.cuda.set_device(0)
+            st = torch.cuda.Stream()
+            for _ in range(3):
+                for k in range(j, len(sizes), 2):
+                    got[k] = evaluate_and_select(g, orders[:sizes[k]], id_base=sizes[k], stream=st)
+        except Exception as e:  # surfaced below
+            errors.append(e)
+
+    ts = [threading.Thread(target=worker, args=(j,)) for j in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+    for w, r in zip(want, got):
+        assert np.array_equal(w[0], r[0]) and np.array_equal(w[1], r[1])
+        assert np.array_equal(w[2], r[2]) and w[3] == r[3]
