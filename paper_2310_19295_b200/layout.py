@@ -334,7 +334,7 @@ def repair_conflicts(m, p):
                 g_lo = np.append(g_lo, edge)
                 g_hi = np.append(g_hi, capacity)
             width = g_hi - g_lo
-            fit = np.flatnonzero(width >= it.size)
+            fit = (width >= it.size).nonzero()[0]
             if fit.size:
                 best = fit[np.argmin(width[fit])]   # first of the smallest
                 new = int(g_lo[best])

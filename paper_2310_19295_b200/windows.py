@@ -88,8 +88,8 @@ def build_window_problems(g, lin, wu_plan=None, ops_per_step: int = 1, time_budg
     out = []
     for w in lin.windows:
         p = slot_of_window[w.index]
-        live_in = np.flatnonzero((b < p) & (p <= L))
-        live_out = np.flatnonzero((b <= p) & (p < L))
+        live_in = ((b < p) & (p <= L)).nonzero()[0]
+        live_out = ((b <= p) & (p < L)).nonzero()[0]
         ops = final_ops[w.index]
         out.append((window_type(index=w.index, leaf=w.leaf, ops=ops),
                     problem_type(graph=g, ops=ops, live_in=live_set(live_in),

@@ -4,7 +4,7 @@ installed (memplan_plugin), plan documents checked byte-identical.
 
   python tools/plan_bench.py [--configs layered gpt2-small bert-large gpt2-xl] [--out f.json]
 
-Each planner runs once per config after one warm-up plan of a small graph (the
+Each planner runs once per config after warm-up plans of two small graphs (the
 reference is deterministic; wall clock, single process).  For the GPU run the
 top functions by cumulative time are recorded (cProfile) to show what stays on
 the host."""
@@ -34,9 +34,14 @@ def main():
     ap.add_argument("--skip-ref", action="store_true")
     a = ap.parse_args()
     mp = plug.load_memplan()
+    import memplan.graphgen as rgen
+    # warm-up: an inference graph and a small training graph, so both planner
+    # paths have loaded their modules and the CUDA context exists
     warm = mp.graph.load_graph(gg.config_doc("layered"))
+    warm_train = rgen.gen_training_graph("transformer_block", 2)
     plug.install(mp)
     mp.planner.plan(warm)       # CUDA context, module loads
+    mp.planner.plan(warm_train)
     plug.uninstall()
     rows = []
     for name in a.configs:
