@@ -247,6 +247,21 @@ int rm_llfb_batch(int32_t P, const int64_t* item_ptr, const int32_t* tensor,
                   const uint8_t* is_act, int32_t mode, int64_t* offset, int64_t* capacity,
                   uint8_t* bound_met, int32_t* comp, int64_t* comp_cap, void* stream);
 
+/* exact_layout's branch-and-bound (layout.py:226-290) for one problem K3's
+ * COMPONENTS pass could not decide: items as for rm_llfb_batch, bottom = the
+ * problem's activations_at_bottom, incumbent[item] = K3's COMPONENTS offsets.
+ * Components whose incumbent exceeds their bound are searched node for node
+ * like the reference (same branching order, same pruning, node_cap counted
+ * over all components; node_cap < 0 = none; deadline = CLOCK_MONOTONIC seconds
+ * checked every 4096 nodes, <= 0 = none).  Outputs: offset[item], capacity,
+ * nodes (the reference's LayoutStats.nodes) and optimal (0 when a budget
+ * stopped a search).  Host code (the search is sequential); components of
+ * more than 64 items fail with RM_ERR_CAPACITY. */
+int rm_layout_search(int32_t n, const int32_t* tensor, const int32_t* start, const int32_t* end,
+                     const int64_t* size, const uint8_t* is_act, int32_t bottom,
+                     const int64_t* incumbent, int64_t node_cap, double deadline, int64_t* offset,
+                     int64_t* capacity, int64_t* nodes, int32_t* optimal);
+
 /* ------------------------------------------- K4: batched window greedy */
 
 /* W greedy_order problems (ordering.py:78-180) over one graph.  Window w

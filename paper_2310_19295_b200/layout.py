@@ -225,34 +225,28 @@ def constrained_llfb_layout(p) -> MemoryLayout:
                         optimal=False, stats=LayoutStats(len(p.items), time.monotonic() - t0))
 
 
-class SearchRequired(RuntimeError):
-    """exact_layout's incumbent missed its lower bound: the branch-and-bound
-    (layout.py:226-290) must run; pass ``search=`` to delegate it."""
-
-
 def exact_layout(p, search=None) -> MemoryLayout:
-    """exact_layout (layout.py:153-302) decided on the GPU whenever every
-    overlap component's long-lived-first incumbent meets its lower bound --
-    then the reference returns that incumbent without search, and so does
-    this.  Otherwise ``search(p)`` is called (e.g. the reference's own
-    exact_layout) or SearchRequired is raised."""
-    t0 = time.monotonic()
+    """exact_layout (layout.py:153-302): K3 decides every problem whose overlap
+    components' long-lived-first incumbents meet their lower bounds (then the
+    reference returns that incumbent without search, and so does this); the
+    other components run the reference's branch-and-bound node for node in
+    libroam (``rm_layout_search``).  ``search(p)``, when given, replaces that
+    step (e.g. the reference's own exact_layout)."""
     if p.time_budget <= 0:
         from .graph import ConfigError
         raise ConfigError("time budget must be positive")
     if not p.items:
         return MemoryLayout(offsets={}, capacity=0, stats=LayoutStats(0, 0.0))
-    r = exact_layout_batch([p])[0]
-    if r is not None:
-        return r
-    if search is None:
-        raise SearchRequired("layout incumbent above its bound: branch-and-bound needed")
-    return search(p)
+    if search is not None:
+        r = exact_layout_batch([p], search=False)[0]
+        return r if r is not None else search(p)
+    return exact_layout_batch([p])[0]
 
 
-def exact_layout_batch(problems: Sequence) -> list[MemoryLayout | None]:
-    """K3 component pass over many exact_layout problems in one launch; None
-    where the search would run (incumbent above bound)."""
+def exact_layout_batch(problems: Sequence, search: bool = True) -> list[MemoryLayout | None]:
+    """K3 component pass over many exact_layout problems in one launch, then
+    the branch-and-bound (rm_layout_search) for the problems whose incumbent
+    missed its bound -- or None for them when ``search`` is False."""
     t0 = time.monotonic()
     out: list[MemoryLayout | None] = [None] * len(problems)
     for bottom in (True, False):
@@ -268,7 +262,30 @@ def exact_layout_batch(problems: Sequence) -> list[MemoryLayout | None]:
                 out[k] = MemoryLayout(offsets=r.offsets, capacity=r.capacity,
                                       activation_block=_act_block(p.items), optimal=True,
                                       stats=LayoutStats(0, time.monotonic() - t0))
+            elif search:
+                out[k] = _branch_and_bound(p, r, t0)
     return out
+
+
+def _branch_and_bound(p, r: PackResult, t0: float) -> MemoryLayout:
+    """layout.py:226-290 over K3's incumbent: one rm_layout_search call.  The
+    deadline is the reference's (t0 + time_budget on the monotonic clock)."""
+    items = p.items
+    N = len(items)
+    start, end, size = _item_arrays(items)
+    tensor = np.fromiter((i.tensor for i in items), np.int64, N).astype(np.int32)
+    is_act = np.fromiter((bool(i.is_activation) for i in items), np.uint8, N)
+    inc = np.fromiter((r.offsets[i.tensor] for i in items), np.int64, N)
+    offset = np.empty(N, np.int64)
+    cap, nodes, opt = C.c_int64(0), C.c_int64(0), C.c_int32(0)
+    check(lib().rm_layout_search(N, ptr(tensor), ptr(start), ptr(end), ptr(size), ptr(is_act),
+                                 1 if p.activations_at_bottom else 0, ptr(inc),
+                                 -1 if p.node_cap is None else int(p.node_cap), t0 + p.time_budget,
+                                 ptr(offset), C.byref(cap), C.byref(nodes), C.byref(opt)),
+          "rm_layout_search")
+    return MemoryLayout(offsets=dict(zip(tensor.tolist(), offset.tolist())), capacity=int(cap.value),
+                        activation_block=_act_block(items), optimal=bool(opt.value),
+                        stats=LayoutStats(int(nodes.value), time.monotonic() - t0))
 
 
 # --------------------------------------------------------- conflict repair

@@ -17,8 +17,8 @@ Dispatch points rebound (reference file:line of the call site):
                               exact_order DFS only where its node cap can bind)
         _solve_layout jobs -> every leaf in ONE K3 launch per mode
                               (constrained LLFB for big leaves, exact_layout's
-                              incumbent+bound for small ones; the reference's
-                              branch-and-bound only where incumbent > bound)
+                              incumbent+bound for small ones, its branch-and-
+                              bound in libroam where incumbent > bound)
   planner.repair_conflicts       planner.py:259    K2 detection + mover placement
   planner.validate_layout        planner.py:260    K2
   ordering.weight_update_cost    ordering.py:310   event sweep once per (graph, bounds)
@@ -113,7 +113,7 @@ class _State:
 
 # dispatch counters since install(): how the planner's subtasks were served
 STATS = {"windows_k4": 0, "windows_k5": 0, "windows_ref_exact": 0, "leaves_k3_constrained": 0,
-         "leaves_k3_exact": 0, "leaves_ref_search": 0}
+         "leaves_k3_exact": 0, "leaves_search": 0}
 
 
 def install(mp=None):
@@ -127,7 +127,6 @@ def install(mp=None):
     orig_solve_window = pl._solve_window
     orig_solve_layout = pl._solve_layout
     orig_pool_map = pl._pool_map
-    ref_exact_layout = lay.exact_layout
     ref_exact_order = ordm.exact_order
 
     def to_layout(m):
@@ -192,11 +191,12 @@ def install(mp=None):
             for p in (jobs[k][0] for k in small):
                 if p.time_budget <= 0:
                     raise gr.ConfigError("time budget must be positive")
+            # K3 decides the leaves whose incumbents meet their bounds; the
+            # others run the branch-and-bound in libroam (rm_layout_search)
             res = _lay.exact_layout_batch([jobs[k][0] for k in small])
             for k, r in zip(small, res):
-                # incumbent above bound: the reference's branch-and-bound decides
-                out[k] = to_layout(r) if r is not None else ref_exact_layout(jobs[k][0])
-                STATS["leaves_k3_exact" if r is not None else "leaves_ref_search"] += 1
+                out[k] = to_layout(r)
+                STATS["leaves_search" if r.stats.nodes else "leaves_k3_exact"] += 1
         return out
 
     def pool_map(fn, jobs, workers):

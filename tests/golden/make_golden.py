@@ -321,6 +321,35 @@ def make_layouts():
     dump("layouts.json", {"violations": viol, "spec": spec, "llfb": llfb, "exact": exact})
 
 
+# ---------------------------------------------------------- layout search
+
+def make_layout_search():
+    """exact_layout problems whose incumbent misses its bound, so the
+    reference's branch-and-bound runs (layout.py:226-290): both activation
+    modes, full searches and node-capped ones (optimal=False, partial best)."""
+    rng = random.Random(23)
+    cases = []
+    tries = 0
+    while len(cases) < 120 and tries < 20000:
+        tries += 1
+        n = rng.randint(3, 16)
+        items = rand_items(rng, n, act_p=0.3, horizon=rng.choice([3, 4, 6, n]))
+        bottom = rng.random() < 0.6
+        p = rl.LayoutProblem(items=tuple(items), activations_at_bottom=bottom, node_cap=200_000)
+        m = rl.exact_layout(p)
+        if m.stats.nodes == 0:
+            continue
+        runs = [(200_000, m)]
+        for cap in sorted({1, max(1, m.stats.nodes // 3), max(1, m.stats.nodes - 1)}):
+            q = rl.LayoutProblem(items=tuple(items), activations_at_bottom=bottom, node_cap=cap)
+            runs.append((cap, rl.exact_layout(q)))
+        for cap, r in runs:
+            cases.append({"items": [it_row(i) for i in items], "bottom": bottom, "node_cap": cap,
+                          "offsets": {str(t): o for t, o in r.offsets.items()}, "capacity": r.capacity,
+                          "optimal": r.optimal, "nodes": r.stats.nodes})
+    dump("layout_search.json", {"cases": cases})
+
+
 # ---------------------------------------------------------------- greedy
 
 def make_greedy():
@@ -450,7 +479,8 @@ def make_plans():
 
 
 if __name__ == "__main__":
-    which = set(sys.argv[1:]) or {"peaks", "schedules", "layouts", "greedy", "exact", "plans"}
-    for w in ("peaks", "schedules", "layouts", "greedy", "exact", "plans"):
+    which = set(sys.argv[1:]) or {"peaks", "schedules", "layouts", "layout_search", "greedy", "exact",
+                                  "plans"}
+    for w in ("peaks", "schedules", "layouts", "layout_search", "greedy", "exact", "plans"):
         if w in which:
             globals()[f"make_{w}"]()

@@ -11,7 +11,7 @@ import pytest
 from conftest import golden
 from oracle import memplan_oracle as O
 from paper_2310_19295_b200.layout import (COMPONENTS, CONSTRAINED, PLAIN, LayoutItem, LayoutProblem,
-                                          SearchRequired, constrained_llfb_layout, exact_layout,
+                                          constrained_llfb_layout, exact_layout,
                                           exact_layout_batch, llfb_layout, pack_batch)
 
 pytestmark = pytest.mark.gpu
@@ -53,20 +53,22 @@ def test_llfb_and_constrained_golden():
 
 def test_exact_golden_decided_without_search():
     """Every golden exact_layout case the reference closed at 0 nodes is decided
-    by K3 alone (same offsets and capacity); the others report the search."""
+    by K3 alone (same offsets and capacity); the others need the search."""
     cases = golden("layouts")["exact"]
     probs = [LayoutProblem(items=_items(c["items"]), activations_at_bottom=True, node_cap=200_000)
              for c in cases]
-    res = exact_layout_batch(probs)
+    res = exact_layout_batch(probs, search=False)
     for c, p, r in zip(cases, probs, res):
         if c["nodes"] == 0:
             assert r is not None, c
             assert r.offsets == _offs(c["offsets"]) and r.capacity == c["capacity"] and r.optimal
         else:
             assert r is None, c
-            with pytest.raises(SearchRequired):
-                exact_layout(p)
             assert exact_layout(p, search=lambda q: "searched") == "searched"
+    # with the search (rm_layout_search) every case is the reference's answer
+    for c, r in zip(cases, exact_layout_batch(probs)):
+        assert (r.offsets, r.capacity, r.optimal, r.stats.nodes) == \
+            (_offs(c["offsets"]), c["capacity"], c["optimal"], c["nodes"]), c
 
 
 def test_exact_spec_examples():
