@@ -262,6 +262,20 @@ int rm_layout_search(int32_t n, const int32_t* tensor, const int32_t* start, con
                      const int64_t* incumbent, int64_t node_cap, double deadline, int64_t* offset,
                      int64_t* capacity, int64_t* nodes, int32_t* optimal);
 
+/* exact_order's capped depth-first search (ordering.py:183-286) for one
+ * window, node for node (memo on the scheduled mask, the reference's branch
+ * pruning and reconstruction walk), for the windows rm_exact_windows hands
+ * back (status 3: more order ideals than the node cap).  node_cap < 0 = none;
+ * deadline = CLOCK_MONOTONIC seconds checked every 1024 nodes (<= 0 = none).
+ * status: 0 searched (order[n_ops] global ids, peak, nodes), 1 ConfigError
+ * (bad_tensor: live-in tensor without a window consumer), 2 precedence cycle,
+ * 4 budget -- the reference then returns its greedy incumbent.  Host code;
+ * windows of more than 64 ops fail with RM_ERR_CAPACITY. */
+int rm_exact_order_search(RmGraph* g, int32_t n_ops, const int32_t* ops, int64_t n_lin,
+                          const int32_t* lin, int64_t n_lout, const int32_t* lout, int64_t node_cap,
+                          double deadline, int32_t* order, int64_t* peak, int64_t* nodes,
+                          int32_t* status, int32_t* bad_tensor);
+
 /* ------------------------------------------- K4: batched window greedy */
 
 /* W greedy_order problems (ordering.py:78-180) over one graph.  Window w

@@ -21,7 +21,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB_PATH = PKG / "libroam.so"
-SOURCES = ("roam_graph.cpp", "layout_search.cpp", "k_eval.cu", "k_eval_v2.cu", "k_eval_v4.cu", "k_gen.cu", "k_layout.cu", "k_pack.cu", "k_greedy.cu", "k_exact.cu")
+SOURCES = ("roam_graph.cpp", "layout_search.cpp", "order_search.cpp", "k_eval.cu", "k_eval_v2.cu", "k_eval_v4.cu", "k_gen.cu", "k_layout.cu", "k_pack.cu", "k_greedy.cu", "k_exact.cu")
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 
 
@@ -125,6 +125,8 @@ SIGNATURES = {
                                 vp, vp]),
     "rm_layout_search": (C.c_int, [C.c_int32, vp, vp, vp, vp, vp, C.c_int32, vp, C.c_int64, C.c_double,
                                    vp, vp, vp, vp]),
+    "rm_exact_order_search": (C.c_int, [vp, C.c_int32, vp, C.c_int64, vp, C.c_int64, vp, C.c_int64,
+                                        C.c_double, vp, vp, vp, vp, vp]),
     "rm_greedy_windows": (C.c_int, [vp, C.c_int32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "rm_exact_windows": (C.c_int, [vp, C.c_int32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "rm_last_error": (C.c_char_p, []),

@@ -112,7 +112,7 @@ class _State:
 
 
 # dispatch counters since install(): how the planner's subtasks were served
-STATS = {"windows_k4": 0, "windows_k5": 0, "windows_ref_exact": 0, "leaves_k3_constrained": 0,
+STATS = {"windows_k4": 0, "windows_k5": 0, "windows_dfs": 0, "windows_dfs_budget": 0, "leaves_k3_constrained": 0,
          "leaves_k3_exact": 0, "leaves_search": 0}
 
 
@@ -127,7 +127,6 @@ def install(mp=None):
     orig_solve_window = pl._solve_window
     orig_solve_layout = pl._solve_layout
     orig_pool_map = pl._pool_map
-    ref_exact_order = ordm.exact_order
 
     def to_layout(m):
         return lay.MemoryLayout(offsets=m.offsets, capacity=m.capacity,
@@ -159,8 +158,20 @@ def install(mp=None):
             if isinstance(r, Exception):
                 raise r
             if r is _ord.NEEDS_SEARCH:
-                out.append(ref_exact_order(p))
-                STATS["windows_ref_exact"] += 1
+                # more order ideals than the node cap: the capped DFS in libroam
+                r = _ord.search_window(p)
+                if isinstance(r, GraphError):
+                    T(functools.partial(_raise, r))()
+                if isinstance(r, Exception):
+                    raise r
+                if r is _ord.BUDGET:   # the reference returns its greedy incumbent
+                    out.append(_ord.greedy_orders([p], ordm.OrderingSolution, ordm.SolverStats)[0])
+                    STATS["windows_dfs_budget"] += 1
+                else:
+                    order, peak, nodes = r
+                    out.append(ordm.OrderingSolution(order=order, peak=peak, optimal=True,
+                                                      stats=ordm.SolverStats(nodes, 0.0)))
+                    STATS["windows_dfs"] += 1
             elif k in exact_keys:
                 order, peak, nodes = r
                 out.append(ordm.OrderingSolution(order=order, peak=peak, optimal=True,

@@ -177,14 +177,46 @@ def exact_windows(problems: Sequence) -> list:
     return out
 
 
+BUDGET = object()   # rm_exact_order_search status 4: the reference returns its greedy incumbent
+
+
+def search_window(p):
+    """exact_order's capped DFS (ordering.py:183-286) on the host in libroam
+    (rm_exact_order_search), node for node: (order, peak, nodes), BUDGET when
+    the node cap or the deadline stops it, or the exception the reference
+    raises.  The deadline is the reference's (t0 + time_budget, monotonic)."""
+    from .evaluator import device_graph
+    t0 = time.monotonic()
+    dg = device_graph(p.graph)
+    ops = np.asarray(sorted(p.ops), np.int32)
+    lin = np.asarray(sorted(p.live_in), np.int32)
+    lout = np.asarray(sorted(p.live_out), np.int32)
+    order = np.empty(max(len(ops), 1), np.int32)
+    peak, nodes = C.c_int64(0), C.c_int64(0)
+    status, bad = C.c_int32(0), C.c_int32(-1)
+    check(lib().rm_exact_order_search(dg.handle, len(ops), ptr(ops), len(lin), ptr(lin), len(lout), ptr(lout),
+                                      -1 if p.node_cap is None else int(p.node_cap), t0 + p.time_budget,
+                                      ptr(order), C.byref(peak), C.byref(nodes), C.byref(status),
+                                      C.byref(bad)), "rm_exact_order_search")
+    if status.value == 1:
+        return ConfigError(f"live-in tensor {bad.value} has no consumer in the window and is not live-out")
+    if status.value == 2:
+        return AssertionError("window precedence contains a cycle")
+    if status.value == 4:
+        return BUDGET
+    return tuple(order[:len(ops)].tolist()), int(peak.value), int(nodes.value)
+
+
 def exact_orders(problems: Sequence, search=None, solution_type=OrderingSolution,
                  stats_type=SolverStats) -> list:
     """exact_order over many windows (one K5 launch per graph).  Windows whose
-    order ideals outnumber their node cap go to ``search`` (the reference's
-    exact_order when called through the planner plug-in); without one they
-    raise RoamError -- there is no CPU path here.  ``stats.nodes`` is the
-    number of order ideals minus one, an upper bound on the reference DFS's
-    expansions (the plan documents never contain it)."""
+    order ideals outnumber their node cap run the reference's capped DFS in
+    libroam (``search_window``): its optimum, or -- when the cap stops it --
+    the greedy incumbent (K4), flagged non-optimal, as the reference returns.
+    ``search`` overrides that step (e.g. the reference's own exact_order).
+    ``stats.nodes`` is the DFS's node count for searched windows and the
+    number of order ideals minus one for K5's (an upper bound on the
+    reference's expansions; the plan documents never contain it)."""
     t0 = time.monotonic()
     for p in problems:
         _check_problem(p)
@@ -201,11 +233,15 @@ def exact_orders(problems: Sequence, search=None, solution_type=OrderingSolution
         if isinstance(r, Exception):
             raise r
         if r is NEEDS_SEARCH:
-            if search is None:
-                raise _lib.RoamError("exact_order: the window has more order ideals than its node cap; "
-                                     "the reference's capped search decides it (pass search=)")
-            out.append(search(p))
-            continue
+            if search is not None:
+                out.append(search(p))
+                continue
+            r = search_window(p)
+            if isinstance(r, Exception):
+                raise r
+            if r is BUDGET:
+                out.append(greedy_orders([p], solution_type, stats_type)[0])
+                continue
         order, peak, nodes = r
         out.append(solution_type(order=order, peak=peak, optimal=True,
                                  stats=stats_type(nodes=nodes, wall_time=wall)))
@@ -213,5 +249,6 @@ def exact_orders(problems: Sequence, search=None, solution_type=OrderingSolution
 
 
 def exact_order(p, search=None) -> OrderingSolution:
-    """Minimum-peak window order (ordering.py:183-286) on the GPU (K5)."""
+    """Minimum-peak window order (ordering.py:183-286): K5 on the GPU, the
+    capped DFS in libroam where the node cap can bind."""
     return exact_orders([p], search=search)[0]

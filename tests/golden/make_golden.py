@@ -387,6 +387,41 @@ def make_greedy():
     dump("greedy.json", {"cases": out, "graphs": graphs})
 
 
+# ------------------------------------------------------- exact order DFS
+
+def make_exact_search():
+    """exact_order's capped DFS (ordering.py:183-286) on wide windows -- the
+    ones whose order ideals can outnumber a node cap -- under caps from tiny
+    (the cap stops it: greedy incumbent, optimal=False) to roomy (the pruned
+    search finishes: its order, peak and node count)."""
+    from memplan.graphgen import gen_random_dag
+    rng = random.Random(31)
+    cases, graphs = [], {}
+    for k in range(40):
+        n = rng.randint(6, 18)
+        g = gen_random_dag(n, density=rng.choice([0.05, 0.1, 0.15, 0.25]), seed=900 + k)
+        name = f"dag{k}"
+        graphs[name] = rg.graph_to_doc(g)
+        windows = [(list(range(g.n_ops)), [], [])]
+        for _ in range(2):
+            ops, li, lo = random_window(g, rng)
+            windows.append((ops, sorted(li), sorted(lo)))
+        for ops, li, lo in windows:
+            for cap in (rng.choice([1, 5, 20]), rng.choice([50, 200, 1000]), 500_000):
+                prob = ro.OrderingProblem(graph=g, ops=tuple(ops), live_in=frozenset(li),
+                                          live_out=frozenset(lo), node_cap=cap)
+                try:
+                    sol = ro.exact_order(prob)
+                except rg.ConfigError as e:
+                    cases.append({"graph": name, "ops": ops, "live_in": li, "live_out": lo,
+                                  "node_cap": cap, "error": str(e)})
+                    continue
+                cases.append({"graph": name, "ops": ops, "live_in": li, "live_out": lo, "node_cap": cap,
+                              "order": list(sol.order), "peak": sol.peak, "optimal": sol.optimal,
+                              "nodes": sol.stats.nodes})
+    dump("exact_search.json", {"cases": cases, "graphs": graphs})
+
+
 # ---------------------------------------------------------------- exact
 
 def random_window(g, rng):
@@ -480,7 +515,7 @@ def make_plans():
 
 if __name__ == "__main__":
     which = set(sys.argv[1:]) or {"peaks", "schedules", "layouts", "layout_search", "greedy", "exact",
-                                  "plans"}
-    for w in ("peaks", "schedules", "layouts", "layout_search", "greedy", "exact", "plans"):
+                                  "exact_search", "plans"}
+    for w in ("peaks", "schedules", "layouts", "layout_search", "greedy", "exact", "exact_search", "plans"):
         if w in which:
             globals()[f"make_{w}"]()

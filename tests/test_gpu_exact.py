@@ -13,7 +13,6 @@ import pytest
 from conftest import golden
 from oracle import memplan_oracle as O
 from paper_2310_19295_b200 import graphgen as gg
-from paper_2310_19295_b200._lib import RoamError
 from paper_2310_19295_b200.graph import ConfigError, load_graph
 from paper_2310_19295_b200.ordering import (NEEDS_SEARCH, OrderingProblem, exact_order, exact_orders,
                                             exact_windows)
@@ -57,9 +56,11 @@ def test_cap_hit_windows_go_back_to_the_search():
     assert hit
     for g, c in hit:
         assert exact_windows([_problem(g, c)])[0] is NEEDS_SEARCH
-        with pytest.raises(RoamError):
-            exact_order(_problem(g, c))
-        # with the reference's search as the fallback the answer is its own
+        # the capped DFS (rm_exact_order_search) stops where the reference's
+        # does, and the answer is the greedy incumbent, flagged non-optimal
+        sol = exact_order(_problem(g, c))
+        assert (list(sol.order), sol.peak, sol.optimal) == (c["order"], c["peak"], False)
+        # an explicit search= still overrides that step
         sol = exact_order(_problem(g, c), search=lambda p: ("searched", p.node_cap))
         assert sol == ("searched", c["node_cap"])
 
