@@ -291,17 +291,23 @@ def classify_tensors(g) -> dict[int, TensorCategory]:
     return dict(hit)
 
 
+_KIND_OF = {k.value: k for k in OpKind}          # str-valued enums hash as their value,
+_CAT_OF = {c.value: c for c in TensorCategory}   # so the reference's members look up too
+
+
 def _classify(g) -> dict[int, TensorCategory]:
+    kinds = [_KIND_OF.get(o.kind) or OpKind(o.kind) for o in g.ops]
+    fwd, bwd, wu = OpKind.FORWARD, OpKind.BACKWARD, OpKind.WEIGHT_UPDATE
     out: dict[int, TensorCategory] = {}
     for t in g.tensors:
-        if TensorCategory(t.category) in _PINNED:
-            out[t.id] = TensorCategory(t.category)
+        cat = _CAT_OF.get(t.category) or TensorCategory(t.category)
+        if cat in _PINNED:
+            out[t.id] = cat
             continue
-        pk = OpKind(g.ops[t.producer].kind)
-        ck = {OpKind(g.ops[c].kind) for c in t.consumers}
-        if pk is OpKind.FORWARD and OpKind.BACKWARD in ck:
+        pk = kinds[t.producer]
+        if pk is fwd and any(kinds[c] is bwd for c in t.consumers):
             out[t.id] = TensorCategory.ACTIVATION
-        elif pk is OpKind.BACKWARD and OpKind.WEIGHT_UPDATE in ck:
+        elif pk is bwd and any(kinds[c] is wu for c in t.consumers):
             out[t.id] = TensorCategory.GRADIENT
         else:
             out[t.id] = TensorCategory.TEMPORARY_BUFFER
@@ -369,7 +375,8 @@ def graph_arrays(g) -> GraphArrays:
     out_ptr = np.zeros(n + 1, dtype=np.int64)
     np.cumsum(out_len, out=out_ptr[1:])
     out_idx = np.fromiter((t for o in g.ops for t in o.outputs), dtype=np.int32, count=int(out_ptr[-1]))
-    op_kind = np.fromiter((KIND_CODE[OpKind(o.kind)] for o in g.ops), dtype=np.uint8, count=n)
+    op_kind = np.fromiter((KIND_CODE[_KIND_OF.get(o.kind) or OpKind(o.kind)] for o in g.ops),
+                          dtype=np.uint8, count=n)
     cats = classify_tensors(g)
     is_act = np.fromiter((cats[t] is TensorCategory.ACTIVATION for t in range(T)), dtype=np.uint8, count=T)
     if max(int(cons_ptr[-1]), int(in_ptr[-1]), int(out_ptr[-1])) >= 2**31:
