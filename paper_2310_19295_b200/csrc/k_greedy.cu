@@ -17,11 +17,15 @@
 //                           twice by one op is never freed by this solver.)
 //
 // Host (C++, this file): builds every window's local problem from the graph
-// handle's CSR in O(window + its consumer entries).  Device: per step, each
-// thread scores its ready ops, a block (delta, index) argmin picks the op, one
-// warp applies it (counts, frees, successor pred counts).  Mutable state
-// (pred counts, consumer counts, scheduled flags) lives in shared memory when
-// it fits, else in a per-window global scratch.
+// handle's CSR in O(window + its consumer entries).  Device: each op's score
+// (out - bytes its inputs would free) is kept in shared memory and updated
+// incrementally -- a tracked tensor's count only falls when an op runs, and
+// when it reaches 1 the one op still holding an entry (found in the tensor's
+// local consumer list) now frees it -- so per step each thread only compares
+// the scores of its ready ops, a block (score, index) argmin picks the op, and
+// one warp applies it (counts, the score updates, frees, successor pred
+// counts).  Mutable state lives in shared memory when it fits, else in a
+// per-window global scratch.
 #include <algorithm>
 #include <climits>
 
@@ -42,6 +46,8 @@ struct K4Args {
   const int64_t* succ_ptr;  // [NO+1] into succ_idx (window-local op index)
   const int32_t* succ_idx;
   const int32_t* count0;    // [NT_] tracked consumer-entry counts
+  const int64_t* tc_ptr;    // [NT_+1] local consumer ops of each tracked tensor
+  const int32_t* tc_idx;
   const int64_t* tsize;     // [NT_]
   const int64_t* start_live;  // [W]
   int32_t* order;           // [NO] global op ids in schedule order
@@ -53,7 +59,7 @@ struct K4Args {
 
 __host__ __device__ inline size_t k4_bytes(int64_t n_ops, int64_t n_ten) {
   auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
-  return al(4 * size_t(n_ops)) + al(size_t(n_ops)) + al(4 * size_t(n_ten));
+  return al(8 * size_t(n_ops)) + al(4 * size_t(n_ops)) + al(size_t(n_ops)) + al(4 * size_t(n_ten));
 }
 
 template <int NT>
@@ -70,9 +76,11 @@ __global__ void __launch_bounds__(NT) k4_greedy(const K4Args a) {
   const int nt = (int)(a.ten_base[w + 1] - tb);
   auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
   unsigned char* ws = a.gscratch_off[w] < 0 ? smem : a.gscratch + a.gscratch_off[w];
-  int* npred = reinterpret_cast<int*>(ws);
-  unsigned char* done = ws + al(4 * size_t(n));
-  int* cnt = reinterpret_cast<int*>(ws + al(4 * size_t(n)) + al(size_t(n)));
+  long long* delta = reinterpret_cast<long long*>(ws);  // out - bytes freed if run now
+  int* npred = reinterpret_cast<int*>(ws + al(8 * size_t(n)));
+  unsigned char* done = ws + al(8 * size_t(n)) + al(4 * size_t(n));
+  int* cnt = reinterpret_cast<int*>(ws + al(8 * size_t(n)) + al(4 * size_t(n)) + al(size_t(n)));
+  const int64_t* tc_ptr = a.tc_ptr + tb;
   const int64_t* out = a.out + ob;
   const int64_t* in_ptr = a.in_ptr + ob;
   const int64_t* succ_ptr = a.succ_ptr + ob;
@@ -80,6 +88,14 @@ __global__ void __launch_bounds__(NT) k4_greedy(const K4Args a) {
   for (int i = tid; i < n; i += NT) {
     npred[i] = a.npred0[ob + i];
     done[i] = 0;
+    // the score is kept up to date instead of recomputed every step: an
+    // input frees when its count is 1, and counts only fall when an op runs
+    long long freed = 0;
+    for (int64_t k = in_ptr[i]; k < in_ptr[i + 1]; ++k) {
+      const int t = __ldg(a.in_idx + k);
+      if (a.count0[tb + t] == 1) freed += tsize[t];
+    }
+    delta[i] = out[i] - freed;
   }
   for (int t = tid; t < nt; t += NT) cnt[t] = a.count0[tb + t];
   if (tid == 0) {
@@ -94,12 +110,7 @@ __global__ void __launch_bounds__(NT) k4_greedy(const K4Args a) {
     int bi = INT_MAX;
     for (int i = tid; i < n; i += NT) {
       if (done[i] || npred[i]) continue;
-      long long freed = 0;
-      for (int64_t k = in_ptr[i]; k < in_ptr[i + 1]; ++k) {
-        const int t = __ldg(a.in_idx + k);
-        if (cnt[t] == 1) freed += tsize[t];
-      }
-      const long long d = out[i] - freed;
+      const long long d = delta[i];
       if (d < bv) {  // ascending i per thread: strict < keeps the smallest
         bv = d;
         bi = i;
@@ -138,7 +149,19 @@ __global__ void __launch_bounds__(NT) k4_greedy(const K4Args a) {
         long long freed = 0;
         for (int64_t k = in_ptr[bi] + lane; k < in_ptr[bi + 1]; k += 32) {
           const int t = __ldg(a.in_idx + k);
-          if (--cnt[t] == 0) freed += tsize[t];  // distinct inputs: no races
+          const int c = --cnt[t];  // distinct inputs: no races
+          if (c == 0) freed += tsize[t];
+          if (c == 1) {
+            // one consumer entry left: its op (not run yet) now frees t
+            for (int64_t q = tc_ptr[t]; q < tc_ptr[t + 1]; ++q) {
+              const int j = __ldg(a.tc_idx + q);
+              if (j != bi && !done[j]) {
+                atomicAdd(reinterpret_cast<unsigned long long*>(delta + j),
+                          (unsigned long long)(-tsize[t]));
+                break;
+              }
+            }
+          }
         }
         for (int64_t k = succ_ptr[bi] + lane; k < succ_ptr[bi + 1]; k += 32)
           npred[__ldg(a.succ_idx + k)] -= 1;     // distinct successors
@@ -202,8 +225,8 @@ extern "C" int rm_greedy_windows(RmGraph* g, int32_t W, const int64_t* win_ptr,
   std::vector<int32_t> loc(n, -1), tloc(T, -1);
   std::vector<uint8_t> is_lin(T, 0), is_lout(T, 0);
   std::vector<int64_t> op_base(W + 1, 0), ten_base(W + 1, 0), start_live(W, 0);
-  std::vector<int32_t> gop, npred0, in_idx, succ_idx, count0;
-  std::vector<int64_t> out_b, in_ptr(1, 0), succ_ptr(1, 0), tsize;
+  std::vector<int32_t> gop, npred0, in_idx, succ_idx, count0, tc_idx;
+  std::vector<int64_t> out_b, in_ptr(1, 0), succ_ptr(1, 0), tsize, tc_ptr(1, 0);
   std::vector<int32_t> ops, rel, tmp;
   std::vector<std::vector<int32_t>> succ;
   std::vector<uint8_t> held;
@@ -257,6 +280,9 @@ extern "C" int rm_greedy_windows(RmGraph* g, int32_t W, const int64_t* win_ptr,
         tloc[t] = nt++;
         tsize.push_back(g->size[t]);
         count0.push_back(local);
+        for (int k = g->cons_ptr[t]; k < g->cons_ptr[t + 1]; ++k)
+          if (loc[g->cons_idx[k]] >= 0) tc_idx.push_back(loc[g->cons_idx[k]]);
+        tc_ptr.push_back((int64_t)tc_idx.size());
       }
     }
     start_live[w] = sl;
@@ -342,8 +368,8 @@ extern "C" int rm_greedy_windows(RmGraph* g, int32_t W, const int64_t* win_ptr,
       out_w[opb_dev[w] + i] = out_b[op_base[w] + i];
     }
   Scratch sc(s);
-  int64_t *d_ob, *d_tb, *d_out, *d_inp, *d_sup, *d_tsz, *d_sl, *d_peak, *d_goff;
-  int32_t *d_gop, *d_np, *d_ini, *d_sui, *d_c0, *d_ord, *d_st;
+  int64_t *d_ob, *d_tb, *d_out, *d_inp, *d_sup, *d_tsz, *d_sl, *d_peak, *d_goff, *d_tcp;
+  int32_t *d_gop, *d_np, *d_ini, *d_sui, *d_c0, *d_ord, *d_st, *d_tci;
   unsigned char* d_g = nullptr;
   auto up = [&](auto** d, const auto& v) -> cudaError_t {
     cudaError_t e = sc.alloc(d, v.size());
@@ -365,6 +391,8 @@ extern "C" int rm_greedy_windows(RmGraph* g, int32_t W, const int64_t* win_ptr,
   RM_CUDA(up(&d_sup, succ_ptr_w));
   RM_CUDA(up(&d_sui, succ_idx));
   RM_CUDA(up(&d_c0, count0));
+  RM_CUDA(up(&d_tcp, tc_ptr));
+  RM_CUDA(up(&d_tci, tc_idx));
   RM_CUDA(up(&d_tsz, tsize));
   RM_CUDA(up(&d_sl, start_live));
   RM_CUDA(up(&d_goff, goff));
@@ -372,9 +400,12 @@ extern "C" int rm_greedy_windows(RmGraph* g, int32_t W, const int64_t* win_ptr,
   RM_CUDA(sc.alloc(&d_peak, size_t(W)));
   RM_CUDA(sc.alloc(&d_st, size_t(W)));
   if (gbytes) RM_CUDA(sc.alloc(&d_g, gbytes));
-  K4Args a{W, d_ob, d_nops, d_tb, d_gop, d_out, d_np, d_inp, d_ini, d_sup, d_sui, d_c0, d_tsz, d_sl,
-           d_ord, d_peak, d_st, d_g, d_goff};
-  int rc = launch_k4_t<256>(a, smem, s);
+  K4Args a{W, d_ob, d_nops, d_tb, d_gop, d_out, d_np, d_inp, d_ini, d_sup, d_sui, d_c0, d_tcp, d_tci,
+           d_tsz, d_sl, d_ord, d_peak, d_st, d_g, d_goff};
+  // wide windows: more threads, fewer ops per thread in each step's score scan
+  int64_t max_ops = 0;
+  for (int w = 0; w < W; ++w) max_ops = std::max<int64_t>(max_ops, op_base[w + 1] - op_base[w]);
+  int rc = max_ops > 2048 ? launch_k4_t<1024>(a, smem, s) : launch_k4_t<256>(a, smem, s);
   if (rc) return rc;
   std::vector<int32_t> ord_w(opb_dev[W]), st_dev(W);
   if (opb_dev[W])
