@@ -19,8 +19,8 @@
 // and expands each ideal at most once, so whenever (#ideals - 1) <= node_cap
 // its cap cannot trigger and this IS its answer.  Windows with more ideals
 // than the cap (or more than K5_MAX_N ops) come back with status 3: their
-// answer depends on how far the pruned DFS gets, and the caller runs the
-// reference search for them.
+// answer depends on how far the pruned DFS gets, and the caller runs that
+// search for them (rm_exact_order_search, order_search.cpp).
 //
 // Device: per window, one sweep counts the ideals (a mask is an ideal iff
 // every member's local preds are in it); then V is filled level by level

@@ -143,7 +143,7 @@ def greedy_order(p) -> OrderingSolution:
 
 # ------------------------------------------------------------------ exact
 
-NEEDS_SEARCH = object()   # rm_exact_windows status 3: the reference's DFS decides
+NEEDS_SEARCH = object()   # rm_exact_windows status 3: the capped DFS (search_window) decides
 
 
 def exact_windows(problems: Sequence) -> list:
