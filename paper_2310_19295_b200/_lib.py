@@ -99,6 +99,7 @@ class RmScheduleResult(C.Structure):
                 ("_pad", C.c_int32)]
 
 
+RM_ERR_CAPACITY = -5
 RM_DEVICE_PTRS = 1
 RM_NO_REDUCE = 2
 RM_ORDERS_U16 = 4

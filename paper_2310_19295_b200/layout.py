@@ -237,16 +237,20 @@ def exact_layout(p, search=None) -> MemoryLayout:
         raise ConfigError("time budget must be positive")
     if not p.items:
         return MemoryLayout(offsets={}, capacity=0, stats=LayoutStats(0, 0.0))
-    if search is not None:
-        r = exact_layout_batch([p], search=False)[0]
-        return r if r is not None else search(p)
-    return exact_layout_batch([p])[0]
+    r = exact_layout_batch([p], search=search is None)[0]
+    if r is not None:
+        return r
+    if search is None:
+        raise _lib.RoamError("exact_layout: a component of more than 64 items needs the search; "
+                             "pass search= (e.g. the reference's exact_layout)")
+    return search(p)
 
 
 def exact_layout_batch(problems: Sequence, search: bool = True) -> list[MemoryLayout | None]:
     """K3 component pass over many exact_layout problems in one launch, then
     the branch-and-bound (rm_layout_search) for the problems whose incumbent
-    missed its bound -- or None for them when ``search`` is False."""
+    missed its bound -- None for them when ``search`` is False, or when a
+    component to search has more than 64 items."""
     t0 = time.monotonic()
     out: list[MemoryLayout | None] = [None] * len(problems)
     for bottom in (True, False):
@@ -267,7 +271,7 @@ def exact_layout_batch(problems: Sequence, search: bool = True) -> list[MemoryLa
     return out
 
 
-def _branch_and_bound(p, r: PackResult, t0: float) -> MemoryLayout:
+def _branch_and_bound(p, r: PackResult, t0: float) -> MemoryLayout | None:
     """layout.py:226-290 over K3's incumbent: one rm_layout_search call.  The
     deadline is the reference's (t0 + time_budget on the monotonic clock)."""
     items = p.items
@@ -278,11 +282,13 @@ def _branch_and_bound(p, r: PackResult, t0: float) -> MemoryLayout:
     inc = np.fromiter((r.offsets[i.tensor] for i in items), np.int64, N)
     offset = np.empty(N, np.int64)
     cap, nodes, opt = C.c_int64(0), C.c_int64(0), C.c_int32(0)
-    check(lib().rm_layout_search(N, ptr(tensor), ptr(start), ptr(end), ptr(size), ptr(is_act),
-                                 1 if p.activations_at_bottom else 0, ptr(inc),
-                                 -1 if p.node_cap is None else int(p.node_cap), t0 + p.time_budget,
-                                 ptr(offset), C.byref(cap), C.byref(nodes), C.byref(opt)),
-          "rm_layout_search")
+    st = lib().rm_layout_search(N, ptr(tensor), ptr(start), ptr(end), ptr(size), ptr(is_act),
+                                1 if p.activations_at_bottom else 0, ptr(inc),
+                                -1 if p.node_cap is None else int(p.node_cap), t0 + p.time_budget,
+                                ptr(offset), C.byref(cap), C.byref(nodes), C.byref(opt))
+    if st == _lib.RM_ERR_CAPACITY:
+        return None   # a component of more than 64 items: the caller decides
+    check(st, "rm_layout_search")
     return MemoryLayout(offsets=dict(zip(tensor.tolist(), offset.tolist())), capacity=int(cap.value),
                         activation_block=_act_block(items), optimal=bool(opt.value),
                         stats=LayoutStats(int(nodes.value), time.monotonic() - t0))

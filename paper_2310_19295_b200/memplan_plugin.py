@@ -112,8 +112,8 @@ class _State:
 
 
 # dispatch counters since install(): how the planner's subtasks were served
-STATS = {"windows_k4": 0, "windows_k5": 0, "windows_dfs": 0, "windows_dfs_budget": 0, "leaves_k3_constrained": 0,
-         "leaves_k3_exact": 0, "leaves_search": 0}
+STATS = {"windows_k4": 0, "windows_k5": 0, "windows_dfs": 0, "windows_dfs_budget": 0, "windows_ref_dfs": 0, "leaves_k3_constrained": 0,
+         "leaves_k3_exact": 0, "leaves_search": 0, "leaves_ref_search": 0}
 
 
 def install(mp=None):
@@ -127,6 +127,8 @@ def install(mp=None):
     orig_solve_window = pl._solve_window
     orig_solve_layout = pl._solve_layout
     orig_pool_map = pl._pool_map
+    ref_exact_order = ordm.exact_order
+    ref_exact_layout = lay.exact_layout
 
     def to_layout(m):
         return lay.MemoryLayout(offsets=m.offsets, capacity=m.capacity,
@@ -159,6 +161,12 @@ def install(mp=None):
                 raise r
             if r is _ord.NEEDS_SEARCH:
                 # more order ideals than the node cap: the capped DFS in libroam
+                # (windows of up to 64 ops; wider ones -- node_limit > 64 --
+                # keep the reference's own DFS)
+                if len(p.ops) > 64:
+                    out.append(ref_exact_order(p))
+                    STATS["windows_ref_dfs"] += 1
+                    continue
                 r = _ord.search_window(p)
                 if isinstance(r, GraphError):
                     T(functools.partial(_raise, r))()
@@ -206,6 +214,10 @@ def install(mp=None):
             # others run the branch-and-bound in libroam (rm_layout_search)
             res = _lay.exact_layout_batch([jobs[k][0] for k in small])
             for k, r in zip(small, res):
+                if r is None:   # a component of > 64 items (layout_limit > 64): the reference's search
+                    out[k] = ref_exact_layout(jobs[k][0])
+                    STATS["leaves_ref_search"] += 1
+                    continue
                 out[k] = to_layout(r)
                 STATS["leaves_search" if r.stats.nodes else "leaves_k3_exact"] += 1
         return out

@@ -78,3 +78,23 @@ def test_exact_layout_searches_like_reference():
             (_offs(c["offsets"]), c["capacity"], c["optimal"], c["nodes"]), c
     one = exact_layout(probs[0])
     assert (one.offsets, one.capacity) == (_offs(cases[0]["offsets"]), cases[0]["capacity"])
+
+
+def test_component_above_64_items_is_reported():
+    """The search keeps its masks in 64 bits: a component of 65 overlapping
+    items whose incumbent misses its bound comes back as RM_ERR_CAPACITY
+    (the planner plug-in then hands the leaf to the reference's search)."""
+    lib = _lib.lib()
+    n = 65
+    tensor = np.arange(n, dtype=np.int32)
+    start = np.zeros(n, np.int32)
+    end = np.ones(n, np.int32)
+    size = np.ones(n, np.int64)
+    act = np.zeros(n, np.uint8)
+    inc = np.arange(n, dtype=np.int64) * 2          # incumbent 2n - 1 > bound n
+    off = np.empty(n, np.int64)
+    cap, nodes, opt = C.c_int64(0), C.c_int64(0), C.c_int32(0)
+    st = lib.rm_layout_search(n, _lib.ptr(tensor), _lib.ptr(start), _lib.ptr(end), _lib.ptr(size),
+                              _lib.ptr(act), 0, _lib.ptr(inc), -1, 0.0, _lib.ptr(off),
+                              C.byref(cap), C.byref(nodes), C.byref(opt))
+    assert st == _lib.RM_ERR_CAPACITY
