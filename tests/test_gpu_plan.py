@@ -80,3 +80,33 @@ def test_cli_plan_and_eval_through_plugin(tmp_path):
         assert main(["eval", "--graph", str(gpath), "--plan", str(out)]) == 0
     finally:
         plug.uninstall()
+
+
+@needs_ref
+def test_capped_searches_match_live_reference():
+    """Node caps tight enough that the planner's windows and leaves reach the
+    capped searches (exact_order's DFS where K5 hands a window back,
+    exact_layout's branch-and-bound where K3's incumbent misses its bound):
+    the libroam restatements stop where the reference stops, so the plan
+    documents -- optimal_leaves included -- stay byte-identical."""
+    import memplan.graphgen as rgen
+    runs = {"windows_dfs": 0, "windows_dfs_budget": 0, "leaves_search": 0}
+    for cfgkw in (dict(order_node_cap=3, layout_node_cap=5), dict(order_node_cap=40),
+                  dict(node_limit=14, order_node_cap=400, layout_limit=16, layout_node_cap=60),
+                  dict(node_limit=6, order_node_cap=2000, layout_node_cap=100_000)):
+        cfg = mp.planner.PlannerConfig(**cfgkw)
+        for arch, blocks in (("transformer_block", 2), ("mlp", 3), ("residual", 3)):
+            g = rgen.gen_training_graph(arch, blocks, optimizer="adam")
+            want = mp.planner.plan_doc_bytes(mp.planner.plan(g, cfg))
+            plug.install(mp)
+            try:
+                got = mp.planner.plan_doc_bytes(mp.planner.plan(g, cfg))
+                for k in runs:
+                    runs[k] += plug.STATS[k]
+            finally:
+                plug.uninstall()
+            assert got == want, (arch, cfgkw)
+    # real plans reach the window DFS; their small leaves meet the layout bound
+    # (SURVEY probe p12), so the branch-and-bound is pinned by
+    # test_layout_search.py instead
+    assert runs["windows_dfs"] + runs["windows_dfs_budget"] > 0, runs
