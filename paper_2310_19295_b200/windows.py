@@ -11,8 +11,11 @@ the reference's per-tensor rule for window w at slot p reduces to
     live_in(w)  = { t : b < p <= L }
     live_out(w) = { t : b <= p <  L }
 
-(b == p exactly when the producer is inside w).  Each window is one vectorised
-pass over the tensors' (b, L) arrays.  Host code: the output is the reference's
+(b == p exactly when the producer is inside w).  The windows are swept once in
+slot order: between consecutive slots only the tensors born or dying in
+between change membership (found by binary search in the (b, L)-sorted
+tensor lists), so each window's sets are its predecessor's plus/minus a few
+ids.  Host code: the output is the reference's
 frozensets.  Equality with the reference is tested on every window the planner
 builds (tests/test_plugin_host.py).
 """
@@ -85,14 +88,66 @@ def build_window_problems(g, lin, wu_plan=None, ops_per_step: int = 1, time_budg
     """ordering.py:470-542 with the reference's own Window / OrderingProblem
     types passed in; same list, same order, same sets."""
     final_ops, slot_of_window, b, L, _ = window_intervals(g, lin, wu_plan)
+    wins = list(lin.windows)
+    slots = [slot_of_window[w.index] for w in wins]
+    sets = _sweep_live_sets(b, L, sorted(set(slots)))
     out = []
-    for w in lin.windows:
-        p = slot_of_window[w.index]
-        live_in = ((b < p) & (p <= L)).nonzero()[0]
-        live_out = ((b <= p) & (p < L)).nonzero()[0]
+    for w, p in zip(wins, slots):
+        live_in, live_out = sets[p]
         ops = final_ops[w.index]
         out.append((window_type(index=w.index, leaf=w.leaf, ops=ops),
-                    problem_type(graph=g, ops=ops, live_in=live_set(live_in),
-                                 live_out=live_set(live_out), ops_per_step=ops_per_step,
-                                 time_budget=time_budget, node_cap=node_cap)))
+                    problem_type(graph=g, ops=ops, live_in=live_in, live_out=live_out,
+                                 ops_per_step=ops_per_step, time_budget=time_budget,
+                                 node_cap=node_cap)))
+    return out
+
+
+def _sweep_live_sets(b: np.ndarray, L: np.ndarray, slots: list[int]) -> dict:
+    """{slot p: (live_in(p), live_out(p))} for ascending slots, swept once:
+    between consecutive slots only the tensors born or dying in between
+    change membership, so each set is the previous one minus/plus a few ids
+    (set algebra on the previous frozenset, no per-id Python objects), and
+    its id array comes from an updated membership mask.
+      live_in(p)  = {t : b < p <= L}     live_out(p) = {t : b <= p < L}"""
+    T = len(b)
+    ob = np.argsort(b, kind="stable")
+    oL = np.argsort(L, kind="stable")
+    bs, Ls = b[ob], L[oL]
+    S = np.asarray(slots, np.int64)
+    Ll, Lr = Ls.searchsorted(S, "left").tolist(), Ls.searchsorted(S, "right").tolist()
+    bl, br = bs.searchsorted(S, "left").tolist(), bs.searchsorted(S, "right").tolist()
+    m_in = np.zeros(T, bool)
+    m_out = np.zeros(T, bool)
+    s_in, s_out = frozenset(), frozenset()
+    out = {}
+    prev = None
+    for k, p in enumerate(slots):
+        if prev is None:
+            add_in = ((b < p) & (p <= L)).nonzero()[0]
+            add_out = ((b <= p) & (p < L)).nonzero()[0]
+            rem_in = rem_out = add_in[:0]
+        else:
+            # live_in: leave when L < p (L in [prev, p)); join when b in [prev, p) and L >= p
+            c = oL[Ll[k - 1]:Ll[k]]
+            rem_in = c[m_in[c]]
+            c = ob[bl[k - 1]:bl[k]]
+            add_in = c[L[c] >= p]
+            # live_out: leave when L <= p (L in (prev, p]); join when b in (prev, p] and L > p
+            c = oL[Lr[k - 1]:Lr[k]]
+            rem_out = c[m_out[c]]
+            c = ob[br[k - 1]:br[k]]
+            add_out = c[L[c] > p]
+        m_in[rem_in] = False
+        m_in[add_in] = True
+        m_out[rem_out] = False
+        m_out[add_out] = True
+        if len(rem_in) or len(add_in):
+            s_in = s_in.difference(rem_in.tolist()).union(add_in.tolist())
+        if len(rem_out) or len(add_out):
+            s_out = s_out.difference(rem_out.tolist()).union(add_out.tolist())
+        li, lo = LiveSet(s_in), LiveSet(s_out)
+        li.arr = m_in.nonzero()[0].astype(np.int32)
+        lo.arr = m_out.nonzero()[0].astype(np.int32)
+        out[p] = (li, lo)
+        prev = p
     return out
