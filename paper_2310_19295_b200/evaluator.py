@@ -22,7 +22,7 @@ from typing import Iterable
 import numpy as np
 
 from . import _lib
-from ._lib import RoamError, check, lib, ptr
+from ._lib import check, lib, ptr
 from .graph import ConfigError, Schedule, ScheduleError, graph_arrays, graph_cache
 
 
