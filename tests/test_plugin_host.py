@@ -242,3 +242,28 @@ def test_subgraph_tree_dropin_matches_reference():
             fn(inference, 20)
         with pytest.raises(mp.graph.ConfigError, match="node_limit"):
             fn(graphs[0], 1)
+
+
+def test_live_set_sweep_matches_interval_rule():
+    """windows._sweep_live_sets against the interval rule it sweeps, on random
+    (birth, last-use) intervals and slot sets, including empty sets, shared
+    endpoints and tensors that never enter."""
+    import random
+
+    import numpy as np
+
+    from paper_2310_19295_b200.windows import _sweep_live_sets
+    rng = random.Random(5)
+    for trial in range(200):
+        T = rng.randint(0, 40)
+        H = rng.randint(1, 30)
+        b = np.array([rng.randint(0, H) for _ in range(T)], np.int64)
+        L = np.array([min(H, bb + rng.randint(0, H)) for bb in b], np.int64)
+        slots = sorted(rng.sample(range(H + 1), rng.randint(1, H + 1)))
+        got = _sweep_live_sets(b, L, slots)
+        for p in slots:
+            want_in = {t for t in range(T) if b[t] < p <= L[t]}
+            want_out = {t for t in range(T) if b[t] <= p < L[t]}
+            li, lo = got[p]
+            assert set(li) == want_in and set(lo) == want_out
+            assert set(li.arr.tolist()) == want_in and set(lo.arr.tolist()) == want_out
