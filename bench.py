@@ -134,6 +134,61 @@ def graph_for(config: str):
     return load_graph(gg.config_doc(config))
 
 
+_REF_GRAPH = None
+
+
+def _ref_init(config: str) -> None:
+    """Pool initializer: the reference planner's own graph object (memplan
+    from baseline/_ref), built once per worker process."""
+    global _REF_GRAPH
+    from paper_2310_19295_b200 import graphgen as gg
+    from paper_2310_19295_b200 import memplan_plugin as plug
+    mp = plug.load_memplan()
+    _REF_GRAPH = (mp, mp.graph.load_graph(gg.config_doc(config)))
+
+
+def _ref_peak(row) -> tuple[int, int]:
+    """The reference's own peak_memory(g, sequential_schedule(g, order))
+    (graph.py:401-468), unmodified."""
+    mp, g = _REF_GRAPH
+    return mp.graph.peak_memory(g, mp.graph.sequential_schedule(g, [int(v) for v in row]))
+
+
+def reference_python(config: str, rows, gpu_peak, gpu_arg, seconds: float) -> dict | None:
+    """The reference implementation itself (pure Python, baseline/_ref) on all
+    host cores over a small sample of the bench's candidates: its rate, and
+    bit-exact parity of the GPU results with it on that sample.  Spawned
+    worker processes (the parent holds a CUDA context) that only run the
+    reference; any failure (no reference installed, a worker dying) skips the
+    leg instead of stalling the bench."""
+    from concurrent.futures import ProcessPoolExecutor
+    import multiprocessing as mpr
+    try:
+        from paper_2310_19295_b200 import memplan_plugin as plug
+        plug.load_memplan()
+        cores = os.cpu_count() or 1
+        S = min(len(rows), 4 * cores)
+        sample = [list(map(int, r)) for r in rows[:S]]
+        with ProcessPoolExecutor(cores, mp_context=mpr.get_context("spawn"), initializer=_ref_init,
+                                 initargs=(config,)) as ex:
+            got = list(ex.map(_ref_peak, sample, timeout=120))      # warm-up + parity sample
+            parity = all((int(gpu_peak[i]), int(gpu_arg[i])) == tuple(got[i]) for i in range(S))
+            done, t0 = 0, time.perf_counter()
+            while True:
+                list(ex.map(_ref_peak, sample, timeout=120))
+                done += S
+                if time.perf_counter() - t0 >= seconds:
+                    break
+            wall = time.perf_counter() - t0
+    except Exception as e:  # the leg is informational: report why it is missing
+        print(f"reference_python leg skipped: {type(e).__name__}: {e}", file=sys.stderr)
+        return None
+    return {"value": done / wall, "unit": UNIT, "cores": cores,
+            "sample": f"first {S} of this run's candidates, repeated for >= {seconds:g} s; the reference's "
+                      f"own peak_memory(g, sequential_schedule(g, o)) (memplan, pure Python) in {cores} "
+                      f"processes; bit-exact parity of the GPU results with it: {parity}"}
+
+
 def ncu_traffic(config: str, batch: int):
     """dram bytes/launch of K1 from a committed ncu --set full summary."""
     p = ROOT / "profiles" / "k1_ncu_summary.json"
@@ -478,6 +533,9 @@ def main() -> None:
         }
         if cpu is not None:
             line["cpu_baseline"] = cpu
+            pyref = reference_python(args.config, host_np, hp, ha, min(args.cpu_seconds, 3.0))
+            if pyref is not None:
+                line["reference_python"] = pyref
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
