@@ -166,7 +166,7 @@ def reference_python(config: str, rows, gpu_peak, gpu_arg, seconds: float) -> di
     try:
         from paper_2310_19295_b200 import memplan_plugin as plug
         plug.load_memplan()
-        cores = os.cpu_count() or 1
+        cores = min(os.cpu_count() or 1, 32)   # bounded spawn cost on very wide hosts
         S = min(len(rows), 4 * cores)
         sample = [list(map(int, r)) for r in rows[:S]]
         with ProcessPoolExecutor(cores, mp_context=mpr.get_context("spawn"), initializer=_ref_init,
