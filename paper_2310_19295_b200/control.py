@@ -300,7 +300,7 @@ def subgraph_tree_factory(mp):
             if sorted_used:
                 umask[np.asarray(sorted_used, np.int64)] = True
             rank = np.bitwise_count(anc[unc] & np.packbits(umask, bitorder="little")).sum(axis=1)
-            for r in np.unique(rank).tolist():
+            for r in sorted(set(rank.tolist())):
                 lo = sorted_used[r - 1] if r > 0 else None
                 hi = sorted_used[r] if r < len(sorted_used) else None
                 residuals.append(build.new_node(kind="independent", outer_fwd=lo, outer_bwd=hi,
