@@ -154,3 +154,23 @@ def test_kahn_candidates_are_topological():
         O.validate_schedule(g, o, O.sequential_timesteps(len(g.ops), o))
         seen.add(tuple(o))
     assert len(seen) == 4
+
+
+def test_bench_reference_arm_contract():
+    """`bench.py --impl reference` (the driver's reference arm) runs on the host
+    alone and prints the contract's JSON line: impl, the metric of our arm,
+    a cpu_baseline describing the run and an e2e object with zero copies."""
+    import json
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--steps", "3",
+                        "--warmup", "1"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["metric"] == "candidate plans evaluated/sec"
+    assert line["unit"] == "candidates/s" and line["higher_is_better"] is True
+    assert line["steps"] == 3 and line["warmup"] == 1 and line["value"] > 0
+    cb = line["cpu_baseline"]
+    assert cb["kind"] in ("port", "reference") and cb["cores"] >= 1 and cb["value"] == line["value"]
+    assert line["e2e"] == {"value": line["value"], "unit": line["unit"], "h2d_bytes_per_step": 0,
+                           "d2h_bytes_per_step": 0}
