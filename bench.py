@@ -508,7 +508,7 @@ def main() -> None:
                             else f" + {args.dist_backend} all_gather of (peak, id)") if world > 1 else ""),
                        "generation_ms": gen_ms},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": traffic,
+                         "frac": achieved / hbm, "frac_of_8tbs_nominal": achieved / 8000.0, "traffic": traffic,
                          "kernel": {4: "k1v4_eval_orders", 3: "k1v3_eval_orders",
                                     2: "k1v2_eval_orders"}.get(info["k1_variant"],
                                                                                     "k1_eval_orders"),
