@@ -325,10 +325,22 @@ __global__ void __launch_bounds__(NT) k3_llfb(const K3Args a) {
         ren[PK ? 0 : m] = a1;
       }
     }
+    // the next item's record is fetched one placement ahead (the working set
+    // of a large leaf lives in global scratch: its loads are the critical path)
+    int i_nx = A < N ? ord[A] : 0;
+    int si_nx = A < N ? st[i_nx] : 0, ei_nx = A < N ? en[i_nx] : 0;
+    long long sz_nx = A < N ? sz[i_nx] : 0, fl_nx = A < N ? flo[i_nx] : 0;
     for (int k = A; k < N; ++k) {
-      const int i = ord[k];
-      const int si = st[i], ei = en[i];
-      const long long szi = sz[i], fl = flo[i];
+      const int i = i_nx;
+      const int si = si_nx, ei = ei_nx;
+      const long long szi = sz_nx, fl = fl_nx;
+      if (k + 1 < N) {
+        i_nx = ord[k + 1];
+        si_nx = st[i_nx];
+        ei_nx = en[i_nx];
+        sz_nx = sz[i_nx];
+        fl_nx = flo[i_nx];
+      }
       const int buf = k & 1;
       if (lane == 31) {
         s_plo[buf][w] = rlo[MAXC - 1];
