@@ -97,6 +97,7 @@ __device__ __forceinline__ unsigned v4_bar_or(int id, unsigned p) {
 template <typename RowT, int NT, int C, bool CLS = false>
 __global__ void __launch_bounds__((v4_cta_cap(C) / NT) * NT, 1) k1v4_eval_orders(const K1V4Args a) {
   extern __shared__ __align__(16) unsigned char smem[];
+  asm volatile("griddepcontrol.launch_dependents;");  // the next launch may start its prologue
   constexpr int SL = NT * C;
   constexpr int Q = SL / 8;                 // 8-id chunks
   constexpr int QR = (Q + NT - 1) / NT;     // chunk rounds per thread
@@ -172,6 +173,11 @@ __global__ void __launch_bounds__((v4_cta_cap(C) / NT) * NT, 1) k1v4_eval_orders
   }
   for (int i = tid; i < (SL + 8) / 2; i += NT) reinterpret_cast<uint32_t*>(pos)[i] = 0x80008000u;
   v4_bar<NT>(bar_id);
+  // programmatic dependent launch: everything above reads only the graph's
+  // read-only metadata, so it may overlap the previous launch's tail; rows,
+  // outputs and the selection counter are touched only after that launch has
+  // completed (a no-op for a normal launch)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   uint32_t v[C];
   auto load_row = [&](int64_t cc) {
@@ -406,7 +412,17 @@ static int launch_k1v4_t(K1V4Args& a, int grid, size_t smem, cudaStream_t s) {
     cudaEventCreate(&e1);
     cudaEventRecord(e0, s);
   }
-  kern<<<grid, NT * a.G, smem, s>>>(a);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NT * a.G);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  RM_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
   RM_LAUNCH_CHECK("k1v4_eval_orders launch");
   if (g_timing) {
     cudaEventRecord(e1, s);
