@@ -17,8 +17,10 @@ Kahn orders (seed 0, ids rank*B ...), generated on device before timing
 (generation timed separately).  Three copies of the batch rotate between
 steps (inputs larger than L2, no flush needed); the K steps are one CUDA-event
 interval on the launching stream, from after the barrier to after the last
-exchange, max over ranks; K1's own launches are timed per step for the
-roofline.
+exchange, max over ranks; the K1 launches run back to back (programmatic
+dependent launch overlaps each launch's metadata staging with the previous
+one's tail) and their average, the stream's interval up to the last K1 / K,
+feeds the roofline.
 """
 
 from __future__ import annotations
