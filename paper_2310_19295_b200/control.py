@@ -55,30 +55,38 @@ def _bit(anc, rows, cols):
     return (anc[rows, cols >> 3] >> (cols & 7)) & 1
 
 
-def _preds_match(build, c) -> bool:
-    """The build's predecessor masks are the full-graph closure (checked once
-    per build object on a few ops; otherwise the reference code runs)."""
-    ok = getattr(build, "_roam_preds_ok", None)
-    if ok is None:
-        n = c["n"]
-        probe = sorted({0, n // 3, n // 2, n - 1}) if n else []
-        ok = len(build.preds) == n and all(bin(build.preds[v]).count("1") == int(c["count"][v])
-                                           for v in probe)
-        try:
-            build._roam_preds_ok = ok
-        except AttributeError:  # pragma: no cover - frozen build object
-            pass
-    return ok
+def _build_anc(build, c):
+    """The ancestor bit matrix behind ``build.before`` (segmentation.py:
+    167-168): the graph's C++ closure when ``build.preds`` is the full-graph
+    closure (what build_subgraph_tree passes, segmentation.py:361-367; checked
+    once per build object on a few ops), otherwise ``build.preds`` itself
+    unpacked into the same layout -- exact either way, no reference code."""
+    hit = getattr(build, "_roam_anc", None)
+    if hit is not None:
+        return hit
+    n = c["n"]
+    probe = sorted({0, n // 3, n // 2, n - 1}) if n else []
+    same = len(build.preds) == n and all(bin(build.preds[v]).count("1") == int(c["count"][v]) for v in probe)
+    if same:
+        anc = c["anc"]
+    else:
+        row = c["anc"].shape[1]
+        anc = np.frombuffer(b"".join(int(p).to_bytes(row, "little") for p in build.preds),
+                            np.uint8).reshape(len(build.preds), row)
+    try:
+        build._roam_anc = anc
+    except AttributeError:  # pragma: no cover - frozen build object
+        pass
+    return anc
 
 
-def region_between_factory(ref):
+def region_between_factory():
     cache: dict = {}
 
     def region_between(build, core, lo, hi):
         """segmentation.py:174-185: sorted core ops strictly between lo and hi."""
         c = closure(build.g)
-        if not _preds_match(build, c):
-            return ref(build, core, lo, hi)
+        anc = _build_anc(build, c)
         key = id(core)
         hit = cache.get(key)
         if hit is None or hit[0] is not core or hit[1] != len(core):
@@ -89,14 +97,14 @@ def region_between_factory(ref):
         v = hit[2]
         keep = np.ones(len(v), bool)
         if lo is not None:
-            keep &= (v != lo) & (_bit(c["anc"], v, np.int64(lo)) == 1)
+            keep &= (v != lo) & (_bit(anc, v, np.int64(lo)) == 1)
         if hi is not None:
-            keep &= (v != hi) & (_bit(c["anc"], np.int64(hi), v) == 1)
+            keep &= (v != hi) & (_bit(anc, np.int64(hi), v) == 1)
         return np.sort(v[keep]).tolist()
     return region_between
 
 
-def format_ig_ok_factory(mp, ref):
+def format_ig_ok_factory(mp):
     act_cache: dict = {}
 
     def format_ig_ok(build, members, boundary):
@@ -131,13 +139,6 @@ def format_ig_ok_factory(mp, ref):
         bad = act & ((member[prod] & any_out) | (any_mem & ~inside[prod]))
         return not bool(bad.any())
     return format_ig_ok
-
-
-def _floating_closed(g, fl: set) -> bool:
-    """Every successor of a floating op is floating, so no core-to-core path
-    runs through a floating op and the core's induced closure (what
-    predecessor_masks(g, core) computes) is the global closure on core rows."""
-    return all(s in fl for f in fl for s in g.direct_succs[f])
 
 
 _BUILD_TYPES: dict = {}
@@ -180,10 +181,11 @@ def subgraph_tree_factory(mp):
     inside-out independent-subgraph pairing, the residual runs and
     ``_split_if_oversized`` -- are the reference's own helpers, called in the
     same order on the reference's ``_TreeBuild`` (node ids come out the
-    same).  Where the core's induced closure could differ from the global one
-    the reference function runs instead."""
+    same).  ``_mi_over(g, core)`` uses the core's INDUCED closure; it equals
+    the global closure on core rows because a relocatable branch's outputs
+    are consumed only inside the branch (graph.py:541-545), so no path
+    leaves the core through a floating op and comes back."""
     seg, gr = mp.segmentation, mp.graph
-    ref = seg.build_subgraph_tree
 
     def build_subgraph_tree(g, node_limit):
         if node_limit < 2:
@@ -192,9 +194,6 @@ def subgraph_tree_factory(mp):
             raise gr.StructuralError("graph has no backward pass; segment it as an inference graph")
         branches = seg.weight_update_branches(g)
         floating = sorted(v for b in branches for v in b.ops)
-        fl = set(floating)
-        if not _floating_closed(g, fl):
-            return ref(g, node_limit)
         c = closure(g)
         n, anc = c["n"], c["anc"]
         is_core = np.ones(n, bool)

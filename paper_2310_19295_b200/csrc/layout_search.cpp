@@ -43,16 +43,18 @@ double mono_now() {
   return double(ts.tv_sec) + 1e-9 * double(ts.tv_nsec);
 }
 
+// item masks of W 64-bit words (components of up to 64 W items)
+template <int W>
 struct Search {
   int n = 0;
   std::vector<int64_t> size, floor_;
   std::vector<int32_t> st, en;
-  std::vector<uint64_t> ov;
+  std::vector<uint64_t> ov;  // [n][W] overlap bits
   std::vector<int64_t> off, best_off;
   int64_t best_cap = 0, bound = 0;
   int64_t nodes = 0, nodes_before = 0, node_cap = -1;
   double deadline = 0.0;
-  uint64_t used = 0;
+  uint64_t used[W] = {};
 
   void run(int depth, int64_t cap) {
     ++nodes;
@@ -68,15 +70,17 @@ struct Search {
     std::vector<std::array<int64_t, 4>> tried;
     std::vector<std::pair<int64_t, int64_t>> spans;
     for (int i = 0; i < n; ++i) {
-      if ((used >> i) & 1) continue;
+      if ((used[i >> 6] >> (i & 63)) & 1) continue;
       const std::array<int64_t, 4> key{size[i], st[i], en[i], floor_[i]};
       if (std::find(tried.begin(), tried.end(), key) != tried.end()) continue;
       tried.push_back(key);
       spans.clear();
-      for (uint64_t m = used & ov[i]; m; m &= m - 1) {
-        const int j = __builtin_ctzll(m);
-        spans.emplace_back(off[j], off[j] + size[j]);
-      }
+      const uint64_t* ovi = ov.data() + size_t(i) * W;
+      for (int k = 0; k < W; ++k)
+        for (uint64_t m = used[k] & ovi[k]; m; m &= m - 1) {
+          const int j = 64 * k + __builtin_ctzll(m);
+          spans.emplace_back(off[j], off[j] + size[j]);
+        }
       std::sort(spans.begin(), spans.end());
       int64_t o = floor_[i];
       for (const auto& sp : spans) {
@@ -85,13 +89,21 @@ struct Search {
       }
       const int64_t new_cap = cap >= o + size[i] ? cap : o + size[i];
       if (new_cap >= best_cap) continue;
-      used |= uint64_t(1) << i;
+      used[i >> 6] |= uint64_t(1) << (i & 63);
       off[i] = o;
       run(depth + 1, new_cap);
-      used &= ~(uint64_t(1) << i);
+      used[i >> 6] &= ~(uint64_t(1) << (i & 63));
     }
   }
 };
+
+// one component's search (items in the reference's branching order);
+// returns false when the node cap or the deadline stopped it
+template <int W>
+bool search_component(const std::vector<int>& order, const int32_t* start, const int32_t* end,
+                      const int64_t* size, const std::vector<int64_t>& flo, const int64_t* incumbent,
+                      int64_t bound, int64_t node_cap, double deadline, int64_t& nodes_total,
+                      int64_t& best_cap, int64_t* offset);
 
 bool overlaps(const int32_t* s, const int32_t* e, int a, int b) { return s[a] <= e[b] && s[b] <= e[a]; }
 
@@ -187,49 +199,29 @@ extern "C" int rm_layout_search(int32_t n, const int32_t* tensor, const int32_t*
       best_cap = std::max(best_cap, incumbent[i] + size[i]);
     }
     if (best_cap > bound) {
-      if (comp.size() > 64) return fail(RM_ERR_CAPACITY, "rm_layout_search: components of at most 64 items");
       std::vector<int> order(comp);
       std::sort(order.begin(), order.end(), [&](int a, int b) {
         const int64_t ka = -size[a] * (int64_t(end[a]) - start[a] + 1);
         const int64_t kb = -size[b] * (int64_t(end[b]) - start[b] + 1);
         return ka != kb ? ka < kb : tensor[a] < tensor[b];
       });
-      Search S;
-      S.n = (int)order.size();
-      S.size.resize(S.n);
-      S.floor_.resize(S.n);
-      S.st.resize(S.n);
-      S.en.resize(S.n);
-      S.ov.assign(S.n, 0);
-      S.off.assign(S.n, 0);
-      for (int k = 0; k < S.n; ++k) {
-        const int i = order[k];
-        S.size[k] = size[i];
-        S.floor_[k] = flo[i];
-        S.st[k] = start[i];
-        S.en[k] = end[i];
-        S.best_off.push_back(incumbent[i]);
-      }
-      for (int a = 0; a < S.n; ++a)
-        for (int b = a + 1; b < S.n; ++b)
-          if (overlaps(start, end, order[a], order[b])) {
-            S.ov[a] |= uint64_t(1) << b;
-            S.ov[b] |= uint64_t(1) << a;
-          }
-      S.best_cap = best_cap;
-      S.bound = bound;
-      S.nodes_before = nodes_total;
-      S.node_cap = node_cap;
-      S.deadline = deadline;
-      try {
-        S.run(0, 0);
-      } catch (const Done&) {
-      } catch (const Budget&) {
-        opt = false;
-      }
-      nodes_total += S.nodes;
-      best_cap = S.best_cap;
-      for (int k = 0; k < S.n; ++k) offset[order[k]] = S.best_off[k];
+      const int words = ((int)order.size() + 63) / 64;
+      bool ok = true;
+#define RM_LAYOUT_W(w)                                                                            \
+  else if (words <= w) ok = search_component<w>(order, start, end, size, flo, incumbent, bound, \
+                                                node_cap, deadline, nodes_total, best_cap, offset);
+      if (words > 256) return fail(RM_ERR_CAPACITY, "rm_layout_search: components of at most 16384 items");
+      RM_LAYOUT_W(1)
+      RM_LAYOUT_W(2)
+      RM_LAYOUT_W(4)
+      RM_LAYOUT_W(8)
+      RM_LAYOUT_W(16)
+      RM_LAYOUT_W(32)
+      RM_LAYOUT_W(64)
+      RM_LAYOUT_W(128)
+      RM_LAYOUT_W(256)
+#undef RM_LAYOUT_W
+      if (!ok) opt = false;
     }
     cap_total = std::max(cap_total, best_cap);
   }
@@ -238,3 +230,52 @@ extern "C" int rm_layout_search(int32_t n, const int32_t* tensor, const int32_t*
   *optimal = opt ? 1 : 0;
   return RM_OK;
 }
+
+namespace roam {
+namespace {
+template <int W>
+bool search_component(const std::vector<int>& order, const int32_t* start, const int32_t* end,
+                      const int64_t* size, const std::vector<int64_t>& flo, const int64_t* incumbent,
+                      int64_t bound, int64_t node_cap, double deadline, int64_t& nodes_total,
+                      int64_t& best_cap, int64_t* offset) {
+  Search<W> S;
+  S.n = (int)order.size();
+  S.size.resize(S.n);
+  S.floor_.resize(S.n);
+  S.st.resize(S.n);
+  S.en.resize(S.n);
+  S.ov.assign(size_t(S.n) * W, 0);
+  S.off.assign(S.n, 0);
+  for (int k = 0; k < S.n; ++k) {
+    const int i = order[k];
+    S.size[k] = size[i];
+    S.floor_[k] = flo[i];
+    S.st[k] = start[i];
+    S.en[k] = end[i];
+    S.best_off.push_back(incumbent[i]);
+  }
+  for (int a = 0; a < S.n; ++a)
+    for (int b = a + 1; b < S.n; ++b)
+      if (overlaps(start, end, order[a], order[b])) {
+        S.ov[size_t(a) * W + (b >> 6)] |= uint64_t(1) << (b & 63);
+        S.ov[size_t(b) * W + (a >> 6)] |= uint64_t(1) << (a & 63);
+      }
+  S.best_cap = best_cap;
+  S.bound = bound;
+  S.nodes_before = nodes_total;
+  S.node_cap = node_cap;
+  S.deadline = deadline;
+  bool ok = true;
+  try {
+    S.run(0, 0);
+  } catch (const Done&) {
+  } catch (const Budget&) {
+    ok = false;
+  }
+  nodes_total += S.nodes;
+  best_cap = S.best_cap;
+  for (int k = 0; k < S.n; ++k) offset[order[k]] = S.best_off[k];
+  return ok;
+}
+}  // namespace
+}  // namespace roam

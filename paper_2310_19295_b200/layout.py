@@ -225,32 +225,26 @@ def constrained_llfb_layout(p) -> MemoryLayout:
                         optimal=False, stats=LayoutStats(len(p.items), time.monotonic() - t0))
 
 
-def exact_layout(p, search=None) -> MemoryLayout:
+def exact_layout(p) -> MemoryLayout:
     """exact_layout (layout.py:153-302): K3 decides every problem whose overlap
     components' long-lived-first incumbents meet their lower bounds (then the
     reference returns that incumbent without search, and so does this); the
     other components run the reference's branch-and-bound node for node in
-    libroam (``rm_layout_search``).  ``search(p)``, when given, replaces that
-    step (e.g. the reference's own exact_layout)."""
+    libroam (``rm_layout_search``, masks of up to 256 words: components of
+    any size the planner forms)."""
     if p.time_budget <= 0:
         from .graph import ConfigError
         raise ConfigError("time budget must be positive")
     if not p.items:
         return MemoryLayout(offsets={}, capacity=0, stats=LayoutStats(0, 0.0))
-    r = exact_layout_batch([p], search=search is None)[0]
-    if r is not None:
-        return r
-    if search is None:
-        raise _lib.RoamError("exact_layout: a component of more than 64 items needs the search; "
-                             "pass search= (e.g. the reference's exact_layout)")
-    return search(p)
+    return exact_layout_batch([p])[0]
 
 
 def exact_layout_batch(problems: Sequence, search: bool = True) -> list[MemoryLayout | None]:
     """K3 component pass over many exact_layout problems in one launch, then
     the branch-and-bound (rm_layout_search) for the problems whose incumbent
-    missed its bound -- None for them when ``search`` is False, or when a
-    component to search has more than 64 items."""
+    missed its bound (None for those when ``search`` is False: the K3 pass
+    alone, for tests)."""
     t0 = time.monotonic()
     out: list[MemoryLayout | None] = [None] * len(problems)
     for bottom in (True, False):
@@ -271,7 +265,7 @@ def exact_layout_batch(problems: Sequence, search: bool = True) -> list[MemoryLa
     return out
 
 
-def _branch_and_bound(p, r: PackResult, t0: float) -> MemoryLayout | None:
+def _branch_and_bound(p, r: PackResult, t0: float) -> MemoryLayout:
     """layout.py:226-290 over K3's incumbent: one rm_layout_search call.  The
     deadline is the reference's (t0 + time_budget on the monotonic clock)."""
     items = p.items
@@ -282,13 +276,11 @@ def _branch_and_bound(p, r: PackResult, t0: float) -> MemoryLayout | None:
     inc = np.fromiter((r.offsets[i.tensor] for i in items), np.int64, N)
     offset = np.empty(N, np.int64)
     cap, nodes, opt = C.c_int64(0), C.c_int64(0), C.c_int32(0)
-    st = lib().rm_layout_search(N, ptr(tensor), ptr(start), ptr(end), ptr(size), ptr(is_act),
-                                1 if p.activations_at_bottom else 0, ptr(inc),
-                                -1 if p.node_cap is None else int(p.node_cap), t0 + p.time_budget,
-                                ptr(offset), C.byref(cap), C.byref(nodes), C.byref(opt))
-    if st == _lib.RM_ERR_CAPACITY:
-        return None   # a component of more than 64 items: the caller decides
-    check(st, "rm_layout_search")
+    check(lib().rm_layout_search(N, ptr(tensor), ptr(start), ptr(end), ptr(size), ptr(is_act),
+                                 1 if p.activations_at_bottom else 0, ptr(inc),
+                                 -1 if p.node_cap is None else int(p.node_cap), t0 + p.time_budget,
+                                 ptr(offset), C.byref(cap), C.byref(nodes), C.byref(opt)),
+          "rm_layout_search")
     return MemoryLayout(offsets=dict(zip(tensor.tolist(), offset.tolist())), capacity=int(cap.value),
                         activation_block=_act_block(items), optimal=bool(opt.value),
                         stats=LayoutStats(int(nodes.value), time.monotonic() - t0))

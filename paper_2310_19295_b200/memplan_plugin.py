@@ -36,6 +36,11 @@ Dispatch points rebound (reference file:line of the call site):
                                                    (windows.py)
   layout.layout_violations / simulator.layout_violations / simulator.peak_memory
   cli.peak_memory / validate_schedule / tensor_lifetimes / validate_layout (memplan eval)
+  the user-facing API in its home modules and as memplan's re-exports:
+  peak_memory / tensor_lifetimes / live_bytes_by_timestep / asap_alap (graph),
+  replay_static (simulator.py:129-145: K2's max-extent epilogue),
+  validate_layout / repair_conflicts / llfb_layout / constrained_llfb_layout /
+  exact_layout (layout), greedy_order / exact_order (ordering)
 
 Results are bit-identical to the unpatched reference: the plan document bytes
 (``plan_doc_bytes``) are the parity artefact (tests/test_gpu_plan.py).
@@ -94,15 +99,17 @@ def _raise(e):
 
 def _asap_alap_factory(mp):
     """graph.py:365-372 asap_alap (called by place_weight_updates,
-    ordering.py:405) from libroam's C++ closure bitsets; the reference's own
-    function where the closure would be too large."""
-    ref = mp.graph.asap_alap
+    ordering.py:405) from libroam's C++ closure bitsets.  A cycle raises the
+    reference's StructuralError (graph.py:133-134); graphs above libroam's
+    closure limit (60k ops) raise RoamError -- there is no fallback."""
 
     def asap_alap(g):
         try:
             asap, alap = _ev.asap_alap(g)
-        except RoamError:
-            return ref(g)
+        except RoamError as e:
+            if "cycle" in str(e):
+                raise mp.graph.StructuralError("graph contains a cycle") from None
+            raise
         return mp.graph.ScheduleBounds(asap=asap, alap=alap)
     return asap_alap
 
@@ -112,8 +119,9 @@ class _State:
 
 
 # dispatch counters since install(): how the planner's subtasks were served
-STATS = {"windows_k4": 0, "windows_k5": 0, "windows_dfs": 0, "windows_dfs_budget": 0, "windows_ref_dfs": 0, "leaves_k3_constrained": 0,
-         "leaves_k3_exact": 0, "leaves_search": 0, "leaves_ref_search": 0}
+# (every one by libroam: there is no reference fallback)
+STATS = {"windows_k4": 0, "windows_k5": 0, "windows_dfs": 0, "windows_dfs_budget": 0,
+         "leaves_k3_constrained": 0, "leaves_k3_exact": 0, "leaves_search": 0}
 
 
 def install(mp=None):
@@ -127,8 +135,6 @@ def install(mp=None):
     orig_solve_window = pl._solve_window
     orig_solve_layout = pl._solve_layout
     orig_pool_map = pl._pool_map
-    ref_exact_order = ordm.exact_order
-    ref_exact_layout = lay.exact_layout
 
     def to_layout(m):
         return lay.MemoryLayout(offsets=m.offsets, capacity=m.capacity,
@@ -138,8 +144,9 @@ def install(mp=None):
     def solve_windows(jobs):
         """Every greedy window in one K4 launch and every exact window in one
         K5 launch; a window with more order ideals than its node cap runs the
-        reference's capped DFS (its answer depends on where that search
-        stops).  Errors surface in job order, as the sequential map raises them."""
+        reference's capped DFS restated in libroam (its answer depends on where
+        that search stops).  Errors surface in job order, as the sequential map
+        raises them."""
         greedy = [k for k, (p, limit) in enumerate(jobs) if len(p.ops) > limit]
         exact = [k for k, (p, limit) in enumerate(jobs) if len(p.ops) <= limit]
         exact_keys = set(exact)
@@ -161,12 +168,7 @@ def install(mp=None):
                 raise r
             if r is _ord.NEEDS_SEARCH:
                 # more order ideals than the node cap: the capped DFS in libroam
-                # (windows of up to 64 ops; wider ones -- node_limit > 64 --
-                # keep the reference's own DFS)
-                if len(p.ops) > 64:
-                    out.append(ref_exact_order(p))
-                    STATS["windows_ref_dfs"] += 1
-                    continue
+                # (multi-word masks: windows of any node_limit)
                 r = _ord.search_window(p)
                 if isinstance(r, GraphError):
                     T(functools.partial(_raise, r))()
@@ -214,10 +216,6 @@ def install(mp=None):
             # others run the branch-and-bound in libroam (rm_layout_search)
             res = _lay.exact_layout_batch([jobs[k][0] for k in small])
             for k, r in zip(small, res):
-                if r is None:   # a component of > 64 items (layout_limit > 64): the reference's search
-                    out[k] = ref_exact_layout(jobs[k][0])
-                    STATS["leaves_ref_search"] += 1
-                    continue
                 out[k] = to_layout(r)
                 STATS["leaves_search" if r.stats.nodes else "leaves_k3_exact"] += 1
         return out
@@ -231,15 +229,11 @@ def install(mp=None):
         return orig_pool_map(fn, jobs, workers)
 
     T = functools.partial(_translate, mp)
-    ref_bwp = pl.build_window_problems
 
     def build_window_problems(g, lin, wu_plan=None, ops_per_step=1, time_budget=60.0, node_cap=None):
-        try:
-            return _win.build_window_problems(g, lin, wu_plan, ops_per_step, time_budget, node_cap,
-                                              window_type=mp.segmentation.Window,
-                                              problem_type=ordm.OrderingProblem)
-        except _win.Unsupported:
-            return ref_bwp(g, lin, wu_plan, ops_per_step, time_budget, node_cap)
+        return _win.build_window_problems(g, lin, wu_plan, ops_per_step, time_budget, node_cap,
+                                          window_type=mp.segmentation.Window,
+                                          problem_type=ordm.OrderingProblem)
 
     fast_linearize = _ctl.linearize_factory(mp)
     fast_tree = _ctl.subgraph_tree_factory(mp)
@@ -264,8 +258,8 @@ def install(mp=None):
         (pl, "build_window_problems"): build_window_problems,
         (ordm, "weight_update_cost"): _weight_update_cost_factory(mp),
         (ordm, "asap_alap"): _asap_alap_factory(mp),
-        (mp.segmentation, "_region_between"): _ctl.region_between_factory(mp.segmentation._region_between),
-        (mp.segmentation, "_format_ig_ok"): _ctl.format_ig_ok_factory(mp, mp.segmentation._format_ig_ok),
+        (mp.segmentation, "_region_between"): _ctl.region_between_factory(),
+        (mp.segmentation, "_format_ig_ok"): _ctl.format_ig_ok_factory(mp),
         (pl, "peak_memory"): T(_ev.peak_memory),
         (pl, "tensor_lifetimes"): T(_ev.tensor_lifetimes),
         (pl, "live_bytes_by_timestep"): T(_ev.live_bytes_by_timestep),
@@ -276,6 +270,33 @@ def install(mp=None):
         (sim, "layout_violations"): T(_lay.layout_violations),
         (sim, "peak_memory"): T(_ev.peak_memory),
     }
+    # the user-facing API: the same functions in their home modules and as
+    # the package's re-exports (memplan/__init__.py), results in the
+    # reference's own types
+    def as_ref_layout(fn):
+        return T(lambda p: to_layout(fn(p)))
+
+    def as_ref_order(batch):
+        return T(lambda p: batch([p], ordm.OrderingSolution, ordm.SolverStats)[0])
+
+    api = {
+        "peak_memory": (gr, T(_ev.peak_memory)),
+        "tensor_lifetimes": (gr, T(_ev.tensor_lifetimes)),
+        "live_bytes_by_timestep": (gr, T(_ev.live_bytes_by_timestep)),
+        "replay_static": (sim, T(_lay.replay_static)),
+        "validate_layout": (lay, T(_lay.validate_layout)),
+        "repair_conflicts": (lay, T(_lay.repair_conflicts)),
+        "llfb_layout": (lay, as_ref_layout(_lay.llfb_layout)),
+        "constrained_llfb_layout": (lay, as_ref_layout(_lay.constrained_llfb_layout)),
+        "exact_layout": (lay, as_ref_layout(_lay.exact_layout)),
+        "greedy_order": (ordm, as_ref_order(_ord.greedy_orders)),
+        "exact_order": (ordm, as_ref_order(_ord.exact_orders)),
+        "asap_alap": (gr, patches[(ordm, "asap_alap")]),
+    }
+    for name, (home, fn) in api.items():
+        patches.setdefault((home, name), fn)
+        if hasattr(mp, name):
+            patches[(mp, name)] = fn
     try:  # the CLI binds its own names at import (cli.py:14-40)
         cli = importlib.import_module(mp.__name__ + ".cli")
         patches.update({

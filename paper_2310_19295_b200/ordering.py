@@ -207,13 +207,11 @@ def search_window(p):
     return tuple(order[:len(ops)].tolist()), int(peak.value), int(nodes.value)
 
 
-def exact_orders(problems: Sequence, search=None, solution_type=OrderingSolution,
-                 stats_type=SolverStats) -> list:
+def exact_orders(problems: Sequence, solution_type=OrderingSolution, stats_type=SolverStats) -> list:
     """exact_order over many windows (one K5 launch per graph).  Windows whose
     order ideals outnumber their node cap run the reference's capped DFS in
     libroam (``search_window``): its optimum, or -- when the cap stops it --
     the greedy incumbent (K4), flagged non-optimal, as the reference returns.
-    ``search`` overrides that step (e.g. the reference's own exact_order).
     ``stats.nodes`` is the DFS's node count for searched windows and the
     number of order ideals minus one for K5's (an upper bound on the
     reference's expansions; the plan documents never contain it)."""
@@ -233,9 +231,6 @@ def exact_orders(problems: Sequence, search=None, solution_type=OrderingSolution
         if isinstance(r, Exception):
             raise r
         if r is NEEDS_SEARCH:
-            if search is not None:
-                out.append(search(p))
-                continue
             r = search_window(p)
             if isinstance(r, Exception):
                 raise r
@@ -248,7 +243,7 @@ def exact_orders(problems: Sequence, search=None, solution_type=OrderingSolution
     return out
 
 
-def exact_order(p, search=None) -> OrderingSolution:
+def exact_order(p) -> OrderingSolution:
     """Minimum-peak window order (ordering.py:183-286): K5 on the GPU, the
-    capped DFS in libroam where the node cap can bind."""
-    return exact_orders([p], search=search)[0]
+    capped DFS in libroam where the node cap can bind (any window width)."""
+    return exact_orders([p])[0]

@@ -11,7 +11,9 @@ the reference's per-tensor rule for window w at slot p reduces to
     live_in(w)  = { t : b < p <= L }
     live_out(w) = { t : b <= p <  L }
 
-(b == p exactly when the producer is inside w).  The windows are swept once in
+(b == p exactly when the producer is inside w -- unless the linearisation
+lists an op in two windows: every such window but the op's owner gets the
+reference's rule evaluated directly, vectorised over tensors).  The windows are swept once in
 slot order: between consecutive slots only the tensors born or dying in
 between change membership (found by binary search in the (b, L)-sorted
 tensor lists), so each window's sets are its predecessor's plus/minus a few
@@ -40,12 +42,12 @@ def live_set(idx: np.ndarray) -> LiveSet:
     return s
 
 
-class Unsupported(Exception):
-    """The linearisation lists an op in two windows; use the reference builder."""
-
-
 def window_intervals(g, lin, wu_plan=None):
-    """(final ops per window, slot per window, b[T], L[T], horizon)."""
+    """(final ops per window, slot per window, b[T], L[T], horizon, shared):
+    ``shared`` = the windows listing an op whose position is another
+    window's slot (the reference keeps the LAST window listing an op as its
+    position, ordering.py:490-503), for which the stabbing rule's premise
+    "producer inside <=> b == p" does not hold."""
     a = graph_arrays(g)
     n = a.n_ops
     extra = {w.index: wu_plan.ops_for_window(w.index) for w in lin.windows} if wu_plan else {}
@@ -58,6 +60,7 @@ def window_intervals(g, lin, wu_plan=None):
             slot_of_window[ref] = i
     final_ops: dict[int, tuple[int, ...]] = {}
     owner = np.full(n, -1, np.int64)
+    listed = False
     for w in lin.windows:
         ops = tuple(sorted((*w.ops, *extra.get(w.index, ()))))
         final_ops[w.index] = ops
@@ -65,10 +68,15 @@ def window_intervals(g, lin, wu_plan=None):
             raise ValueError(f"window {w.index} not in slot sequence")
         if ops:
             idx = np.asarray(ops, np.int64)
-            if (owner[idx] >= 0).any() and (owner[idx] != w.index).any():
-                raise Unsupported("op placed in two windows")
-            owner[idx] = w.index
+            listed = listed or bool((owner[idx] >= 0).any())
+            owner[idx] = w.index          # the last window listing an op wins
             op_pos[idx] = slot_of_window[w.index]
+    shared = set()
+    if listed:   # an op in two windows: every listing window but its owner
+        for w in lin.windows:
+            ops = final_ops[w.index]
+            if ops and (owner[np.asarray(ops, np.int64)] != w.index).any():
+                shared.add(w.index)
     horizon = len(lin.slots)
     producer = a.producer.astype(np.int64)
     if (op_pos[producer] < 0).any() or (a.cons_idx.size and (op_pos[a.cons_idx] < 0).any()):
@@ -80,21 +88,43 @@ def window_intervals(g, lin, wu_plan=None):
     nz = np.flatnonzero(counts > 0)
     if nz.size:
         L[nz] = np.maximum.reduceat(op_pos[a.cons_idx], a.cons_ptr[:-1][nz].astype(np.int64))
-    return final_ops, slot_of_window, b, L, horizon
+    return final_ops, slot_of_window, b, L, horizon, shared
+
+
+def _exact_sets(a, ops, p, b, L):
+    """The reference's per-tensor rule (ordering.py:505-527) for one window,
+    vectorised over tensors: membership of producer and consumers in the
+    window's own op set, positions from op_pos."""
+    inside = np.zeros(a.n_ops, bool)
+    inside[np.asarray(ops, np.int64)] = True
+    prod_in = inside[np.asarray(a.producer, np.int64)]
+    cp = np.asarray(a.cons_ptr, np.int64)
+    has = cp[1:] > cp[:-1]
+    local = np.zeros(len(b), bool)
+    if a.cons_idx.size:
+        ent = np.append(inside[np.asarray(a.cons_idx, np.int64)], False).astype(np.int64)
+        local[has] = np.add.reduceat(ent, cp[:-1][has]) > 0
+    later = L > p
+    live_out = (prod_in & later) | (~prod_in & (b < p) & later)
+    live_in = ~prod_in & (b < p) & (local | later)
+    return live_set(np.flatnonzero(live_in)), live_set(np.flatnonzero(live_out))
 
 
 def build_window_problems(g, lin, wu_plan=None, ops_per_step: int = 1, time_budget: float = 60.0,
                           node_cap=None, *, window_type, problem_type):
     """ordering.py:470-542 with the reference's own Window / OrderingProblem
     types passed in; same list, same order, same sets."""
-    final_ops, slot_of_window, b, L, _ = window_intervals(g, lin, wu_plan)
+    final_ops, slot_of_window, b, L, _, shared = window_intervals(g, lin, wu_plan)
     wins = list(lin.windows)
     slots = [slot_of_window[w.index] for w in wins]
     sets = _sweep_live_sets(b, L, sorted(set(slots)))
     out = []
     for w, p in zip(wins, slots):
-        live_in, live_out = sets[p]
         ops = final_ops[w.index]
+        if w.index in shared:
+            live_in, live_out = _exact_sets(graph_arrays(g), ops, p, b, L)
+        else:
+            live_in, live_out = sets[p]
         out.append((window_type(index=w.index, leaf=w.leaf, ops=ops),
                     problem_type(graph=g, ops=ops, live_in=live_in, live_out=live_out,
                                  ops_per_step=ops_per_step, time_budget=time_budget,

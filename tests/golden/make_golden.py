@@ -422,6 +422,50 @@ def make_exact_search():
     dump("exact_search.json", {"cases": cases, "graphs": graphs})
 
 
+# --------------------------------------- wide searches (beyond 64 bits)
+
+def make_wide_search():
+    """The two capped searches on problems wider than one 64-bit mask word
+    (node_limit / layout_limit > 64): exact_order on windows of 65-140 ops
+    (chain-like DAGs whose pruned DFS finishes, wide ones that a node cap
+    stops) and exact_layout on overlap components of 65-120 items whose
+    incumbent misses its bound, under node caps from 1 to 20k."""
+    import time as _t
+    rng = random.Random(47)
+    orders, graphs = [], {}
+    for k in range(24):
+        n = rng.randint(65, 140)
+        dens = rng.choice([0.02, 0.05, 0.3, 0.6, 0.9])
+        g = gen_random_dag(n, density=dens, seed=1300 + k)
+        name = f"wide{k}"
+        graphs[name] = rg.graph_to_doc(g)
+        for cap in (rng.choice([1, 10, 100]), rng.choice([1000, 5000]), 20_000):
+            prob = ro.OrderingProblem(graph=g, ops=tuple(range(n)), node_cap=cap)
+            t0 = _t.monotonic()
+            sol = ro.exact_order(prob)
+            orders.append({"graph": name, "ops": list(range(n)), "live_in": [], "live_out": [],
+                           "node_cap": cap, "order": list(sol.order), "peak": sol.peak,
+                           "optimal": sol.optimal, "nodes": sol.stats.nodes,
+                           "ref_s": round(_t.monotonic() - t0, 3)})
+    layouts = []
+    tries = 0
+    while len(layouts) < 48 and tries < 400:
+        tries += 1
+        n = rng.randint(65, 120)
+        horizon = rng.choice([6, 10, 20])
+        items = rand_items(rng, n, act_p=0.2, horizon=horizon)
+        bottom = rng.random() < 0.5
+        for cap in (1, rng.choice([50, 500]), 20_000):
+            q = rl.LayoutProblem(items=tuple(items), activations_at_bottom=bottom, node_cap=cap)
+            m = rl.exact_layout(q)
+            if m.stats.nodes == 0:
+                break
+            layouts.append({"items": [it_row(i) for i in items], "bottom": bottom, "node_cap": cap,
+                            "offsets": {str(t): o for t, o in m.offsets.items()}, "capacity": m.capacity,
+                            "optimal": m.optimal, "nodes": m.stats.nodes})
+    dump("wide_search.json", {"orders": orders, "graphs": graphs, "layouts": layouts})
+
+
 # ---------------------------------------------------------------- exact
 
 def random_window(g, rng):
@@ -515,7 +559,8 @@ def make_plans():
 
 if __name__ == "__main__":
     which = set(sys.argv[1:]) or {"peaks", "schedules", "layouts", "layout_search", "greedy", "exact",
-                                  "exact_search", "plans"}
-    for w in ("peaks", "schedules", "layouts", "layout_search", "greedy", "exact", "exact_search", "plans"):
+                                  "exact_search", "plans", "wide_search"}
+    for w in ("peaks", "schedules", "layouts", "layout_search", "greedy", "exact", "exact_search", "plans",
+              "wide_search"):
         if w in which:
             globals()[f"make_{w}"]()

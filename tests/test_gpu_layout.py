@@ -48,3 +48,15 @@ def test_large_random_vs_oracle(N):
             and offsets.get(j, 0) < offsets.get(i, 0) + rows[i][1]] if N <= 700 else None
     if want is not None:
         assert pairs == want
+
+
+def test_replay_extent_golden():
+    """replay_static's actual extent (simulator.py:137-145: the max over steps
+    of max(off + size) over live items with offsets = the max over all such
+    items, never below 0) from K2's epilogue, on every golden layout."""
+    from paper_2310_19295_b200.layout import _k2
+    for c in golden("layouts")["violations"]:
+        items = [LayoutItem(*r) for r in c["items"]]
+        offs = {int(k): v for k, v in c["offsets"].items()}
+        _, _, _, mx = _k2(items, offs, c["capacity"], 16)
+        assert mx == max(c["replay_extent"], 0), c

@@ -37,11 +37,24 @@ def test_golden_plan_bytes(name):
     assert got == c["plan"]
 
 
+def _config_graph(name):
+    if name.startswith("ref-"):   # the reference's own generator, e.g. ref-transformer_block-100
+        import memplan.graphgen as rgen
+        _, arch, blocks = name.split("-")
+        return rgen.gen_training_graph(arch, int(blocks), optimizer="adam")
+    return mp.graph.load_graph(gg.config_doc(name))
+
+
 @needs_ref
-@pytest.mark.parametrize("name", ["layered", "gpt2-small"])
-def test_config_plan_matches_live_reference(name):
-    g = mp.graph.load_graph(gg.config_doc(name))
+@pytest.mark.parametrize("name", ["layered", "gpt2-small", "bert-large", "gpt2-xl", "ref-transformer_block-100",
+                                  "ref-residual-60", "ref-mlp-60"])
+def test_config_plan_matches_live_reference(name, monkeypatch):
+    """BASELINE configs 1-4 (and the reference's own generator at 100 blocks):
+    plan documents byte-identical to the unpatched reference run live on the
+    same box, with no reference solver reachable under the plug-in."""
+    g = _config_graph(name)
     want = mp.planner.plan_doc_bytes(mp.planner.plan(g))
+    _ban_reference_solvers(monkeypatch)
     plug.install(mp)
     try:
         got = mp.planner.plan_doc_bytes(mp.planner.plan(g))
@@ -110,3 +123,93 @@ def test_capped_searches_match_live_reference():
     # (SURVEY probe p12), so the branch-and-bound is pinned by
     # test_layout_search.py instead
     assert runs["windows_dfs"] + runs["windows_dfs_budget"] > 0, runs
+
+
+# the reference functions no plan may run once the plug-in is installed
+_BANNED = [("ordering", "exact_order"), ("planner", "exact_order"), ("ordering", "greedy_order"),
+           ("planner", "greedy_order"), ("layout", "exact_layout"), ("planner", "exact_layout"),
+           ("layout", "constrained_llfb_layout"), ("planner", "constrained_llfb_layout"),
+           ("layout", "llfb_layout"), ("ordering", "build_window_problems"), ("graph", "asap_alap"),
+           ("graph", "predecessor_masks"), ("segmentation", "predecessor_masks"),
+           ("graph", "successor_masks"), ("segmentation", "successor_masks"),
+           ("graph", "live_bytes_by_timestep"), ("graph", "peak_memory"), ("layout", "layout_violations")]
+
+
+def _ban_reference_solvers(monkeypatch):
+    def banned(*a, **k):
+        raise AssertionError("a reference solver ran under the plug-in")
+    n = 0
+    for mod, name in _BANNED:
+        m = getattr(mp, mod)
+        if hasattr(m, name):
+            monkeypatch.setattr(m, name, banned)
+            n += 1
+    return n
+
+
+WIDE = {
+    "layered-80": (lambda: gg.layered_dag_doc(layers=10, width=8),
+                   dict(node_limit=600, layout_limit=300, order_node_cap=5000, layout_node_cap=5000)),
+    "layered-80-roomy": (lambda: gg.layered_dag_doc(layers=10, width=8),
+                         dict(node_limit=100, layout_limit=100, order_node_cap=50_000, layout_node_cap=50_000)),
+    "layered-96": (lambda: gg.layered_dag_doc(layers=8, width=12),
+                   dict(node_limit=600, layout_limit=300, order_node_cap=5000, layout_node_cap=5000)),
+    "gpt2-small-600": (lambda: gg.config_doc("gpt2-small"),
+                       dict(node_limit=600, layout_limit=300, order_node_cap=5000, layout_node_cap=5000)),
+    "gpt2-small-80": (lambda: gg.config_doc("gpt2-small"),
+                      dict(node_limit=80, layout_limit=80, order_node_cap=20_000, layout_node_cap=20_000)),
+}
+
+
+@needs_ref
+@pytest.mark.parametrize("name", sorted(WIDE))
+def test_wide_limits_served_by_libroam(name, monkeypatch):
+    """node_limit / layout_limit above 64: windows of 80-541 ops reach the
+    exact search and leaves of 240-288 items the branch-and-bound.  Every one
+    is served by libroam (multi-word masks) -- the reference's solvers,
+    window builder and closure functions are replaced by raising stubs while
+    the plug-in plans -- and the documents equal the live reference's."""
+    mk, kw = WIDE[name]
+    g = mp.graph.load_graph(mk())
+    cfg = mp.planner.PlannerConfig(**kw)
+    want = mp.planner.plan_doc_bytes(mp.planner.plan(g, cfg))
+    assert _ban_reference_solvers(monkeypatch) >= 12
+    plug.install(mp)
+    try:
+        got = mp.planner.plan_doc_bytes(mp.planner.plan(g, cfg))
+        stats = dict(plug.STATS)
+    finally:
+        plug.uninstall()
+    assert got == want
+    served = stats["windows_k5"] + stats["windows_dfs"] + stats["windows_dfs_budget"]
+    assert served > 0 and "windows_ref_dfs" not in stats and "leaves_ref_search" not in stats, stats
+
+
+@needs_ref
+@pytest.mark.parametrize("name", ["gpt2-small", "bert-large", "ref-transformer_block-20"])
+def test_replay_static_dropin_matches_live_reference(name):
+    """simulator.replay_static (simulator.py:129-145) rebound to K2's
+    max-extent epilogue: (actual, violations) equal to the reference's
+    O(steps x N) replay on a planned layout, on the same layout with a
+    few tensors shifted into each other (violations in the reference's
+    message order), with an offset missing, and through memplan's re-export."""
+    import dataclasses
+    g = _config_graph(name)
+    p = mp.planner.plan(g)
+    offs = dict(p.layout.offsets)
+    ids = sorted(offs)[:: max(1, len(offs) // 7)]
+    for t in ids[1:]:
+        offs[t] = offs[ids[0]]
+    broken = dataclasses.replace(p.layout, offsets=offs)
+    missing = dataclasses.replace(p.layout, offsets={t: o for t, o in p.layout.offsets.items() if t != ids[0]})
+    want = [mp.simulator.replay_static(g, p.schedule, m) for m in (p.layout, broken, missing)]
+    assert want[0][1] == [] and want[1][1] and want[2][1]
+    plug.install(mp)
+    try:
+        before = launch_count()
+        got = [mp.simulator.replay_static(g, p.schedule, m) for m in (p.layout, broken, missing)]
+        assert mp.replay_static(g, p.schedule, p.layout) == want[0]
+        assert launch_count() > before
+    finally:
+        plug.uninstall()
+    assert got == want

@@ -80,21 +80,26 @@ def test_exact_layout_searches_like_reference():
     assert (one.offsets, one.capacity) == (_offs(cases[0]["offsets"]), cases[0]["capacity"])
 
 
-def test_component_above_64_items_is_reported():
-    """The search keeps its masks in 64 bits: a component of 65 overlapping
-    items whose incumbent misses its bound comes back as RM_ERR_CAPACITY
-    (the planner plug-in then hands the leaf to the reference's search)."""
-    lib = _lib.lib()
-    n = 65
-    tensor = np.arange(n, dtype=np.int32)
-    start = np.zeros(n, np.int32)
-    end = np.ones(n, np.int32)
-    size = np.ones(n, np.int64)
-    act = np.zeros(n, np.uint8)
-    inc = np.arange(n, dtype=np.int64) * 2          # incumbent 2n - 1 > bound n
-    off = np.empty(n, np.int64)
-    cap, nodes, opt = C.c_int64(0), C.c_int64(0), C.c_int32(0)
-    st = lib.rm_layout_search(n, _lib.ptr(tensor), _lib.ptr(start), _lib.ptr(end), _lib.ptr(size),
-                              _lib.ptr(act), 0, _lib.ptr(inc), -1, 0.0, _lib.ptr(off),
-                              C.byref(cap), C.byref(nodes), C.byref(opt))
-    assert st == _lib.RM_ERR_CAPACITY
+def test_wide_components_match_reference_host():
+    """Components of 65-120 items (layout_limit > 64): the search's masks span
+    several 64-bit words; offsets, capacity, optimal flag and node count
+    equal the reference's under node caps from 1 to 20k
+    (tests/golden/wide_search.json)."""
+    cases = golden("wide_search")["layouts"]
+    assert len(cases) >= 40 and any(c["optimal"] for c in cases)
+    assert min(len(c["items"]) for c in cases) > 64
+    for c in cases:
+        rows = [tuple(r) for r in c["items"]]
+        got = _search(rows, c["bottom"], c["node_cap"], _incumbent(rows, c["bottom"]))
+        assert got == (_offs(c["offsets"]), c["capacity"], c["optimal"], c["nodes"]), c["node_cap"]
+
+
+@pytest.mark.gpu
+def test_wide_exact_layout_product_path():
+    from paper_2310_19295_b200.layout import LayoutItem, LayoutProblem, exact_layout_batch
+    cases = golden("wide_search")["layouts"]
+    probs = [LayoutProblem(items=tuple(LayoutItem(*r) for r in c["items"]), activations_at_bottom=c["bottom"],
+                           node_cap=c["node_cap"]) for c in cases]
+    for c, r in zip(cases, exact_layout_batch(probs)):
+        assert (r.offsets, r.capacity, r.optimal, r.stats.nodes) == \
+            (_offs(c["offsets"]), c["capacity"], c["optimal"], c["nodes"]), c["node_cap"]

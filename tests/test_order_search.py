@@ -19,7 +19,7 @@ from paper_2310_19295_b200.ordering import BUDGET, OrderingProblem, search_windo
 def _cases(name):
     G = golden(name)
     graphs = {}
-    for c in G["cases"]:
+    for c in G["orders" if name == "wide_search" else "cases"]:
         key = c["graph"] if "doc" not in c else id(c)
         if key not in graphs:
             graphs[key] = load_graph(c["doc"] if "doc" in c else G["graphs"][c["graph"]])
@@ -31,7 +31,7 @@ def _problem(g, c):
                            node_cap=c["node_cap"])
 
 
-@pytest.mark.parametrize("name", ["exact_search", "exact"])
+@pytest.mark.parametrize("name", ["exact_search", "exact", "wide_search"])
 def test_dfs_matches_reference_host(name):
     n_opt = n_budget = 0
     for g, c in _cases(name):
@@ -43,7 +43,7 @@ def test_dfs_matches_reference_host(name):
         else:
             assert r is BUDGET, c
             n_budget += 1
-    assert n_opt > 100 and n_budget >= 2
+    assert n_opt > (30 if name == "wide_search" else 100) and n_budget >= 2
 
 
 @pytest.mark.gpu
@@ -53,3 +53,16 @@ def test_exact_orders_with_dfs_fallback():
     sols = exact_orders([_problem(g, c) for g, c in cases])
     for (g, c), s in zip(cases, sols):
         assert (list(s.order), s.peak, s.optimal) == (c["order"], c["peak"], c["optimal"]), c
+
+
+@pytest.mark.gpu
+def test_wide_windows_product_path():
+    """Windows of 65-140 ops (node_limit > 64) through the product path: K5
+    hands them back, the multi-word DFS decides (reference's order, peak,
+    optimal flag)."""
+    from paper_2310_19295_b200.ordering import exact_orders
+    cases = list(_cases("wide_search"))
+    assert min(len(c["ops"]) for _, c in cases) > 64
+    sols = exact_orders([_problem(g, c) for g, c in cases])
+    for (g, c), s in zip(cases, sols):
+        assert (list(s.order), s.peak, s.optimal) == (c["order"], c["peak"], c["optimal"]), c["graph"]

@@ -159,8 +159,8 @@ def test_control_plane_dropins_match_reference():
     from paper_2310_19295_b200 import control
     seg = mp.segmentation
     ref_rb, ref_ok, ref_lin = seg._region_between, seg._format_ig_ok, seg.linearize
-    fast_rb = control.region_between_factory(ref_rb)
-    fast_ok = control.format_ig_ok_factory(mp, ref_ok)
+    fast_rb = control.region_between_factory()
+    fast_ok = control.format_ig_ok_factory(mp)
     fast_lin = control.linearize_factory(mp)
     calls = {"rb": 0, "ok": 0}
 
@@ -267,3 +267,61 @@ def test_live_set_sweep_matches_interval_rule():
             li, lo = got[p]
             assert set(li) == want_in and set(lo) == want_out
             assert set(li.arr.tolist()) == want_in and set(lo.arr.tolist()) == want_out
+
+
+@pytest.mark.skipif(mp is None, reason="reference memplan not importable")
+def test_window_problems_op_in_two_windows_matches_reference():
+    """A linearisation that lists ops in two windows (the reference then keeps
+    the LAST listing window as the op's position, ordering.py:490-503): the
+    non-owner windows get the reference's rule evaluated directly, the rest
+    the interval rule -- equal to the reference on every window."""
+    import dataclasses
+    import random
+
+    import memplan.graphgen as rgen
+
+    from paper_2310_19295_b200 import windows as W
+    rng = random.Random(5)
+    n_shared = 0
+    for arch, blocks in (("transformer_block", 3), ("mlp", 4), ("residual", 3)):
+        g = rgen.gen_training_graph(arch, blocks, optimizer="adam")
+        tree = mp.segmentation.build_subgraph_tree(g, 8)
+        lin = mp.segmentation.linearize(g, tree)
+        wu = mp.ordering.place_weight_updates(g, tree, 2.0)
+        wins = [w for w in lin.windows if w.ops]
+        for trial in range(12):
+            a, b = rng.sample(range(len(wins)), 2)
+            moved = tuple(rng.sample(wins[a].ops, min(len(wins[a].ops), rng.randint(1, 3))))
+            new = list(lin.windows)
+            k = new.index(wins[b])
+            new[k] = dataclasses.replace(new[k], ops=tuple(sorted(set(new[k].ops) | set(moved))))
+            lin2 = dataclasses.replace(lin, windows=tuple(new))
+            want = mp.ordering.build_window_problems(g, lin2, wu)
+            got = W.build_window_problems(g, lin2, wu, window_type=mp.segmentation.Window,
+                                          problem_type=mp.ordering.OrderingProblem)
+            assert got == want
+            n_shared += 1
+    assert n_shared >= 30
+
+
+@pytest.mark.skipif(mp is None, reason="reference memplan not importable")
+def test_region_between_with_custom_build_preds():
+    """_region_between on a _TreeBuild whose preds are NOT the graph's closure
+    (the core's induced closure): the drop-in unpacks build.preds itself --
+    the reference's answer, without running reference code."""
+    import memplan.graphgen as rgen
+
+    from paper_2310_19295_b200 import control
+    seg, rg = mp.segmentation, mp.graph
+    fast = control.region_between_factory()
+    for arch in ("transformer_block", "residual"):
+        g = rgen.gen_training_graph(arch, 3, optimizer="adam")
+        branches = rg.weight_update_branches(g)
+        floating = {v for b in branches for v in b.ops}
+        core = [v for v in range(g.n_ops) if v not in floating]
+        for preds in (rg.predecessor_masks(g, core[: len(core) // 2]), rg.predecessor_masks(g)):
+            build = seg._TreeBuild(g=g, node_limit=8, preds=preds, categories=rg.classify_tensors(g),
+                                   branches=branches)
+            for lo, hi in ((None, core[len(core) // 3]), (core[2], core[-3]), (core[5], None),
+                           (core[len(core) // 4], core[len(core) // 3])):
+                assert fast(build, core, lo, hi) == seg._region_between(build, core, lo, hi)
