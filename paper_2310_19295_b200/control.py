@@ -170,6 +170,62 @@ def _fast_build_type(seg):
     return cls
 
 
+def _mi_full(g, c):
+    """``_mi_over(g, all ops)`` (segmentation.py:108-117) and each op's count
+    of memory-insensitive ancestors: ancestors from the C++ closure, the
+    descendants as n-1-alap (libroam's asap_alap), MI ops ordered by their
+    ancestor count (distinct: they are totally ordered)."""
+    from .evaluator import asap_alap
+    n, anc = c["n"], c["anc"]
+    n_anc = c["count"]
+    n_desc = n - 1 - np.asarray(asap_alap(g)[1], np.int64) if n else np.zeros(0, np.int64)
+    mi_mask = n_anc + n_desc == n - 1
+    mi = sorted(np.nonzero(mi_mask)[0].tolist(), key=lambda v: int(n_anc[v]))
+    mimask = np.zeros(anc.shape[1] * 8, bool)
+    if mi:
+        mimask[np.asarray(mi, np.int64)] = True
+    gap = np.bitwise_count(anc & np.packbits(mimask, bitorder="little")).sum(axis=1, dtype=np.int64)
+    return mi, mi_mask, gap
+
+
+def segment_tree_factory(mp):
+    """Drop-in for segmentation.build_segment_tree (segmentation.py:451-476)
+    and independent_segments (120-136), the inference-graph decomposition:
+    the memory-insensitive ops and each op's number of MI ancestors come from
+    the C++ closure instead of big-int masks popcounted per op; the nodes are
+    the reference's own ``SubgraphNode`` with the same ids and fields."""
+    seg, gr = mp.segmentation, mp.graph
+
+    def independent_segments(g):
+        c = closure(g)
+        mi, mi_mask, gap = _mi_full(g, c)
+        other = np.nonzero(~mi_mask)[0]
+        out = []
+        for k in range(len(mi) + 1):
+            members = tuple(other[gap[other] == k].tolist())
+            out.append(seg.Segment(lo=mi[k - 1] if k > 0 else None,
+                                   hi=mi[k] if k < len(mi) else None, members=members))
+        return out
+
+    def build_segment_tree(g, node_limit):
+        if node_limit < 2:
+            raise gr.ConfigError("node_limit must be >= 2")
+        children = []
+        next_id = 1
+        for s in independent_segments(g):
+            if not s.members:
+                continue
+            children.append(seg.SubgraphNode(id=next_id, kind="independent", outer_fwd=s.lo, outer_bwd=s.hi,
+                                             members=s.members, unsplittable=len(s.members) > node_limit))
+            next_id += 1
+        if not children:
+            children.append(seg.SubgraphNode(id=next_id, kind="independent", tag="catchall"))
+        mi, _, _ = _mi_full(g, closure(g))
+        return seg.SubgraphNode(id=0, kind="root", children=tuple(children), pinned_ops=tuple(sorted(mi)))
+
+    return independent_segments, build_segment_tree
+
+
 def subgraph_tree_factory(mp):
     """Drop-in for segmentation.build_subgraph_tree (segmentation.py:343-448).
 

@@ -9,7 +9,7 @@
 namespace roam {
 
 extern thread_local bool g_timing;     // rm_set_timing
-extern int g_sm_reserve;               // rm_set_sm_reserve: SMs K1 leaves free
+extern thread_local int g_sm_reserve;  // rm_set_sm_reserve: SMs K1 leaves free (this thread's calls)
 extern thread_local double g_last_ms;  // rm_last_kernel_ms
 
 __device__ __forceinline__ void gbar(int id, int nt) {

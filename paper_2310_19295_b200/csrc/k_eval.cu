@@ -21,6 +21,7 @@
 //          group exclusive scan of chunk totals, (max, min-index) reduction.
 #include <climits>
 #include <cstring>
+#include <map>
 
 #include <cstdlib>
 
@@ -29,7 +30,7 @@
 namespace roam {
 
 thread_local bool g_timing = false;
-int g_sm_reserve = 0;
+thread_local int g_sm_reserve = 0;
 thread_local double g_last_ms = -1.0;
 
 struct K1Args {
@@ -844,18 +845,19 @@ int rm_eval_select_key(RmGraph* g, const void* orders, int64_t B, int64_t id_bas
     RM_CUDA(cudaStreamSynchronize(s));
     return RM_OK;
   }
-  // per-thread, per-device partials and a counter the kernel leaves at zero
+  // partials and a counter the kernel leaves at zero, one set per (device,
+  // stream): launches on one stream are ordered (PDL waits before touching
+  // them), launches on different streams never share a counter
   struct SelCtx {
-    int dev = -1;
     long long* partial = nullptr;
     unsigned* counter = nullptr;
   };
-  static thread_local SelCtx ctx;
-  if (ctx.dev != g->device) {
+  static thread_local std::map<std::pair<int, cudaStream_t>, SelCtx> ctxs;
+  SelCtx& ctx = ctxs[{g->device, s}];
+  if (!ctx.counter) {
     RM_CUDA(cudaMalloc(&ctx.partial, sizeof(long long) * 4096));
     RM_CUDA(cudaMalloc(&ctx.counter, sizeof(unsigned)));
-    RM_CUDA(cudaMemset(ctx.counter, 0, sizeof(unsigned)));
-    ctx.dev = g->device;
+    RM_CUDA(cudaMemsetAsync(ctx.counter, 0, sizeof(unsigned), s));
   }
   const K1KeySel sel{out_key, ctx.partial, ctx.counter, id_base, id_bits};
   bool fused = false;

@@ -347,7 +347,9 @@ extern "C" int rm_exact_windows(RmGraph* g, int32_t W, const int64_t* win_ptr,
   else RM_CUDA(sc.alloc(&d_v, 1));
   K5Args a{W, d_nops, d_ob, d_gop, d_pred, d_out, d_tb, d_cm, d_tsz, d_sl, d_cap,
            d_ord, d_peak, d_nodes, d_st, d_v, gmax, max_ten};
-  const size_t smem = (8u << K5_SMEM_N) + 8 * size_t(K5_MAX_N + max_ten) + 4 * size_t(K5_MAX_N + max_ten);
+  // + 16 B: the tensor loops' remainder may read s_cm as a pair (LDS.64) one
+  // word past its last entry (compute-sanitizer memcheck, k_exact.cu walk)
+  const size_t smem = (8u << K5_SMEM_N) + 8 * size_t(K5_MAX_N + max_ten) + 4 * size_t(K5_MAX_N + max_ten) + 16;
   constexpr int NT = 512;
   RM_CUDA(smem_optin(k5_exact<NT>));
   k5_exact<NT><<<grid, NT, smem, s>>>(a);

@@ -97,6 +97,18 @@ def _stream_handle(stream) -> int | None:
     return getattr(stream, "cuda_stream", stream) or None
 
 
+def _on(stream):
+    """Allocate a call's outputs on the stream its kernels run on: torch's
+    caching allocator ties a block to the stream current at allocation, so
+    outputs made on another stream could be reused while the kernels still
+    write them (a raw handle is the caller's to order)."""
+    import contextlib
+    if stream is not None and hasattr(stream, "cuda_stream"):
+        import torch
+        return torch.cuda.stream(stream)
+    return contextlib.nullcontext()
+
+
 # ------------------------------------------------------ single schedules
 
 _MSG = {
@@ -239,11 +251,12 @@ def evaluate_orders(g, orders, stream=None):
         import torch
         if orders.dim() != 2 or orders.shape[1] != n:
             raise ValueError(f"orders must be [B, {n}]")
-        orders = orders.contiguous()
-        B = orders.shape[0]
-        peak, arg, val = _device_outputs(orders, B)
-        check(lib().rm_eval_orders(dg.handle, ptr(orders), B, flags, ptr(peak), ptr(arg), ptr(val),
-                                   _stream_handle(stream)), "rm_eval_orders")
+        with _on(stream):
+            orders = orders.contiguous()
+            B = orders.shape[0]
+            peak, arg, val = _device_outputs(orders, B)
+            check(lib().rm_eval_orders(dg.handle, ptr(orders), B, flags, ptr(peak), ptr(arg), ptr(val),
+                                       _stream_handle(stream)), "rm_eval_orders")
         return peak, arg, val.view(torch.bool)
     _lib.require_device()
     o, flags = _host_rows(orders, n)
@@ -268,12 +281,13 @@ def evaluate_and_select(g, orders, id_base: int = 0, stream=None):
         import torch
         if orders.dim() != 2 or orders.shape[1] != n:
             raise ValueError(f"orders must be [B, {n}]")
-        orders = orders.contiguous()
-        B = orders.shape[0]
-        peak, arg, val = _device_outputs(orders, B)
-        best = torch.empty(2, dtype=torch.int64, device=orders.device)
-        check(lib().rm_eval_select(dg.handle, ptr(orders), B, id_base, flags, ptr(peak), ptr(arg),
-                                   ptr(val), ptr(best), _stream_handle(stream)), "rm_eval_select")
+        with _on(stream):
+            orders = orders.contiguous()
+            B = orders.shape[0]
+            peak, arg, val = _device_outputs(orders, B)
+            best = torch.empty(2, dtype=torch.int64, device=orders.device)
+            check(lib().rm_eval_select(dg.handle, ptr(orders), B, id_base, flags, ptr(peak), ptr(arg),
+                                       ptr(val), ptr(best), _stream_handle(stream)), "rm_eval_select")
         return peak, arg, val, best
     _lib.require_device()
     o, flags = _host_rows(orders, n)
@@ -291,10 +305,11 @@ def select_device(peak, valid, id_base: int = 0, stream=None):
     """Device-resident argmin: 2-element int64 CUDA tensor {peak, id + id_base}
     (no host synchronisation; the multi-GPU exchange consumes it directly)."""
     import torch
-    out = torch.empty(2, dtype=torch.int64, device=peak.device)
-    v = valid.view(torch.uint8) if valid.dtype == torch.bool else valid.to(torch.uint8)
-    check(lib().rm_argmin(ptr(peak), ptr(v), peak.shape[0], id_base, _lib.RM_DEVICE_PTRS, ptr(out),
-                          _stream_handle(stream)), "rm_argmin")
+    with _on(stream):
+        out = torch.empty(2, dtype=torch.int64, device=peak.device)
+        v = valid.view(torch.uint8) if valid.dtype == torch.bool else valid.to(torch.uint8)
+        check(lib().rm_argmin(ptr(peak), ptr(v), peak.shape[0], id_base, _lib.RM_DEVICE_PTRS, ptr(out),
+                              _stream_handle(stream)), "rm_argmin")
     return out
 
 
@@ -302,11 +317,12 @@ def select_key_device(g, peak, valid, id_base: int, id_bits: int, stream=None):
     """Device-resident packed key (peak << id_bits) | id of the first strict
     minimum (INT64_MAX if none valid): one int64 for all_reduce(MIN)."""
     import torch
-    out = torch.empty(1, dtype=torch.int64, device=peak.device)
-    v = valid.view(torch.uint8) if valid.dtype == torch.bool else valid.to(torch.uint8)
-    check(lib().rm_argmin_key(ptr(peak), ptr(v), peak.shape[0], id_base, id_bits,
-                              device_graph(g).info()["total_bytes"], ptr(out), _stream_handle(stream)),
-          "rm_argmin_key")
+    with _on(stream):
+        out = torch.empty(1, dtype=torch.int64, device=peak.device)
+        v = valid.view(torch.uint8) if valid.dtype == torch.bool else valid.to(torch.uint8)
+        check(lib().rm_argmin_key(ptr(peak), ptr(v), peak.shape[0], id_base, id_bits,
+                                  device_graph(g).info()["total_bytes"], ptr(out), _stream_handle(stream)),
+              "rm_argmin_key")
     return out
 
 
@@ -323,13 +339,14 @@ def evaluate_select_key(g, orders, id_base: int, id_bits: int, stream=None):
         raise ValueError("evaluate_select_key takes CUDA rows")
     if orders.dim() != 2 or orders.shape[1] != n:
         raise ValueError(f"orders must be [B, {n}]")
-    orders = orders.contiguous()
-    B = orders.shape[0]
-    peak, arg, val = _device_outputs(orders, B)
-    key = torch.empty(1, dtype=torch.int64, device=orders.device)
-    check(lib().rm_eval_select_key(dg.handle, ptr(orders), B, id_base, id_bits, flags, ptr(peak),
-                                   ptr(arg), ptr(val), ptr(key), _stream_handle(stream)),
-          "rm_eval_select_key")
+    with _on(stream):
+        orders = orders.contiguous()
+        B = orders.shape[0]
+        peak, arg, val = _device_outputs(orders, B)
+        key = torch.empty(1, dtype=torch.int64, device=orders.device)
+        check(lib().rm_eval_select_key(dg.handle, ptr(orders), B, id_base, id_bits, flags, ptr(peak),
+                                       ptr(arg), ptr(val), ptr(key), _stream_handle(stream)),
+              "rm_eval_select_key")
     return peak, arg, val.view(torch.bool), key
 
 
@@ -340,10 +357,11 @@ def argmin_orders(peak, valid, id_base: int = 0, stream=None) -> tuple[int, int]
     out = np.empty(2, np.int64)
     if hasattr(peak, "is_cuda") and peak.is_cuda:
         import torch
-        dout = torch.empty(2, dtype=torch.int64, device=peak.device)
-        v = valid.view(torch.uint8) if valid.dtype == torch.bool else valid.to(torch.uint8)
-        check(lib().rm_argmin(ptr(peak), ptr(v), peak.shape[0], id_base, _lib.RM_DEVICE_PTRS,
-                              ptr(dout), _stream_handle(stream)), "rm_argmin")
+        with _on(stream):
+            dout = torch.empty(2, dtype=torch.int64, device=peak.device)
+            v = valid.view(torch.uint8) if valid.dtype == torch.bool else valid.to(torch.uint8)
+            check(lib().rm_argmin(ptr(peak), ptr(v), peak.shape[0], id_base, _lib.RM_DEVICE_PTRS,
+                                  ptr(dout), _stream_handle(stream)), "rm_argmin")
         return tuple(int(x) for x in dout.cpu().tolist())
     p = np.ascontiguousarray(peak, dtype=np.int64)
     v = np.ascontiguousarray(valid, dtype=np.uint8)
@@ -356,9 +374,10 @@ def generate_orders(g, seed: int, first_id: int, B: int, device=None, stream=Non
     import torch
     dg = device_graph(g)
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-    out = torch.empty((B, dg.n_ops), dtype=torch.int32, device=dev)
-    check(lib().rm_gen_orders(dg.handle, seed & (2**64 - 1), first_id, B, ptr(out),
-                              _stream_handle(stream)), "rm_gen_orders")
+    with _on(stream):
+        out = torch.empty((B, dg.n_ops), dtype=torch.int32, device=dev)
+        check(lib().rm_gen_orders(dg.handle, seed & (2**64 - 1), first_id, B, ptr(out),
+                                  _stream_handle(stream)), "rm_gen_orders")
     return out
 
 

@@ -237,6 +237,7 @@ def install(mp=None):
 
     fast_linearize = _ctl.linearize_factory(mp)
     fast_tree = _ctl.subgraph_tree_factory(mp)
+    fast_segments, fast_segment_tree = _ctl.segment_tree_factory(mp)
     wu_branches = _ctl.weight_update_branches_factory(mp)
     fast_assign = _ctl.assign_shared_tensors_factory(mp)
     cats = _ctl.classify_tensors_factory(mp)
@@ -249,6 +250,9 @@ def install(mp=None):
         (mp.segmentation, "assign_shared_tensors"): fast_assign,
         (pl, "assign_shared_tensors"): fast_assign,
         (pl, "build_subgraph_tree"): fast_tree,
+        (mp.segmentation, "independent_segments"): fast_segments,
+        (mp.segmentation, "build_segment_tree"): fast_segment_tree,
+        (pl, "build_segment_tree"): fast_segment_tree,
         (gr, "weight_update_branches"): wu_branches,
         (mp.segmentation, "weight_update_branches"): wu_branches,
         (ordm, "weight_update_branches"): wu_branches,
@@ -292,6 +296,7 @@ def install(mp=None):
         "greedy_order": (ordm, as_ref_order(_ord.greedy_orders)),
         "exact_order": (ordm, as_ref_order(_ord.exact_orders)),
         "asap_alap": (gr, patches[(ordm, "asap_alap")]),
+        "independent_segments": (mp.segmentation, fast_segments),
     }
     for name, (home, fn) in api.items():
         patches.setdefault((home, name), fn)

@@ -107,17 +107,21 @@ def evaluate_sharded(g, total: int, seed: int = 0, group=None, stream=None,
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     lo, hi = shard_range(total, world, rank)
     dev = torch.device("cuda", torch.cuda.current_device())
-    best = torch.tensor([NONE_PEAK, -1], dtype=torch.int64, device=dev)
-    n_valid = torch.zeros((), dtype=torch.int64, device=dev)
-    for c0 in range(lo, hi, max(1, chunk)):
-        nb = min(chunk, hi - c0)
-        orders = ev.generate_orders(g, seed, c0, nb, device=dev, stream=stream)
-        peak, _, valid = ev.evaluate_orders(g, orders, stream=stream)
-        cb = ev.select_device(peak, valid, id_base=c0, stream=stream)
-        n_valid += valid.sum()
-        # chunks arrive in id order: a later chunk wins only with a strictly smaller peak
-        take = (cb[1] >= 0) & ((best[1] < 0) | (cb[0] < best[0]))
-        best = torch.where(take, cb, best)
+    # every allocation and torch op of the loop on the kernels' stream
+    with ev._on(stream):
+        best = torch.tensor([NONE_PEAK, -1], dtype=torch.int64, device=dev)
+        n_valid = torch.zeros((), dtype=torch.int64, device=dev)
+        for c0 in range(lo, hi, max(1, chunk)):
+            nb = min(chunk, hi - c0)
+            orders = ev.generate_orders(g, seed, c0, nb, device=dev, stream=stream)
+            peak, _, valid = ev.evaluate_orders(g, orders, stream=stream)
+            cb = ev.select_device(peak, valid, id_base=c0, stream=stream)
+            n_valid += valid.sum()
+            # chunks arrive in id order: a later chunk wins only with a strictly smaller peak
+            take = (cb[1] >= 0) & ((best[1] < 0) | (cb[0] < best[0]))
+            best = torch.where(take, cb, best)
+    if stream is not None and hasattr(stream, "synchronize"):
+        torch.cuda.current_stream().wait_stream(stream)
     if world > 1:
         best = allgather_best(best, group)
     b = [int(x) for x in best.cpu().tolist()]

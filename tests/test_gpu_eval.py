@@ -316,6 +316,32 @@ def test_fused_key_selection(name, variant):
         set_k1_variant(0)
 
 
+def test_fused_selection_on_two_streams_from_one_thread():
+    """Fused K1 selections issued from one thread on two streams with no sync
+    in between keep separate partials and counters (one set per stream): each
+    key equals its own batch's first strict minimum, and a third round on the
+    same streams still elects the last group correctly."""
+    import torch
+    from paper_2310_19295_b200.evaluator import evaluate_select_key
+    from paper_2310_19295_b200.sharding import decode_key, key_bits
+    g = load_graph(gg.config_doc("gpt2-small"))
+    a = generate_orders(g, 11, 0, 20000)
+    b = generate_orders(g, 12, 0, 9000)
+    bits = key_bits(1 << 20)
+    want = []
+    for rows in (a, b):
+        p, _, v = evaluate_orders(g, rows)
+        want.append(O.first_strict_min(p.cpu().tolist(), v.cpu().tolist()))
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(3):
+        _, _, _, k1 = evaluate_select_key(g, a, 0, bits, stream=s1)
+        _, _, _, k2 = evaluate_select_key(g, b, 0, bits, stream=s2)
+        torch.cuda.synchronize()
+        assert decode_key(int(k1.item()), bits) == tuple(want[0])
+        assert decode_key(int(k2.item()), bits) == tuple(want[1])
+
+
 def test_host_staged_calls_from_two_threads():
     """libroam is re-entrant: host-buffer calls of different batch sizes (so
     different K1 launch geometries and shared-memory sizes) from two threads on

@@ -325,3 +325,28 @@ def test_region_between_with_custom_build_preds():
             for lo, hi in ((None, core[len(core) // 3]), (core[2], core[-3]), (core[5], None),
                            (core[len(core) // 4], core[len(core) // 3])):
                 assert fast(build, core, lo, hi) == seg._region_between(build, core, lo, hi)
+
+
+@pytest.mark.skipif(mp is None, reason="reference memplan not importable")
+def test_segment_tree_dropin_matches_reference():
+    """build_segment_tree / independent_segments (segmentation.py:120-136,
+    451-476), the inference-graph decomposition plan() runs on graphs with no
+    backward op, from the C++ closure: the reference's segments and tree node
+    for node on the layered config graph, random DAGs and chains (host-only)."""
+    import memplan.graphgen  # noqa: F401  (mp.graphgen)
+
+    from paper_2310_19295_b200 import control
+    from paper_2310_19295_b200 import graphgen as gg
+    seg = mp.segmentation
+    fast_segments, fast_tree = control.segment_tree_factory(mp)
+    graphs = [mp.graph.load_graph(gg.config_doc("layered")),
+              mp.graph.load_graph(gg.layered_dag_doc(layers=6, width=1))]
+    graphs += [mp.graphgen.gen_random_dag(n, d, seed=seed) for n, d, seed in
+               ((1, 0.3, 0), (12, 0.2, 1), (40, 0.1, 2), (60, 0.05, 3), (80, 0.3, 4))]
+    graphs.append(mp.graphgen.gen_greedy_trap(0))
+    for g in graphs:
+        assert fast_segments(g) == seg.independent_segments(g)
+        for limit in (2, 5, 20, 10**6):
+            assert _tree_key(fast_tree(g, limit)) == _tree_key(seg.build_segment_tree(g, limit))
+    with pytest.raises(mp.graph.ConfigError, match="node_limit"):
+        fast_tree(graphs[0], 1)
