@@ -315,11 +315,11 @@ int64_t rm_launch_count(void);
 /* Device time (ms) of the last rm_eval_orders K1 launch on this thread when
  * timing was requested through rm_set_timing(1); -1 if unavailable. */
 int rm_set_timing(int enable);
-/* Force the K1 evaluator variant on this thread: 0 auto (v4, else v3 pairs /
- * v2, else generic), 1 the generic evaluator, 2 v2 (one candidate per group),
- * 3 v3 (two candidates per group), 4 v4 (sentinel permutation check, SIMD
- * edge checks); unsupported choices fall back.  For tests and A/B
- * measurement. */
+/* Force the K1 evaluator variant on this thread: 0 auto (v5, else v4, else
+ * v3 pairs / v2, else generic), 1 the generic evaluator, 2 v2 (one candidate
+ * per group), 3 v3 (two candidates per group), 4 v4 (sentinel permutation
+ * check, SIMD edge checks), 5 v5 (v4's checks, one dynamic class byte per
+ * position); unsupported choices fall back.  For tests and A/B measurement. */
 int rm_set_k1_variant(int variant);
 /* Leave `sms` SMs idle in every K1 launch of this process (default 0), so a
  * collective issued on another stream (the multi-GPU selection exchange) runs

@@ -399,10 +399,11 @@ extern "C" int rm_greedy_windows(RmGraph* g, int32_t W, const int64_t* win_ptr,
   RM_CUDA(sc.alloc(&d_ord, size_t(std::max<int64_t>(opb_dev[W], 1))));
   RM_CUDA(sc.alloc(&d_peak, size_t(W)));
   RM_CUDA(sc.alloc(&d_st, size_t(W)));
-  // a window the kernel abandons (cycle) leaves its peak unwritten: defined
-  // bytes for the read-back (compute-sanitizer initcheck)
+  // a window the kernel abandons (cycle) leaves its peak and the rest of its
+  // order unwritten: defined bytes for the read-back (compute-sanitizer initcheck)
   RM_CUDA(cudaMemsetAsync(d_peak, 0, size_t(W) * 8, s));
   RM_CUDA(cudaMemsetAsync(d_st, 0, size_t(W) * 4, s));
+  RM_CUDA(cudaMemsetAsync(d_ord, 0xff, size_t(std::max<int64_t>(opb_dev[W], 1)) * 4, s));
   if (gbytes) RM_CUDA(sc.alloc(&d_g, gbytes));
   K4Args a{W, d_ob, d_nops, d_tb, d_gop, d_out, d_np, d_inp, d_ini, d_sup, d_sui, d_c0, d_tcp, d_tci,
            d_tsz, d_sl, d_ord, d_peak, d_st, d_g, d_goff};

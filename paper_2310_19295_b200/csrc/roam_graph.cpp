@@ -238,8 +238,13 @@ static void build_k1v4_host(RmGraph& g) {
     g.h4_mpair.push_back(((w & 0xffffu) << 1) | ((w >> 16) << 17));
     g.h4_msz.push_back(g.h2_msz[m]);
   }
-  while (g.h4_mpair.size() % NT) {
-    g.h4_mpair.push_back(0);
+  // padding pairs (zero size) name one id twice, a different id each, so
+  // their free atomics land on distinct slots: a padding list that all
+  // pointed at id 0 serialised its 32 lanes on one address (ncu: 40
+  // wavefronts per candidate for that one ATOMS)
+  for (uint32_t i = 0; g.h4_mpair.size() % NT; ++i) {
+    const uint32_t id = n > 0 ? i % (uint32_t)n : 0u;
+    g.h4_mpair.push_back((id << 1) | (id << 17));
     g.h4_msz.push_back(0);
   }
   g.h4_msz.insert(g.h4_msz.end(), g.h2_msz.begin() + g.h2_mpair.size(), g.h2_msz.end());
@@ -269,6 +274,99 @@ static void build_k1v4_host(RmGraph& g) {
   g.k4v.n_edges = (int64_t)g.h4_edges.size();
   g.k4v.n_pair = (int64_t)g.h4_mpair.size();
   g.k4v.ok = 1;
+}
+
+// K1 v5 metadata (see roam_internal.h K1V5Meta).  An op's events in one
+// candidate are its static frees and outputs plus, for each multi-consumer
+// tensor it is a maximal consumer of, whether it is the latest one: every
+// distinct signature (fs, out, those tensors' sizes) gets a block of 2^m
+// consecutive classes, class = block base + mask.
+static void build_k1v5_host(RmGraph& g) {
+  g.k5v.ok = 0;
+  if (!g.k4v.ok || !g.k2v.ok) return;
+  const int n = g.n, SL = g.k4v.SL, NT = g.k4v.NT;
+  if (SL > 8192) return;  // a consumer id and a 3-bit bit index share 16 bits
+  const int shift = g.k2v.shift;
+  const size_t M = g.h_msize.size();
+  std::vector<std::vector<int>> dyn(n);
+  for (size_t m = 0; m < M; ++m)
+    for (int q = g.h_mptr[m]; q < g.h_mptr[m + 1]; ++q) dyn[g.h_mcons[q]].push_back((int)m);
+  std::map<std::vector<int64_t>, int> blocks;
+  std::vector<int32_t> tab;
+  auto block = [&](const std::vector<int64_t>& sig) -> int {
+    auto it = blocks.find(sig);
+    if (it != blocks.end()) return it->second;
+    const int b = (int)(tab.size() / 2), m = (int)sig.size() - 2;
+    for (int mask = 0; mask < (1 << m); ++mask) {
+      int64_t f = sig[0];
+      for (int i = 0; i < m; ++i)
+        if (mask >> i & 1) f += sig[2 + i];
+      tab.push_back((int32_t)(uint32_t)f);  // <= UINT32_MAX (build_k1v2_host's bound)
+      tab.push_back((int32_t)sig[1]);
+    }
+    blocks.emplace(sig, b);
+    return b;
+  };
+  std::vector<uint8_t> base(size_t(SL + 16), 0);
+  const int zero = block({0, 0});
+  std::fill(base.begin(), base.end(), (uint8_t)zero);
+  for (int v = 0; v < n; ++v) {
+    const int m = (int)dyn[v].size();
+    if (m > 7) return;
+    std::vector<int64_t> sig = {g.h_fs[g.h_vidx[v]] >> shift, g.h_out[g.h_vidx[v]] >> shift};
+    for (int t : dyn[v]) sig.push_back(g.h_msize[t] >> shift);
+    const int b = block(sig);
+    if (b + (1 << m) > 256) return;
+    base[v] = (uint8_t)b;
+  }
+  auto idx_of = [&](int v, int t) {
+    return (uint32_t)(std::find(dyn[v].begin(), dyn[v].end(), t) - dyn[v].begin());
+  };
+  std::vector<uint32_t> pw;
+  g.h5_gptr.assign(1, 0);
+  g.h5_gcons.clear();
+  g.h5_g4.clear();
+  for (size_t m = 0; m < M; ++m) {
+    const int q0 = g.h_mptr[m], q1 = g.h_mptr[m + 1];
+    if (q1 - q0 == 2) {
+      const int a = g.h_mcons[q0], b = g.h_mcons[q0 + 1];
+      pw.push_back((uint32_t)a | ((uint32_t)b << 13) | (idx_of(a, (int)m) << 26) | (idx_of(b, (int)m) << 29));
+    } else if (q1 - q0 <= 4) {
+      uint32_t e[4];
+      for (int q = q0; q < q0 + 4; ++q) {
+        const int c = g.h_mcons[q < q1 ? q : q0];
+        e[q - q0] = (uint32_t)c | (idx_of(c, (int)m) << 13);
+      }
+      g.h5_g4.push_back(e[0] | (e[1] << 16));
+      g.h5_g4.push_back(e[2] | (e[3] << 16));
+    } else {
+      for (int q = q0; q < q1; ++q) {
+        const int c = g.h_mcons[q];
+        g.h5_gcons.push_back((uint16_t)(c | (idx_of(c, (int)m) << 13)));
+      }
+      g.h5_gptr.push_back((uint32_t)g.h5_gcons.size());
+    }
+  }
+  while ((g.h5_g4.size() / 2) % NT) g.h5_g4.push_back(0xe000e000u);
+  // lane interleave: slot tid + i*NT holds pair tid*pk + i, so the lanes of a
+  // warp touch pairs pk apart (nearby pairs share class-byte words, and
+  // same-word atomics from one instruction serialise); padding slots hold
+  // pair (0, 0) with bit indices 7 (0xfc000000), which the kernel predicates off
+  const size_t P = pw.size(), pk = (P + NT - 1) / NT;
+  g.h5_dpair.assign(pk * NT, 0xfc000000u);
+  for (size_t i = 0; i < pk; ++i)
+    for (int t = 0; t < NT; ++t) {
+      const size_t src = size_t(t) * pk + i, dst = size_t(t) + i * NT;
+      if (src < P) g.h5_dpair[dst] = pw[src];
+    }
+  g.h5_base = base;
+  g.h5_tab = tab;
+  g.k5v.ncls = (int)(tab.size() / 2);
+  g.k5v.n_pair = (int64_t)g.h5_dpair.size();
+  g.k5v.n_g4 = (int64_t)g.h5_g4.size() / 2;
+  g.k5v.n_gen = (int64_t)g.h5_gptr.size() - 1;
+  g.k5v.n_gcons = (int64_t)g.h5_gcons.size();
+  g.k5v.ok = 1;
 }
 
 // SIMD edge-mask words of K1 v4, em[q] (one per 8-id chunk q, held in a
@@ -371,9 +469,10 @@ static int build_k1_host(RmGraph& g, bool allow_reduce) {
   build_k1v2_host(g, out, fs);
   build_k1v4_host(g);
   build_k1_em(g);
+  build_k1v5_host(g);
 
   RmGraphInfo& I = g.info;
-  I.k1_variant = g.k4v.ok ? 4 : g.k2v.ok ? (g.n <= 1024 ? 3 : 2) : 1;
+  I.k1_variant = g.k5v.ok ? 5 : g.k4v.ok ? 4 : g.k2v.ok ? (g.n <= 1024 ? 3 : 2) : 1;
   I.unit_shift = g.k2v.shift;
   I.n_check_edges = (int64_t)g.h_edge_u.size();
   I.n_multi = (int64_t)g.h_msize.size();
@@ -562,6 +661,12 @@ int rm_graph_create(const RmGraphDesc* d, uint32_t flags, RmGraph** out) {
     if (!e && g->k4v.ok) e = up(g->k4v.em, g->h4_em);
     if (!e && g->k4v.ok && g->k4v.ncls) e = up(g->k4v.cls, g->h4_cls);
     if (!e && g->k4v.ok && g->k4v.ncls) e = up(g->k4v.tab, g->h4_tab);
+    if (!e && g->k5v.ok) e = up(g->k5v.base, g->h5_base);
+    if (!e && g->k5v.ok) e = up(g->k5v.tab, g->h5_tab);
+    if (!e && g->k5v.ok) e = up(g->k5v.dpair, g->h5_dpair);
+    if (!e && g->k5v.ok) e = up(g->k5v.g4, g->h5_g4);
+    if (!e && g->k5v.ok) e = up(g->k5v.gptr, g->h5_gptr);
+    if (!e && g->k5v.ok) e = up(g->k5v.gcons, g->h5_gcons);
     if (!e) e = up(g->d_size, g->size);
     if (!e) e = up(g->d_producer, g->producer);
     if (!e) e = up(g->d_cons_ptr, g->cons_ptr);

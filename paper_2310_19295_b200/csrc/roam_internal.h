@@ -133,6 +133,28 @@ struct K1V4Meta {
   DevBuf cls, tab;
 };
 
+// K1 v5 metadata (k_eval_v5.cu; on top of K1V4Meta's geometry, em and
+// generic edges).  One byte per op per candidate: class(v, mask) = base[v] +
+// mask, mask bit i set when v is the latest maximal consumer of its i-th
+// multi-consumer tensor (build_k1v5_host); ok = 0 when a graph needs more
+// than 255 classes or an op has more than 7 multi-consumer tensors.
+//   base  = base class per id [SL + 16] (padding ids and the sink: a zero class)
+//   tab   = int2 {fs, out} units per class [ncls]
+//   dpair = two-consumer tensors a | b << 13 | ia << 26 | ib << 29 (ia / ib:
+//           the tensor's bit index in a's / b's class); lane-interleaved (slot
+//           tid + i*NT holds the thread's i-th pair, consecutive lanes far
+//           apart) and padded to a multiple of NT with 0xfc000000 (pair (0, 0))
+//   g4    = the 3-4 consumer tensors, four u16 (id | bit index << 13) each
+//           (a short list repeats its first entry), padded to a multiple of
+//           NT with 0xe000 entries
+//   gptr / gcons = the >= 5 consumer tensors as a CSR of the same u16 entries
+struct K1V5Meta {
+  int ok = 0;
+  int ncls = 0;
+  int64_t n_pair = 0, n_g4 = 0, n_gen = 0, n_gcons = 0;
+  DevBuf base, tab, dpair, g4, gptr, gcons;
+};
+
 }  // namespace roam
 
 struct RmGraph {
@@ -154,12 +176,17 @@ struct RmGraph {
   roam::K1Meta k1;
   roam::K1V2Meta k2v;
   roam::K1V4Meta k4v;
+  roam::K1V5Meta k5v;
   std::vector<int32_t> h2_opv;     // 2n
   std::vector<uint32_t> h2_edges, h2_mpair, h2_mptr, h2_msz;
   std::vector<uint16_t> h2_mcons;
   std::vector<uint32_t> h4_em, h4_edges, h4_mpair, h4_msz;
   std::vector<uint8_t> h4_cls;
   std::vector<int32_t> h4_tab;
+  std::vector<uint8_t> h5_base;
+  std::vector<int32_t> h5_tab;
+  std::vector<uint32_t> h5_dpair, h5_gptr, h5_g4;
+  std::vector<uint16_t> h5_gcons;
   roam::DevBuf d_size, d_producer, d_cons_ptr, d_cons_idx, d_in_ptr, d_in_idx, d_out_ptr,
       d_out_idx, d_pred_ptr, d_pred_idx, d_succ_ptr, d_succ_idx;
 };
