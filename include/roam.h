@@ -319,7 +319,8 @@ int rm_set_timing(int enable);
  * v3 pairs / v2, else generic), 1 the generic evaluator, 2 v2 (one candidate
  * per group), 3 v3 (two candidates per group), 4 v4 (sentinel permutation
  * check, SIMD edge checks), 5 v5 (v4's checks, one dynamic class byte per
- * position); unsupported choices fall back.  For tests and A/B measurement. */
+ * position), 6 v5 with rows staged by cp.async.bulk; unsupported choices
+ * fall back.  For tests and A/B measurement. */
 int rm_set_k1_variant(int variant);
 /* Leave `sms` SMs idle in every K1 launch of this process (default 0), so a
  * collective issued on another stream (the multi-GPU selection exchange) runs

@@ -70,7 +70,9 @@ int launch_k1v4(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, in
                 uint8_t* valid, cudaStream_t s, bool u16_rows, const K1KeySel* sel = nullptr);
 
 // K1 v5 (k_eval_v5.cu): same contract; returns 1 when g->k5v.ok == 0.
+// bulk_rows: stage rows with cp.async.bulk instead of the register prefetch.
 int launch_k1v5(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, int32_t* argmax,
-                uint8_t* valid, cudaStream_t s, bool u16_rows, const K1KeySel* sel = nullptr);
+                uint8_t* valid, cudaStream_t s, bool u16_rows, const K1KeySel* sel = nullptr,
+                bool bulk_rows = false);
 
 }  // namespace roam

@@ -493,8 +493,8 @@ int launch_k1(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, int3
               bool* fused = nullptr) {
   if (fused) *fused = false;
   if (B <= 0) return RM_OK;
-  if (g->k5v.ok && (t_force_variant == 0 || t_force_variant == 5)) {
-    const int rc = launch_k1v5(g, orders_dev, B, peak, argmax, valid, s, u16_rows, sel);
+  if (g->k5v.ok && (t_force_variant == 0 || t_force_variant >= 5)) {
+    const int rc = launch_k1v5(g, orders_dev, B, peak, argmax, valid, s, u16_rows, sel, t_force_variant == 6);
     if (rc != 1) {
       if (fused) *fused = sel != nullptr && rc == RM_OK;
       return rc;
@@ -623,7 +623,7 @@ int rm_set_sm_reserve(int sms) {
   return RM_OK;
 }
 int rm_set_k1_variant(int variant) {
-  if (variant < 0 || variant > 5) return fail(RM_ERR_INVALID_ARG, "variant must be 0..5");
+  if (variant < 0 || variant > 6) return fail(RM_ERR_INVALID_ARG, "variant must be 0..6");
   t_force_variant = variant;
   return RM_OK;
 }

@@ -44,8 +44,9 @@ struct K1V5Args {
   const uint32_t* em;  // SIMD edge-mask word per 8-id chunk (shared with v4)
   const uint32_t* edges;
   int n_edges;  // multiple of 4 * NT
-  const uint32_t* dpair;  // two-consumer tensors: a | b << 13 | ia << 26 | ib << 29 (ia / ib:
-  int n_pair;             // the tensor's bit in a's / b's class), padded to a multiple of NT
+  const uint32_t* dpair;  // two-consumer tensors: pos byte offsets 2a | 2b << 16 ...
+  const uint32_t* dtgt;   // ... and class-bit targets ta | tb << 16, t = word | shift << 11
+  int n_pair;             // multiple of NT (padding: target 0xffffffff)
   const uint2* g4;       // 3-4 consumer tensors: four u16 (id | bit index << 13),
   int n_g4;               // a short list repeating its first; multiple of NT, pads 0xe000
   const uint32_t* gptr;   // >= 5 consumer tensors: CSR of consumer id | bit index << 13
@@ -55,11 +56,11 @@ struct K1V5Args {
   int32_t* argmax;
   uint8_t* valid;
   K1KeySel sel;
-  size_t off_ltab, off_edges, off_dpair, off_g4, off_gptr, off_gcons;
-  size_t off_groups, group_bytes, off_cls, off_xc, off_red;
+  size_t off_ltab, off_edges, off_dpair, off_dtgt, off_g4, off_gptr, off_gcons;
+  size_t off_groups, group_bytes, off_cls, off_xc, off_red, off_rbuf, off_mbar;
 };
 
-static constexpr uint32_t K1V5_PAD = 0xfc000000u;  // pair (0, 0), bit indices 7
+static constexpr uint32_t K1V5_PAD = 0xffffffffu;  // padding pair target
 
 template <int C>
 struct V5Geom {
@@ -75,7 +76,10 @@ __device__ __forceinline__ unsigned v5_lds_u16(const unsigned char* base, unsign
 __device__ __forceinline__ unsigned v5_simd_gt(unsigned v, unsigned u, unsigned nm) {
   return ((v | 0x80008000u) - u - 0x00010001u) | nm;
 }
-__host__ __device__ constexpr int v5_cta_cap(int c) { return c >= 32 ? 512 : 1024; }
+// threads per CTA: the register-held row prefetch of the LDG form needs 128
+// registers at C >= 32 (512 threads); the bulk-copy form stages rows in shared
+// memory instead and fits 640
+__host__ __device__ constexpr int v5_cta_cap(int c, bool bulk) { return c >= 32 ? (bulk ? 640 : 512) : 1024; }
 
 template <int NT>
 __device__ __forceinline__ void v5_bar(int id) {
@@ -87,8 +91,8 @@ __device__ __forceinline__ unsigned v5_bar_or(int id, unsigned p) {
   else return (unsigned)gbar_or(id, NT, (int)p);
 }
 
-template <typename RowT, int NT, int C>
-__global__ void __launch_bounds__((v5_cta_cap(C) / NT) * NT, 1) k1v5_eval_orders(const K1V5Args a) {
+template <typename RowT, int NT, int C, bool BULK>
+__global__ void __launch_bounds__((v5_cta_cap(C, BULK) / NT) * NT, 1) k1v5_eval_orders(const K1V5Args a) {
   extern __shared__ __align__(16) unsigned char smem[];
   asm volatile("griddepcontrol.launch_dependents;");
   constexpr int SL = NT * C;
@@ -100,6 +104,7 @@ __global__ void __launch_bounds__((v5_cta_cap(C) / NT) * NT, 1) k1v5_eval_orders
   // positions j*NT + tid with j < JSAFE are always < n: the launcher runs the
   // C >= 32 instances only when n > SL / 2
   constexpr int JSAFE = (C >= 32 && NT >= 64) ? C / 2 : 0;
+  constexpr int PR = C >= 32 ? 6 : C / 4;  // two-consumer tensors per thread kept in registers
   const int n = a.n;
   const RowT* orders = static_cast<const RowT*>(a.orders);
   const int lane = threadIdx.x & 31;
@@ -115,7 +120,10 @@ __global__ void __launch_bounds__((v5_cta_cap(C) / NT) * NT, 1) k1v5_eval_orders
     long long* lt = reinterpret_cast<long long*>(smem + a.off_ltab);
     for (int i = threadIdx.x; i < a.ncls * 32; i += blockDim.x) lt[i] = __ldg(tab + (i >> 5));
     if (a.n_edges > (C / 4) * NT) cp16(a.edges, a.off_edges, 4 * size_t(a.n_edges));
-    if (a.n_pair > (C / 4) * NT) cp16(a.dpair, a.off_dpair, 4 * size_t(a.n_pair));
+    if (a.n_pair > PR * NT) {
+      cp16(a.dpair, a.off_dpair, 4 * size_t(a.n_pair));
+      cp16(a.dtgt, a.off_dtgt, 4 * size_t(a.n_pair));
+    }
     cp16(a.g4, a.off_g4, 8 * size_t(a.n_g4));
     cp16(a.gptr, a.off_gptr, align16(4 * size_t(a.n_gen + 1)));
     cp16(a.gcons, a.off_gcons, align16(2 * size_t(a.n_gcons)));
@@ -126,6 +134,7 @@ __global__ void __launch_bounds__((v5_cta_cap(C) / NT) * NT, 1) k1v5_eval_orders
   const unsigned lane8 = (unsigned)lane * 8u;
   const uint32_t* edges = reinterpret_cast<const uint32_t*>(smem + a.off_edges);
   const uint32_t* dpair = reinterpret_cast<const uint32_t*>(smem + a.off_dpair);
+  const uint32_t* dtgt = reinterpret_cast<const uint32_t*>(smem + a.off_dtgt);
   const uint2* g4 = reinterpret_cast<const uint2*>(smem + a.off_g4);
   const uint32_t* gptr = reinterpret_cast<const uint32_t*>(smem + a.off_gptr);
   const uint16_t* gcons = reinterpret_cast<const uint16_t*>(smem + a.off_gcons);
@@ -152,10 +161,13 @@ __global__ void __launch_bounds__((v5_cta_cap(C) / NT) * NT, 1) k1v5_eval_orders
 #pragma unroll
   for (int i = 0; i < ER; ++i) er[i] = (ereg && i < ek) ? __ldg(a.edges + tid + i * NT) : 0u;
   const int pk = n_pair / NT;
-  const bool preg = pk <= ER;
-  uint32_t pw[ER];
+  const bool preg = pk <= PR;
+  uint32_t pw[PR], pt[PR];
 #pragma unroll
-  for (int i = 0; i < ER; ++i) pw[i] = (preg && i < pk) ? __ldg(a.dpair + tid + i * NT) : 0u;
+  for (int i = 0; i < PR; ++i) {
+    pw[i] = (preg && i < pk) ? __ldg(a.dpair + tid + i * NT) : 0u;
+    pt[i] = (preg && i < pk) ? __ldg(a.dtgt + tid + i * NT) : K1V5_PAD;
+  }
   uint32_t em[QR];
 #pragma unroll
   for (int r = 0; r < QR; ++r) {
@@ -169,8 +181,39 @@ __global__ void __launch_bounds__((v5_cta_cap(C) / NT) * NT, 1) k1v5_eval_orders
   // has NT % C == 0, so that is xc0 + j * (NT / C) * XS (immediate offsets)
   static_assert(NT % C == 0, "v5 geometry: NT must be a multiple of C");
   unsigned char* const xc0 = xc + (tid / C) * XS + (tid % C);
+  // BULK: the group's row buffer and its mbarrier; rows arrive by
+  // cp.async.bulk (one elected thread issues, the copy engine writes shared
+  // memory), so no register holds a prefetched row
+  const unsigned rbuf_s = (unsigned)__cvta_generic_to_shared(gbase + a.off_rbuf);
+  const unsigned mbar_s = (unsigned)__cvta_generic_to_shared(gbase + a.off_mbar);
+  if (BULK && tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar_s) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   v5_bar<NT>(bar_id);
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  constexpr int ES = (int)sizeof(RowT);
+  const uintptr_t ord0 = reinterpret_cast<uintptr_t>(orders);
+  const uintptr_t ord_end16 = (ord0 + uintptr_t(a.B) * uintptr_t(n) * ES) & ~uintptr_t(15);
+  // the 16-byte-aligned span holding row cc (never past the batch's last
+  // aligned byte: a row's last elements beyond it are read from global)
+  auto span = [&](int64_t cc, uintptr_t& a0, unsigned& bytes) {
+    const uintptr_t g0 = ord0 + uintptr_t(cc) * uintptr_t(n) * ES;
+    a0 = g0 & ~uintptr_t(15);
+    uintptr_t a1 = (g0 + uintptr_t(n) * ES + 15) & ~uintptr_t(15);
+    if (a1 > ord_end16) a1 = ord_end16 > a0 ? ord_end16 : a0;
+    bytes = (unsigned)(a1 - a0);
+  };
+  auto issue = [&](int64_t cc) {  // one thread of the group
+    uintptr_t a0;
+    unsigned bytes;
+    span(cc, a0, bytes);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar_s), "r"(bytes) : "memory");
+    if (bytes)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(rbuf_s), "l"(a0), "r"(bytes), "r"(mbar_s) : "memory");
+  };
+  unsigned phase = 0;
 
   uint32_t v[C];
   auto load_row = [&](int64_t cc) {
@@ -187,8 +230,37 @@ __global__ void __launch_bounds__((v5_cta_cap(C) / NT) * NT, 1) k1v5_eval_orders
   };
   long long kbest = LLONG_MAX;
   int64_t c = int64_t(blockIdx.x) * a.G + gid;
-  if (c < a.B) load_row(c);
+  if (c < a.B) {
+    if constexpr (BULK) {
+      if (tid == 0) issue(c);
+    } else {
+      load_row(c);
+    }
+  }
   for (; c < a.B; c += cstride) {
+    if constexpr (BULK) {  // this candidate's row: wait for its copy, read it
+      asm volatile(
+          "{\n\t.reg .pred p;\n\t"
+          "W%=:\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+          "@!p bra W%=;\n\t}" ::"r"(mbar_s), "r"(phase) : "memory");
+      phase ^= 1u;
+      uintptr_t a0;
+      unsigned bytes;
+      span(c, a0, bytes);
+      const uintptr_t g0 = ord0 + uintptr_t(c) * uintptr_t(n) * ES;
+      const int head = (int)((g0 - a0) / ES);
+      const int ncop = (int)((a0 + bytes - g0) / ES);  // elements in the buffer
+      const RowT* rb = reinterpret_cast<const RowT*>(gbase + a.off_rbuf) + head;
+      const RowT* row = orders + c * int64_t(n);
+#pragma unroll
+      for (int j = 0; j < C; ++j) {
+        const int k = tid + j * NT;
+        // padding slots k >= n hold op id k (the span may run past the row)
+        v[j] = j < JSAFE ? (uint32_t)rb[k]
+                         : (k < n ? (k < ncop ? (uint32_t)rb[k] : (uint32_t)__ldcs(row + k)) : (uint32_t)k);
+      }
+    }
     // ---- P1: restore this candidate's class bytes; scatter positions
 #pragma unroll
     for (int r = 0; r < QR; ++r) {
@@ -202,6 +274,12 @@ __global__ void __launch_bounds__((v5_cta_cap(C) / NT) * NT, 1) k1v5_eval_orders
       pos[v[j]] = (uint16_t)(tid + j * NT);
     }
     v5_bar<NT>(bar_id);
+    if constexpr (BULK) {  // every thread has read the row buffer: refill it
+      if (tid == 0 && c + cstride < a.B) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(c + cstride);
+      }
+    }
     // ---- P2 (id-major): missing ids (sentinel) and the (u, u+1), (u, u+2) edges
     unsigned sent = 0, ok = 0xffffffffu;
 #pragma unroll
@@ -244,30 +322,28 @@ __global__ void __launch_bounds__((v5_cta_cap(C) / NT) * NT, 1) k1v5_eval_orders
     // ---- P2: multi-consumer tensors: the latest maximal consumer's class
     // byte gains the tensor's bit (positions of a broken row may be the
     // sentinel; the bits stay in range either way)
-    // pair word w: a | b << 13 | ia << 26 | ib << 29
-    // (padding slots name id 0 twice with bit indices 7: a = b marks them,
-    // their lanes are predicated off)
-    auto pair_free = [&](uint32_t w, unsigned pa, unsigned pbv) {
-      const bool bw = pbv > pa;
-      if (w != K1V5_PAD)
-        add_bit(bw ? ((w >> 13) & 0x1fffu) : (w & 0x1fffu), 1u << (bw ? (w >> 29) : ((w >> 26) & 7u)));
+    // pair (a, b): the later consumer's class byte gains the tensor's bit;
+    // the target half t = class word | bit shift << 11 is picked by one PRMT
+    auto pair_free = [&](uint32_t t2, unsigned pa, unsigned pbv) {
+      const unsigned t = __byte_perm(t2, 0u, pbv > pa ? 0x4432u : 0x4410u);
+      if (t2 != K1V5_PAD)
+        atomicAdd(reinterpret_cast<unsigned*>(clsp) + (t & 0x7ffu), 1u << (t >> 11));
     };
     int m_first = tid;
     if (preg) {
-      unsigned pa[ER], pbv[ER];
+      unsigned pa[PR], pbv[PR];
 #pragma unroll
-      for (int i = 0; i < ER; ++i) {
-        pa[i] = pos[pw[i] & 0x1fffu];
-        pbv[i] = pos[(pw[i] >> 13) & 0x1fffu];
+      for (int i = 0; i < PR; ++i) {
+        pa[i] = v5_lds_u16(posb, pw[i] & 0xffffu);
+        pbv[i] = v5_lds_u16(posb, pw[i] >> 16);
       }
 #pragma unroll
-      for (int i = 0; i < ER; ++i)
-        if (i < pk) pair_free(pw[i], pa[i], pbv[i]);
+      for (int i = 0; i < PR; ++i) pair_free(pt[i], pa[i], pbv[i]);
       m_first = n_pair;
     }
     for (int m = m_first; m < n_pair; m += NT) {
       const uint32_t w = dpair[m];
-      pair_free(w, pos[w & 0x1fffu], pos[(w >> 13) & 0x1fffu]);
+      pair_free(dtgt[m], v5_lds_u16(posb, w & 0xffffu), v5_lds_u16(posb, w >> 16));
     }
     for (int m = tid; m < n_g4; m += NT) {
       const uint2 e = g4[m];
@@ -303,8 +379,10 @@ __global__ void __launch_bounds__((v5_cta_cap(C) / NT) * NT, 1) k1v5_eval_orders
       if (QFULL || q < Q)
         *reinterpret_cast<uint4*>(pos + 8 * q) = make_uint4(0x80008000u, 0x80008000u, 0x80008000u, 0x80008000u);
     }
-    const int64_t cn = c + cstride;
-    if (cn < a.B) load_row(cn);
+    if constexpr (!BULK) {
+      const int64_t cn = c + cstride;
+      if (cn < a.B) load_row(cn);
+    }
     v5_bar<NT>(bar_id);
     // ---- P4: blocked scan over this thread's C positions
     const int k0 = tid * C;
@@ -431,9 +509,9 @@ __global__ void __launch_bounds__((v5_cta_cap(C) / NT) * NT, 1) k1v5_eval_orders
   }
 }
 
-template <typename RowT, int NT, int C>
+template <typename RowT, int NT, int C, bool BULK>
 static int launch_k1v5_t(K1V5Args& a, int grid, size_t smem, cudaStream_t s) {
-  auto kern = k1v5_eval_orders<RowT, NT, C>;
+  auto kern = k1v5_eval_orders<RowT, NT, C, BULK>;
   RM_CUDA(smem_optin(kern));
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (g_timing) {
@@ -468,9 +546,11 @@ static int launch_k1v5_t(K1V5Args& a, int grid, size_t smem, cudaStream_t s) {
 // the instance table must list every (NT, C) k1v4_geometry (roam_graph.cpp)
 // picks for a class-form graph
 template <typename RowT>
-static int launch_k1v5_nt(K1V5Args& a, int NT, int C, int grid, size_t smem, cudaStream_t s) {
-#define RM_K1V5_CASE(nt, cc) \
-  if (NT == nt && C == cc) return launch_k1v5_t<RowT, nt, cc>(a, grid, smem, s);
+static int launch_k1v5_nt(K1V5Args& a, int NT, int C, bool bulk, int grid, size_t smem, cudaStream_t s) {
+#define RM_K1V5_CASE(nt, cc)                                                      \
+  if (NT == nt && C == cc)                                                        \
+    return bulk ? launch_k1v5_t<RowT, nt, cc, true>(a, grid, smem, s)             \
+                : launch_k1v5_t<RowT, nt, cc, false>(a, grid, smem, s);
   RM_K1V5_CASE(32, 4)
   RM_K1V5_CASE(32, 8)
   RM_K1V5_CASE(64, 8)
@@ -485,7 +565,7 @@ static int launch_k1v5_nt(K1V5Args& a, int NT, int C, int grid, size_t smem, cud
 }
 
 int launch_k1v5(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, int32_t* argmax,
-                uint8_t* valid, cudaStream_t s, bool u16_rows, const K1KeySel* sel) {
+                uint8_t* valid, cudaStream_t s, bool u16_rows, const K1KeySel* sel, bool bulk_rows) {
   const K1V5Meta& m = g->k5v;
   const K1V4Meta& m4 = g->k4v;
   if (!m.ok || !m4.ok) return 1;
@@ -502,6 +582,7 @@ int launch_k1v5(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, in
   a.edges = m4.edges.as<uint32_t>();
   a.n_edges = (int)m4.n_edges;
   a.dpair = m.dpair.as<uint32_t>();
+  a.dtgt = m.dtgt.as<uint32_t>();
   a.n_pair = (int)m.n_pair;
   a.g4 = m.g4.as<uint2>();
   a.n_g4 = (int)m.n_g4;
@@ -519,17 +600,28 @@ int launch_k1v5(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, in
   a.off_ltab = align16(size_t(SL + 16));
   a.off_edges = a.off_ltab + 256 * size_t(a.ncls);
   a.off_dpair = align16(a.off_edges + 4 * size_t(a.n_edges));
-  a.off_g4 = align16(a.off_dpair + 4 * size_t(a.n_pair));
+  a.off_dtgt = align16(a.off_dpair + 4 * size_t(a.n_pair));
+  a.off_g4 = align16(a.off_dtgt + 4 * size_t(a.n_pair));
   a.off_gptr = align16(a.off_g4 + 8 * size_t(a.n_g4));
   a.off_gcons = align16(a.off_gptr + 4 * size_t(a.n_gen + 1));
   a.off_groups = align16(a.off_gcons + 2 * size_t(a.n_gcons));
   a.off_cls = align16(2 * size_t(SL + 8));
   a.off_xc = align16(a.off_cls + size_t(SL + 16));
   a.off_red = align16(a.off_xc + size_t(NT) * xs);
-  a.group_bytes = align16(a.off_red + 3 * 8 * size_t(NT / 32) + 16);
   if (C >= 32 && NT >= 64 && a.n <= SL / 2) return 1;  // the kernel's JSAFE
+  // bulk-copied rows (rm_set_k1_variant(6); C >= 32 geometries): the first
+  // half of a row must lie in the copied span (n >= SL/2 + 8).  Measured
+  // slower than the register prefetch on GPT-2 small (0.0735 vs 0.0670 ms per
+  // 16k candidates): 640 threads at 96 registers raise warps per SM 24 -> 30 %,
+  // but the kernel is issue-bound and the shared-memory reads of the staged
+  // row add 14 % instructions
+  const bool bulk = bulk_rows && C >= 32 && NT >= 64 && a.n >= SL / 2 + 8;
+  const int esz = u16_rows ? 2 : 4;
+  a.off_rbuf = align16(a.off_red + 3 * 8 * size_t(NT / 32) + 16);
+  a.off_mbar = bulk ? align16(a.off_rbuf + size_t(esz) * a.n + 32) : a.off_rbuf;
+  a.group_bytes = bulk ? align16(a.off_mbar + 8) : a.off_rbuf;
   const size_t avail = max_smem > (int)a.off_groups ? size_t(max_smem) - a.off_groups : 0;
-  const int cap = (C >= 32 ? 512 : 1024) / NT;
+  const int cap = v5_cta_cap(C, bulk) / NT;
   int G = std::min({(int)(avail / a.group_bytes), cap, 15});
   if (G < 1) return 1;
   const int64_t sms = k1_sms(g->device);
@@ -537,8 +629,8 @@ int launch_k1v5(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, in
   a.G = G;
   const size_t smem = a.off_groups + size_t(G) * a.group_bytes;
   const int grid = (int)std::min<int64_t>(sms, (B + G - 1) / G);
-  return u16_rows ? launch_k1v5_nt<uint16_t>(a, NT, C, grid, smem, s)
-                  : launch_k1v5_nt<int32_t>(a, NT, C, grid, smem, s);
+  return u16_rows ? launch_k1v5_nt<uint16_t>(a, NT, C, bulk, grid, smem, s)
+                  : launch_k1v5_nt<int32_t>(a, NT, C, bulk, grid, smem, s);
 }
 
 }  // namespace roam

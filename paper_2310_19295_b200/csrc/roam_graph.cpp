@@ -322,7 +322,10 @@ static void build_k1v5_host(RmGraph& g) {
   auto idx_of = [&](int v, int t) {
     return (uint32_t)(std::find(dyn[v].begin(), dyn[v].end(), t) - dyn[v].begin());
   };
-  std::vector<uint32_t> pw;
+  std::vector<uint32_t> pw, pt;
+  auto target = [&](int v, int t) {  // class word of v | bit shift << 11
+    return (uint32_t)(v >> 2) | ((uint32_t)(8 * (v & 3)) + idx_of(v, t)) << 11;
+  };
   g.h5_gptr.assign(1, 0);
   g.h5_gcons.clear();
   g.h5_g4.clear();
@@ -330,7 +333,8 @@ static void build_k1v5_host(RmGraph& g) {
     const int q0 = g.h_mptr[m], q1 = g.h_mptr[m + 1];
     if (q1 - q0 == 2) {
       const int a = g.h_mcons[q0], b = g.h_mcons[q0 + 1];
-      pw.push_back((uint32_t)a | ((uint32_t)b << 13) | (idx_of(a, (int)m) << 26) | (idx_of(b, (int)m) << 29));
+      pw.push_back((uint32_t)(2 * a) | ((uint32_t)(2 * b) << 16));
+      pt.push_back(target(a, (int)m) | (target(b, (int)m) << 16));
     } else if (q1 - q0 <= 4) {
       uint32_t e[4];
       for (int q = q0; q < q0 + 4; ++q) {
@@ -350,14 +354,18 @@ static void build_k1v5_host(RmGraph& g) {
   while ((g.h5_g4.size() / 2) % NT) g.h5_g4.push_back(0xe000e000u);
   // lane interleave: slot tid + i*NT holds pair tid*pk + i, so the lanes of a
   // warp touch pairs pk apart (nearby pairs share class-byte words, and
-  // same-word atomics from one instruction serialise); padding slots hold
-  // pair (0, 0) with bit indices 7 (0xfc000000), which the kernel predicates off
+  // same-word atomics from one instruction serialise); padding slots read
+  // pos[0] and hold target 0xffffffff, which the kernel predicates off
   const size_t P = pw.size(), pk = (P + NT - 1) / NT;
-  g.h5_dpair.assign(pk * NT, 0xfc000000u);
+  g.h5_dpair.assign(pk * NT, 0u);
+  g.h5_dtgt.assign(pk * NT, 0xffffffffu);
   for (size_t i = 0; i < pk; ++i)
     for (int t = 0; t < NT; ++t) {
       const size_t src = size_t(t) * pk + i, dst = size_t(t) + i * NT;
-      if (src < P) g.h5_dpair[dst] = pw[src];
+      if (src < P) {
+        g.h5_dpair[dst] = pw[src];
+        g.h5_dtgt[dst] = pt[src];
+      }
     }
   g.h5_base = base;
   g.h5_tab = tab;
@@ -664,6 +672,7 @@ int rm_graph_create(const RmGraphDesc* d, uint32_t flags, RmGraph** out) {
     if (!e && g->k5v.ok) e = up(g->k5v.base, g->h5_base);
     if (!e && g->k5v.ok) e = up(g->k5v.tab, g->h5_tab);
     if (!e && g->k5v.ok) e = up(g->k5v.dpair, g->h5_dpair);
+    if (!e && g->k5v.ok) e = up(g->k5v.dtgt, g->h5_dtgt);
     if (!e && g->k5v.ok) e = up(g->k5v.g4, g->h5_g4);
     if (!e && g->k5v.ok) e = up(g->k5v.gptr, g->h5_gptr);
     if (!e && g->k5v.ok) e = up(g->k5v.gcons, g->h5_gcons);

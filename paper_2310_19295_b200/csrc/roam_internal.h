@@ -140,10 +140,11 @@ struct K1V4Meta {
 // than 255 classes or an op has more than 7 multi-consumer tensors.
 //   base  = base class per id [SL + 16] (padding ids and the sink: a zero class)
 //   tab   = int2 {fs, out} units per class [ncls]
-//   dpair = two-consumer tensors a | b << 13 | ia << 26 | ib << 29 (ia / ib:
-//           the tensor's bit index in a's / b's class); lane-interleaved (slot
-//           tid + i*NT holds the thread's i-th pair, consecutive lanes far
-//           apart) and padded to a multiple of NT with 0xfc000000 (pair (0, 0))
+//   dpair = two-consumer tensors as pos byte offsets 2a | 2b << 16, dtgt =
+//           their class-bit targets ta | tb << 16 (t = class word index |
+//           (8 * (id & 3) + bit index) << 11); lane-interleaved (slot tid +
+//           i*NT holds the thread's i-th pair, consecutive lanes far apart),
+//           padded to a multiple of NT with target 0xffffffff
 //   g4    = the 3-4 consumer tensors, four u16 (id | bit index << 13) each
 //           (a short list repeats its first entry), padded to a multiple of
 //           NT with 0xe000 entries
@@ -152,7 +153,7 @@ struct K1V5Meta {
   int ok = 0;
   int ncls = 0;
   int64_t n_pair = 0, n_g4 = 0, n_gen = 0, n_gcons = 0;
-  DevBuf base, tab, dpair, g4, gptr, gcons;
+  DevBuf base, tab, dpair, dtgt, g4, gptr, gcons;
 };
 
 }  // namespace roam
@@ -185,7 +186,7 @@ struct RmGraph {
   std::vector<int32_t> h4_tab;
   std::vector<uint8_t> h5_base;
   std::vector<int32_t> h5_tab;
-  std::vector<uint32_t> h5_dpair, h5_gptr, h5_g4;
+  std::vector<uint32_t> h5_dpair, h5_dtgt, h5_gptr, h5_g4;
   std::vector<uint16_t> h5_gcons;
   roam::DevBuf d_size, d_producer, d_cons_ptr, d_cons_idx, d_in_ptr, d_in_idx, d_out_ptr,
       d_out_idx, d_pred_ptr, d_pred_idx, d_succ_ptr, d_succ_idx;

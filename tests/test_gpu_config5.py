@@ -46,7 +46,7 @@ def test_gpt2xl_chunk_three_ways():
     host = orders.cpu().numpy()
     host[::101] = host[::101][:, ::-1]                 # invalid rows mixed in
     want = coracle.eval_orders(coracle.CGraph(g), host)
-    for variant in (5, 4):
+    for variant in (5, 6, 4):
         ev.set_k1_variant(variant)
         try:
             p, a, v = (x.cpu().numpy() for x in ev.evaluate_orders(g, orders.new_tensor(host)))

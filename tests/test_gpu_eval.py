@@ -138,7 +138,7 @@ def test_reference_unit_answers_through_gpu():
         sequential_schedule(d, (3, 0, 1, 2))
 
 
-@pytest.mark.parametrize("variant", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("variant", [1, 2, 3, 4, 5, 6])
 @pytest.mark.parametrize("name", ["layered", "gpt2-small", "bert-large", "gpt2-xl"])
 def test_both_k1_variants_vs_c_oracle(name, variant):
     """Every K1 variant -- v5 (dynamic class bytes, the default on the training
@@ -210,7 +210,7 @@ def test_packed_key_selection_matches_first_strict_min():
     assert decode_key(none, bits) == (2**63 - 1, -1)
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6])
 def test_uint16_rows_match_int32(variant):
     """uint16 rows (RM_ORDERS_U16) give exactly the int32 results on every
     evaluator, host-staged and device-resident."""
@@ -285,7 +285,7 @@ def test_random_hazard_graphs_vs_oracle(seed):
                     assert (int(peak[k]), int(arg[k])) == want[:2], (seed, trial, variant, row)
 
 
-@pytest.mark.parametrize("variant", [0, 2, 4])
+@pytest.mark.parametrize("variant", [0, 2, 4, 6])
 @pytest.mark.parametrize("name", ["layered", "gpt2-small", "bert-large", "gpt2-xl"])
 def test_fused_key_selection(name, variant):
     """K1 with the packed-key selection fused into the launch (v4) or chained
