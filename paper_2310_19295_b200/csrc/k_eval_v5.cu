@@ -56,7 +56,7 @@ struct K1V5Args {
   int32_t* argmax;
   uint8_t* valid;
   K1KeySel sel;
-  size_t off_ltab, off_edges, off_dpair, off_dtgt, off_g4, off_gptr, off_gcons;
+  size_t off_base, off_edges, off_dpair, off_dtgt, off_g4, off_gptr, off_gcons;
   size_t off_groups, group_bytes, off_cls, off_xc, off_red, off_rbuf, off_mbar;
 };
 
@@ -114,10 +114,10 @@ __global__ void __launch_bounds__((v5_cta_cap(C, BULK) / NT) * NT, 1) k1v5_eval_
       uint4* dst = reinterpret_cast<uint4*>(smem + off);
       for (size_t i = threadIdx.x; i < bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
     };
-    cp16(a.base, 0, align16(size_t(SL + 16)));
+    cp16(a.base, a.off_base, align16(size_t(SL + 16)));
     // lane-replicated class table: entry (c, l) at ltab[c * 32 + l]
     const long long* tab = static_cast<const long long*>(a.tab);
-    long long* lt = reinterpret_cast<long long*>(smem + a.off_ltab);
+    long long* lt = reinterpret_cast<long long*>(smem);
     for (int i = threadIdx.x; i < a.ncls * 32; i += blockDim.x) lt[i] = __ldg(tab + (i >> 5));
     if (a.n_edges > (C / 4) * NT) cp16(a.edges, a.off_edges, 4 * size_t(a.n_edges));
     if (a.n_pair > PR * NT) {
@@ -129,8 +129,10 @@ __global__ void __launch_bounds__((v5_cta_cap(C, BULK) / NT) * NT, 1) k1v5_eval_
     cp16(a.gcons, a.off_gcons, align16(2 * size_t(a.n_gcons)));
   }
   __syncthreads();
-  const uint8_t* base8 = smem;
-  const unsigned char* ltab_b = smem + a.off_ltab;  // entry (c, l) at byte c * 256 + l * 8
+  const uint8_t* base8 = smem + a.off_base;
+  // the class table sits at the start of shared memory: entry (c, l) at byte
+  // c * 256 + l * 8, so a lookup is [PRMT result + the window base]
+  const unsigned char* ltab_b = smem;
   const unsigned lane8 = (unsigned)lane * 8u;
   const uint32_t* edges = reinterpret_cast<const uint32_t*>(smem + a.off_edges);
   const uint32_t* dpair = reinterpret_cast<const uint32_t*>(smem + a.off_dpair);
@@ -597,8 +599,8 @@ int launch_k1v5(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, in
   const int xs = C >= 32 ? C + 16 : C == 16 ? 48 : C;  // V5Geom<C>::XS
   int max_smem = 0;
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device);
-  a.off_ltab = align16(size_t(SL + 16));
-  a.off_edges = a.off_ltab + 256 * size_t(a.ncls);
+  a.off_base = 256 * size_t(a.ncls);
+  a.off_edges = align16(a.off_base + size_t(SL + 16));
   a.off_dpair = align16(a.off_edges + 4 * size_t(a.n_edges));
   a.off_dtgt = align16(a.off_dpair + 4 * size_t(a.n_pair));
   a.off_g4 = align16(a.off_dtgt + 4 * size_t(a.n_pair));
