@@ -206,6 +206,32 @@ def ncu_traffic(config: str, batch: int):
     return None
 
 
+def parity_probe(ev, coracle, cores: int) -> dict:
+    """Bit-exact check of K1 on a graph whose candidates are NOT degenerate:
+    the training graphs' counter-RNG candidates mostly share one peak (GPT-2
+    small: 1 distinct peak in 4,096), the layered DAG's spread over hundreds.
+    4,096 layered candidates plus every 7th one corrupted (a swap: mostly
+    invalid), GPU against the C oracle: peaks, argmax and validity."""
+    import numpy as np
+    g = graph_for("layered")
+    S = 4096
+    rows = ev.generate_orders(g, 0, 0, S).cpu().numpy()
+    rng = np.random.default_rng(1)
+    for r in range(0, S, 7):
+        i, j = rng.integers(0, rows.shape[1], 2)
+        rows[r, [i, j]] = rows[r, [j, i]]
+    gp, ga, gv = ev.evaluate_orders(g, rows)
+    want = coracle.eval_orders(coracle.CGraph(g), rows, threads=cores)
+    ok = bool(np.array_equal(gv, want[2]) and np.array_equal(gp[gv], want[0][want[2]])
+              and np.array_equal(ga[gv], want[1][want[2]]))
+    if not ok:
+        raise SystemExit("GPU results differ from the CPU oracle on the layered parity probe")
+    return {"layered": {"sample": S, "corrupted": len(range(0, S, 7)), "bit_exact": ok,
+                        "valid": int(want[2].sum()),
+                        "distinct_peaks": int(len(np.unique(want[0][want[2]]))),
+                        "distinct_argmax": int(len(np.unique(want[1][want[2]])))}}
+
+
 # ------------------------------------------------------------ reference arm
 
 def run_reference(args) -> None:
@@ -216,8 +242,9 @@ def run_reference(args) -> None:
     g = graph_for(args.config)
     cg = coracle.CGraph(g)
     cores = os.cpu_count() or 1
-    # bounded sample of the same workload (same candidate ids as rank 0)
-    sample = 2048
+    # the same workload as our arm's N=1 line: the same candidate ids
+    # (rank 0's [0, B)), every step
+    sample = args.batch or DEFAULT_BATCH[args.config]
     orders = coracle.kahn_orders(cg, 0, 0, sample, threads=cores)
     for _ in range(max(args.warmup, 1)):
         coracle.eval_orders(cg, orders, threads=cores)
@@ -232,8 +259,9 @@ def run_reference(args) -> None:
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": f"{WORKLOAD[args.config]}: bounded sample of {sample} per step",
-                   "graph": args.config, "n_ops": cg.n, "n_tensors": cg.T},
+        "config": {"workload": f"{WORKLOAD[args.config]}: {sample} per GPU", "graph": args.config,
+                   "n_ops": cg.n, "n_tensors": cg.T, "candidates_per_gpu": sample,
+                   "candidate_ids": f"rank r evaluates [r*{sample}, (r+1)*{sample})"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": f"{sample} counter-RNG Kahn candidates (seed 0, ids 0..{sample - 1}) "
                                    f"per step; oracle/peak_oracle.c restating graph.py:375-468, "
@@ -497,6 +525,11 @@ def main() -> None:
                "sample": f"first {S} of this run's candidates, repeated for >= {args.cpu_seconds:g} s "
                          f"wall; oracle/peak_oracle.c restating graph.py:375-468 on {cores} pthreads; "
                          f"bit-exact parity with the GPU results on the sample: {parity}"}
+        parity_info = {args.config: {
+            "sample": S, "bit_exact": parity, "valid": int(want[2].sum()),
+            "distinct_peaks": int(len(np.unique(want[0][want[2]]))),
+            "distinct_argmax": int(len(np.unique(want[1][want[2]])))}}
+        parity_info.update(parity_probe(ev, coracle, cores))
 
     if rank == 0:
         line = {
@@ -537,6 +570,7 @@ def main() -> None:
         }
         if cpu is not None:
             line["cpu_baseline"] = cpu
+            line["parity"] = parity_info
             pyref = reference_python(args.config, host_np, hp, ha, min(args.cpu_seconds, 3.0))
             if pyref is not None:
                 line["reference_python"] = pyref

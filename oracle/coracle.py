@@ -35,6 +35,8 @@ def _load():
         _lib.oracle_eval_orders.restype = C.c_int
         _lib.oracle_eval_orders.argtypes = [C.c_int, C.c_int] + [C.c_void_p] * 7 + [
             C.c_int64, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
+        _lib.oracle_eval_orders_events.restype = C.c_int
+        _lib.oracle_eval_orders_events.argtypes = _lib.oracle_eval_orders.argtypes
         _lib.oracle_kahn_orders.restype = C.c_int
         _lib.oracle_kahn_orders.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64,
                                             C.c_int64, C.c_int64, C.c_int, C.c_void_p]
@@ -73,15 +75,19 @@ class CGraph:
         self.succ_idx = np.array([w for s in succs for w in s], np.int32)
 
 
-def eval_orders(cg: CGraph, orders: np.ndarray, threads: int | None = None):
-    """(peak int64[B], argmax int32[B], valid bool[B]); invalid rows peak 0."""
+def eval_orders(cg: CGraph, orders: np.ndarray, threads: int | None = None, events: bool = False):
+    """(peak int64[B], argmax int32[B], valid bool[B]); invalid rows peak 0.
+    events=True: lifetimes as a +size/-size event sweep (same results, O(n+T+E)
+    per row) for checking million-row batches; the default keeps the
+    reference's per-step add loop (graph.py:452-458)."""
     L = _load()
     o = np.ascontiguousarray(orders, dtype=np.int32)
     B = o.shape[0]
     peak = np.empty(B, np.int64)
     arg = np.empty(B, np.int32)
     val = np.empty(B, np.uint8)
-    L.oracle_eval_orders(cg.n, cg.T, _p(cg.size), _p(cg.producer), _p(cg.cons_ptr), _p(cg.cons_idx),
+    fn = L.oracle_eval_orders_events if events else L.oracle_eval_orders
+    fn(cg.n, cg.T, _p(cg.size), _p(cg.producer), _p(cg.cons_ptr), _p(cg.cons_idx),
                          _p(cg.pred_ptr), _p(cg.pred_idx), _p(o), B, threads or os.cpu_count() or 1,
                          _p(peak), _p(arg), _p(val))
     return peak, arg, val.astype(bool)

@@ -34,6 +34,7 @@ typedef struct {
   int64_t* peak;
   int32_t* argmax;
   uint8_t* valid;
+  int events;
 } Job;
 
 static void eval_range(Job* j) {
@@ -81,15 +82,67 @@ static void eval_range(Job* j) {
   free(live);
 }
 
+/* The same function for large-batch checking: identical validation, then the
+ * lifetimes as +size / -size events (a difference array) instead of the
+ * reference's per-step add loop -- O(n + T + E) per candidate.  Checked
+ * against eval_range row for row (tests/test_oracle_golden.py). */
+static void eval_range_events(Job* j) {
+  const int n = j->n, T = j->T;
+  int32_t* pos = (int32_t*)malloc(sizeof(int32_t) * (n ? n : 1));
+  int64_t* diff = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n + 1));
+  for (int64_t b = j->b0; b < j->b1; ++b) {
+    const int32_t* o = j->orders + b * (int64_t)n;
+    int ok = 1;
+    for (int v = 0; v < n; ++v) pos[v] = -1;
+    for (int i = 0; i < n && ok; ++i) {
+      int v = o[i];
+      if (v < 0 || v >= n || pos[v] >= 0) ok = 0;
+      else pos[v] = i;
+    }
+    for (int v = 0; v < n && ok; ++v)
+      for (int k = j->pred_ptr[v]; k < j->pred_ptr[v + 1]; ++k)
+        if (pos[j->pred_idx[k]] > pos[v]) { ok = 0; break; }
+    j->valid[b] = (uint8_t)ok;
+    if (!ok || n == 0) {
+      j->peak[b] = 0;
+      j->argmax[b] = 0;
+      continue;
+    }
+    memset(diff, 0, sizeof(int64_t) * (size_t)(n + 1));
+    for (int t = 0; t < T; ++t) {
+      int birth = pos[j->producer[t]];
+      int death = -1;
+      for (int k = j->cons_ptr[t]; k < j->cons_ptr[t + 1]; ++k)
+        if (pos[j->cons_idx[k]] > death) death = pos[j->cons_idx[k]];
+      if (j->cons_ptr[t] == j->cons_ptr[t + 1]) death = n - 1;
+      if (death < birth) death = birth;
+      diff[birth] += j->size[t];
+      diff[death + 1] -= j->size[t];
+    }
+    int64_t live = diff[0], best = diff[0];
+    int arg = 0;
+    for (int s = 1; s < n; ++s) {
+      live += diff[s];
+      if (live > best) { best = live; arg = s; }
+    }
+    j->peak[b] = best;
+    j->argmax[b] = arg;
+  }
+  free(pos);
+  free(diff);
+}
+
 static void* worker(void* p) {
-  eval_range((Job*)p);
+  if (((Job*)p)->events) eval_range_events((Job*)p);
+  else eval_range((Job*)p);
   return NULL;
 }
 
-int oracle_eval_orders(int n, int T, const int64_t* size, const int32_t* producer,
-                       const int32_t* cons_ptr, const int32_t* cons_idx, const int32_t* pred_ptr,
-                       const int32_t* pred_idx, const int32_t* orders, int64_t B, int threads,
-                       int64_t* peak, int32_t* argmax, uint8_t* valid) {
+static int eval_orders_impl(int n, int T, const int64_t* size, const int32_t* producer,
+                            const int32_t* cons_ptr, const int32_t* cons_idx,
+                            const int32_t* pred_ptr, const int32_t* pred_idx,
+                            const int32_t* orders, int64_t B, int threads, int64_t* peak,
+                            int32_t* argmax, uint8_t* valid, int events) {
   if (threads < 1) threads = 1;
   if (threads > B) threads = B > 0 ? (int)B : 1;
   Job* jobs = (Job*)calloc((size_t)threads, sizeof(Job));
@@ -99,15 +152,34 @@ int oracle_eval_orders(int n, int T, const int64_t* size, const int32_t* produce
     j->n = n; j->T = T; j->size = size; j->producer = producer;
     j->cons_ptr = cons_ptr; j->cons_idx = cons_idx; j->pred_ptr = pred_ptr; j->pred_idx = pred_idx;
     j->orders = orders; j->peak = peak; j->argmax = argmax; j->valid = valid;
+    j->events = events;
     j->b0 = B * k / threads;
     j->b1 = B * (k + 1) / threads;
   }
   for (int k = 1; k < threads; ++k) pthread_create(&th[k], NULL, worker, &jobs[k]);
-  eval_range(&jobs[0]);
+  worker(&jobs[0]);
   for (int k = 1; k < threads; ++k) pthread_join(th[k], NULL);
   free(jobs);
   free(th);
   return 0;
+}
+
+int oracle_eval_orders(int n, int T, const int64_t* size, const int32_t* producer,
+                       const int32_t* cons_ptr, const int32_t* cons_idx, const int32_t* pred_ptr,
+                       const int32_t* pred_idx, const int32_t* orders, int64_t B, int threads,
+                       int64_t* peak, int32_t* argmax, uint8_t* valid) {
+  return eval_orders_impl(n, T, size, producer, cons_ptr, cons_idx, pred_ptr, pred_idx, orders, B,
+                          threads, peak, argmax, valid, 0);
+}
+
+/* oracle_eval_orders with the event-sweep lifetimes (same results). */
+int oracle_eval_orders_events(int n, int T, const int64_t* size, const int32_t* producer,
+                              const int32_t* cons_ptr, const int32_t* cons_idx,
+                              const int32_t* pred_ptr, const int32_t* pred_idx,
+                              const int32_t* orders, int64_t B, int threads, int64_t* peak,
+                              int32_t* argmax, uint8_t* valid) {
+  return eval_orders_impl(n, T, size, producer, cons_ptr, cons_idx, pred_ptr, pred_idx, orders, B,
+                          threads, peak, argmax, valid, 1);
 }
 
 /* ------------------------------------------------------------------------

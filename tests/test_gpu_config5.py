@@ -21,13 +21,29 @@ pytestmark = pytest.mark.gpu
 
 
 def test_config5_full_size_one_gpu():
+    """All 1,048,576 candidates: every GPU (peak, argmax, valid) equals the C
+    oracle's (event-sweep mode, every host core) row for row, and the sharded
+    search's answer is the first strict minimum over the whole id range
+    (tests/oracles.py:46-56; planner.py:209-216)."""
     g = load_graph(gg.config_doc("gpt2-xl"))
-    total = 1 << 20
-    res = evaluate_sharded(g, total, seed=0, chunk=1 << 16)
+    total, chunk = 1 << 20, 1 << 16
+    res = evaluate_sharded(g, total, seed=0, chunk=chunk)
     assert res.local_range == (0, total) and res.local_valid == total
-    row = ev.generate_orders(g, 0, res.best_id, 1).cpu().numpy()
-    peak, _, valid = coracle.eval_orders(coracle.CGraph(g), row)
-    assert bool(valid[0]) and int(peak[0]) == res.best_peak
+    cg = coracle.CGraph(g)
+    peaks = np.empty(total, np.int64)
+    valid = np.empty(total, bool)
+    for c0 in range(0, total, chunk):
+        orders = ev.generate_orders(g, 0, c0, chunk)
+        p, a, v = (x.cpu().numpy() for x in ev.evaluate_orders(g, orders))
+        want = coracle.eval_orders(cg, orders.cpu().numpy(), events=True)
+        assert np.array_equal(v, want[2]), c0
+        assert np.array_equal(p[v], want[0][want[2]]) and np.array_equal(a[v], want[1][want[2]]), c0
+        peaks[c0:c0 + chunk], valid[c0:c0 + chunk] = want[0], want[2]
+    assert valid.all()
+    best = int(np.argmin(peaks))          # first index attaining the minimum
+    assert (res.best_peak, res.best_id) == (int(peaks[best]), best)
+    print(f"config 5: {total} candidates, {len(np.unique(peaks))} distinct peaks, "
+          f"first strict min {int(peaks[best])} at id {best}")
 
 
 def test_chunking_does_not_change_the_answer():

@@ -88,6 +88,31 @@ def test_c_oracle_matches_python_oracle():
                 assert not val[k]
 
 
+def test_event_sweep_oracle_matches_literal_oracle():
+    """The C oracle's event-sweep mode (used to check million-row batches)
+    returns what its literal per-step mode returns (graph.py:452-458) row for
+    row: golden corpora, every config graph's candidates, corrupted rows."""
+    from paper_2310_19295_b200 import graphgen as gg
+    cases = []
+    for entry in golden("peaks")["training"] + golden("peaks")["random_dags"]:
+        cases.append((load_graph(entry["doc"]), np.array([r["order"] for r in entry["rows"]], np.int32)))
+    rng = np.random.default_rng(0)
+    for name in ("layered", "gpt2-small", "bert-large", "gpt2-xl"):
+        g = load_graph(gg.config_doc(name))
+        rows = coracle.kahn_orders(coracle.CGraph(g), 0, 0, 64)
+        for r in range(0, 64, 5):
+            i, j = rng.integers(0, rows.shape[1], 2)
+            rows[r, [i, j]] = rows[r, [j, i]]
+        rows[3, 0] = len(g.ops) + 2
+        cases.append((g, rows))
+    for g, rows in cases:
+        cg = coracle.CGraph(g)
+        a = coracle.eval_orders(cg, rows, threads=2)
+        b = coracle.eval_orders(cg, rows, threads=2, events=True)
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
+
+
 def test_schedules_match_reference():
     S = golden("schedules")
     fx = {k: load_graph(v) for k, v in golden("peaks")["fixtures"].items()}
