@@ -216,6 +216,50 @@ int rm_layout_violations(int64_t N, const int32_t* start, const int32_t* end,
                          int64_t capacity, uint8_t* item_flags, int64_t* pairs /* [2*max] */,
                          int64_t max_pairs, int64_t* n_pairs, int64_t* max_extent, void* stream);
 
+/* repair_conflicts (layout.py:409-470): items sorted by tensor id, every
+ * one with an offset.  Each round finds the conflicting pairs (time AND
+ * address overlap) on the device with the items resident, elects one mover
+ * per pair (the non-activation side, else the smaller (size, lifetime,
+ * -tensor)) and re-places the movers in (size, lifetime, tensor) order on the
+ * host: the smallest free gap of the mover's lifetime that fits (lowest on
+ * ties), else on top of everything it overlaps in time; capacity grows to
+ * fit.  offset[] and *capacity are updated in place; *rounds = rounds that
+ * moved something.  After N + 1 rounds a remaining conflict fails with
+ * RM_ERR_GRAPH ("conflict repair did not converge", layout.py:468-469).
+ * Host pointers; synchronous. */
+int rm_repair_conflicts(int64_t N, const int64_t* tensor, const int32_t* start, const int32_t* end,
+                        const int64_t* size, const uint8_t* is_act, int64_t* offset,
+                        int64_t* capacity, int32_t* rounds, void* stream);
+
+/* The placement step of one repair round alone (layout.py:445-467), host
+ * code: movers[] (item indices, in placement order) re-placed one after the
+ * other against items with has_offset set. */
+int rm_repair_place(int64_t N, const int32_t* start, const int32_t* end, const int64_t* size,
+                    const uint8_t* has_offset, int64_t* offset, int64_t* capacity,
+                    int64_t n_movers, const int64_t* movers);
+
+/* place_weight_updates (ordering.py:387-467), host C++.  Activation tensors
+ * k: lifetime [act_start, act_end] = [asap(producer), max alap(consumers)]
+ * (n-1 without consumers), act_size; mean_size = the graph's mean tensor
+ * size.  The slot skeleton (Linearization.slots): slot_kind 0 = op slot_ref,
+ * 1 = window slot_ref, windows' ops in win_ptr/win_ops CSR, tail_window -1
+ * for None.  Branches b (already filtered to floating ones): first op,
+ * gradient producers (grad_ptr CSR), grad_bytes, resolved alpha.  Outputs in
+ * the reference's placement order k: out_branch[k] (input branch index),
+ * delayed, target window, ready_t, size_ratio, projected_use;
+ * activation_total (0 without branches).  A gradient producer outside every
+ * slot fails with RM_ERR_GRAPH and *missing_op = that op (the reference's
+ * KeyError). */
+int rm_place_weight_updates(int32_t n_ops, const int32_t* asap, int64_t n_act, const int32_t* act_start,
+                            const int32_t* act_end, const int64_t* act_size, double mean_size,
+                            int32_t n_slots, const int32_t* slot_kind, const int32_t* slot_ref,
+                            int32_t n_windows, const int64_t* win_ptr, const int32_t* win_ops,
+                            int32_t tail_window, int32_t n_branches, const int32_t* br_first,
+                            const int64_t* grad_ptr, const int32_t* grad_producer, const int64_t* grad_bytes,
+                            const double* alpha, double r, int32_t force_immediate, int32_t* out_branch,
+                            uint8_t* out_delayed, int32_t* out_target, int32_t* out_ready, double* out_ratio,
+                            double* out_projected, int64_t* activation_total, int32_t* missing_op);
+
 /* ---------------------------------------------- K3: batched LLFB packer */
 
 enum {

@@ -21,7 +21,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB_PATH = PKG / "libroam.so"
-SOURCES = ("roam_graph.cpp", "layout_search.cpp", "order_search.cpp", "k_eval.cu", "k_eval_v2.cu", "k_eval_v4.cu", "k_eval_v5.cu", "k_gen.cu", "k_layout.cu", "k_pack.cu", "k_greedy.cu", "k_exact.cu")
+SOURCES = ("roam_graph.cpp", "layout_search.cpp", "order_search.cpp", "wu_place.cpp", "k_eval.cu", "k_eval_v2.cu", "k_eval_v4.cu", "k_eval_v5.cu", "k_gen.cu", "k_layout.cu", "k_repair.cu", "k_pack.cu", "k_greedy.cu", "k_exact.cu")
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 
 
@@ -100,6 +100,7 @@ class RmScheduleResult(C.Structure):
 
 
 RM_ERR_CAPACITY = -5
+RM_ERR_GRAPH = -6
 RM_DEVICE_PTRS = 1
 RM_NO_REDUCE = 2
 RM_ORDERS_U16 = 4
@@ -122,6 +123,11 @@ SIGNATURES = {
                                    C.POINTER(RmScheduleResult), vp, vp, vp, vp]),
     "rm_layout_violations": (C.c_int, [C.c_int64, vp, vp, vp, vp, vp, C.c_int64, vp, vp,
                                        C.c_int64, vp, vp, vp]),
+    "rm_repair_place": (C.c_int, [C.c_int64, vp, vp, vp, vp, vp, vp, C.c_int64, vp]),
+    "rm_repair_conflicts": (C.c_int, [C.c_int64, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "rm_place_weight_updates": (C.c_int, [C.c_int32, vp, C.c_int64, vp, vp, vp, C.c_double, C.c_int32, vp, vp,
+                                          C.c_int32, vp, vp, C.c_int32, C.c_int32, vp, vp, vp, vp, vp,
+                                          C.c_double, C.c_int32] + [vp] * 8),
     "rm_llfb_batch": (C.c_int, [C.c_int32, vp, vp, vp, vp, vp, vp, C.c_int32, vp, vp, vp, vp,
                                 vp, vp]),
     "rm_layout_search": (C.c_int, [C.c_int32, vp, vp, vp, vp, vp, C.c_int32, vp, C.c_int64, C.c_double,

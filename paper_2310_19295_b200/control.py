@@ -553,3 +553,92 @@ def _linearize_factory(mp):
         return seg.Linearization(slots=tuple(slots), windows=tuple(windows), leaf_of_op=leaf_of_op,
                                  tail_window=tail_window)
     return linearize
+
+
+def place_weight_updates_factory(mp):
+    """Drop-in for ordering.place_weight_updates (ordering.py:387-467): the
+    branch loop in libroam's host C++ (``rm_place_weight_updates``, wu_place.cpp)
+    over the activation lifetimes swept once, returning the reference's own
+    WeightUpdatePlan / BranchPlacement records.  The reference's callees stay
+    the (rebound) module globals it would call: linearize, asap_alap,
+    weight_update_branches, resolve_alpha (whose ConfigError surfaces for the
+    first branch in the reference's placement order)."""
+    import ctypes as C
+
+    ordm, gr = mp.ordering, mp.graph
+
+    def place_weight_updates(g, tree, r, alpha=None, *, force_immediate=False):
+        alpha = ordm.DEFAULT_ALPHA if alpha is None else alpha
+        lin = ordm.linearize(g, tree)
+        bounds = ordm.asap_alap(g)
+        floating = set(tree.floating_ops)
+        branches = [b for b in ordm.weight_update_branches(g) if b.ops and b.ops[0] in floating]
+        T = g.n_tensors
+        mean_size = sum(t.size for t in g.tensors) / T if T else 0.0
+        n = g.n_ops
+        asap = np.asarray(bounds.asap, np.int32)
+        alap = np.asarray(bounds.alap, np.int64)
+        a = graph_arrays(g)
+        cats = ordm.classify_tensors(g)
+        act = np.fromiter((cats[t] is gr.TensorCategory.ACTIVATION for t in range(T)), bool, T)
+        ids = np.flatnonzero(act)
+        cp = np.asarray(a.cons_ptr, np.int64)
+        # max alap over each tensor's consumers (horizon n - 1 without any)
+        tend = np.full(T, n - 1, np.int64)
+        nz = np.flatnonzero(cp[1:] > cp[:-1])
+        if len(nz):
+            tend[nz] = np.maximum.reduceat(alap[np.asarray(a.cons_idx, np.int64)], cp[nz])
+        end = tend[ids]
+        act_start = asap[np.asarray(a.producer, np.int64)[ids]].astype(np.int32) if len(ids) else np.zeros(0, np.int32)
+        act_end = end.astype(np.int32)
+        act_size = np.asarray(a.size, np.int64)[ids]
+        # slot skeleton: kind 0 = op, 1 = window
+        S = len(lin.slots)
+        kind = np.fromiter((0 if k == "op" else 1 for k, _ in lin.slots), np.int32, S)
+        ref = np.fromiter((v for _, v in lin.slots), np.int32, S)
+        W = len(lin.windows)
+        wlen = np.fromiter((len(w.ops) for w in lin.windows), np.int64, W)
+        wptr = np.zeros(W + 1, np.int64)
+        np.cumsum(wlen, out=wptr[1:])
+        wops = np.fromiter((v for w in lin.windows for v in w.ops), np.int32, int(wptr[-1]))
+        B = len(branches)
+        alphas = []
+        for b in branches:
+            try:
+                alphas.append(ordm.resolve_alpha(g, b, alpha))
+            except gr.ConfigError:
+                # the reference resolves alphas in placement order: raise for
+                # the first unresolvable branch in that order
+                key = lambda b: (max(bounds.asap[g.tensors[t].producer] for t in b.gradients), b.ops[0])  # noqa: E731
+                for bb in sorted(branches, key=key):
+                    ordm.resolve_alpha(g, bb, alpha)
+                raise
+        first = np.fromiter((b.ops[0] for b in branches), np.int32, B)
+        glen = np.fromiter((len(b.gradients) for b in branches), np.int64, B)
+        gptr = np.zeros(B + 1, np.int64)
+        np.cumsum(glen, out=gptr[1:])
+        gprod = np.fromiter((g.tensors[t].producer for b in branches for t in b.gradients), np.int32,
+                            int(gptr[-1]))
+        gbytes = np.fromiter((b.grad_bytes for b in branches), np.int64, B)
+        alph = np.asarray(alphas, np.float64)
+        o_b, o_t, o_r = (np.zeros(B, np.int32) for _ in range(3))
+        o_d = np.zeros(B, np.uint8)
+        o_ratio, o_proj = np.zeros(B), np.zeros(B)
+        total, missing = C.c_int64(0), C.c_int32(-1)
+        rc = lib().rm_place_weight_updates(
+            n, ptr(asap), len(ids), ptr(act_start), ptr(act_end), ptr(act_size), float(mean_size), S,
+            ptr(kind), ptr(ref), W, ptr(wptr), ptr(wops),
+            -1 if lin.tail_window is None else int(lin.tail_window), B, ptr(first), ptr(gptr), ptr(gprod),
+            ptr(gbytes), ptr(alph), float(r), 1 if force_immediate else 0, ptr(o_b), ptr(o_d), ptr(o_t),
+            ptr(o_r), ptr(o_ratio), ptr(o_proj), C.byref(total), C.byref(missing))
+        if missing.value >= 0:
+            raise KeyError(missing.value)
+        check(rc, "rm_place_weight_updates")
+        placements = tuple(
+            ordm.BranchPlacement(branch=branches[b], delayed=bool(d), target_window=t,
+                                 target_leaf=lin.windows[t].leaf, alpha=alphas[b], size_ratio=ratio,
+                                 ready_t=rt, projected_use=pu)
+            for b, d, t, rt, ratio, pu in zip(o_b.tolist(), o_d.tolist(), o_t.tolist(), o_r.tolist(),
+                                               o_ratio.tolist(), o_proj.tolist()))
+        return ordm.WeightUpdatePlan(placements=placements, activation_total=int(total.value))
+    return place_weight_updates

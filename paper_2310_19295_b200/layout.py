@@ -24,7 +24,7 @@ from typing import Mapping, Sequence
 import numpy as np
 
 from . import _lib
-from ._lib import check, lib, ptr
+from ._lib import RM_ERR_GRAPH, check, lib, ptr
 from .graph import Schedule, TensorCategory, classify_tensors
 
 
@@ -290,74 +290,37 @@ def _branch_and_bound(p, r: PackResult, t0: float) -> MemoryLayout:
 
 def repair_conflicts(m, p):
     """Re-place the smaller, shorter-lived member of every conflicting pair
-    (layout.py:409-470).  Conflict detection -- the O(N^2) part, 91.5 s of
-    279 s at 10.8k ops in the reference -- is K2; mover placement (best-fit
-    gap, strict < on gap size so the lowest-addressed smallest gap wins) is a
-    vectorised host sweep per mover.  Returns ``dataclasses.replace(m, ...)``
-    so the caller's layout type is preserved."""
+    (layout.py:409-470) in one libroam call (rm_repair_conflicts): per round
+    the device tests every item pair for time x address overlap with the
+    items resident and flags each pair's elected mover (K2's tiled geometry;
+    91.5 s of 279 s at 10.8k ops in the reference); the host C++ places the
+    movers (best-fit gap, strict < on gap size so the lowest-addressed
+    smallest gap wins).  Returns ``dataclasses.replace(m, ...)`` so the
+    caller's layout type is preserved."""
     from dataclasses import replace
 
     from .graph import StructuralError
     items = sorted(p.items, key=lambda i: i.tensor)
-    by_id = {i.tensor: i for i in p.items}
     offsets = dict(m.offsets)
-    capacity = m.capacity
     N = len(items)
+    for it in items:                      # layout.py:424-426 reads every offset
+        if it.tensor not in offsets:
+            raise KeyError(it.tensor)
+    if N < 2:
+        return replace(m, offsets=offsets, capacity=m.capacity)
+    _lib.require_device()
     tid = np.fromiter((i.tensor for i in items), np.int64, N)
     st, en, sz = _item_arrays(items)
-    st64, en64 = st.astype(np.int64), en.astype(np.int64)
-
-    def conflicts():
-        return conflict_pairs(items, offsets) if N > 1 else []
-
-    def mover(a, b):
-        if a.is_activation != b.is_activation:
-            return b if a.is_activation else a
-        ka = (a.size, a.end - a.start, -a.tensor)
-        kb = (b.size, b.end - b.start, -b.tensor)
-        return a if ka < kb else b
-
-    # offsets keyed by items' tensors (every item of p has one after concat)
-    has = np.fromiter((t in offsets for t in tid.tolist()), bool, N)
-    for _ in range(N + 1):
-        pairs = conflicts()
-        if not pairs:
-            break
-        movers = sorted({mover(items[a], items[b]).tensor for a, b in pairs},
-                        key=lambda t: (by_id[t].size, by_id[t].end - by_id[t].start, t))
-        off = np.fromiter((offsets.get(t, 0) for t in tid.tolist()), np.int64, N)
-        pos = {t: k for k, t in enumerate(tid.tolist())}
-        for t in movers:
-            k = pos[t]
-            it = by_id[t]
-            sel = has & (st64 <= it.end) & (it.start <= en64)
-            sel[k] = False
-            lo = off[sel]
-            hi = lo + sz[sel]
-            o = np.argsort(lo, kind="stable")
-            lo, hi = lo[o], hi[o]
-            if lo.size:
-                edge_before = np.maximum.accumulate(np.concatenate(([0], hi[:-1])))
-                edge_before = np.maximum(edge_before, 0)
-                gap = lo > edge_before
-                g_lo, g_hi = edge_before[gap], lo[gap]
-                edge = int(max(0, hi.max()))
-            else:
-                g_lo = g_hi = np.zeros(0, np.int64)
-                edge = 0
-            if capacity > edge:
-                g_lo = np.append(g_lo, edge)
-                g_hi = np.append(g_hi, capacity)
-            width = g_hi - g_lo
-            fit = (width >= it.size).nonzero()[0]
-            if fit.size:
-                best = fit[np.argmin(width[fit])]   # first of the smallest
-                new = int(g_lo[best])
-            else:
-                new = edge
-            offsets[t] = new
-            off[k] = new
-            capacity = max(capacity, new + it.size)
-    if conflicts():
+    act = np.fromiter((bool(i.is_activation) for i in items), np.uint8, N)
+    off = np.fromiter((offsets[t] for t in tid.tolist()), np.int64, N)
+    before = off.copy()
+    cap = C.c_int64(int(m.capacity))
+    rounds = C.c_int32(0)
+    rc = lib().rm_repair_conflicts(N, ptr(tid), ptr(st), ptr(en), ptr(sz), ptr(act), ptr(off),
+                                   C.byref(cap), C.byref(rounds), None)
+    if rc == RM_ERR_GRAPH:
         raise StructuralError("conflict repair did not converge")
-    return replace(m, offsets=offsets, capacity=capacity)
+    check(rc, "rm_repair_conflicts")
+    for k in np.flatnonzero(off != before).tolist():
+        offsets[int(tid[k])] = int(off[k])
+    return replace(m, offsets=offsets, capacity=int(cap.value))

@@ -22,6 +22,8 @@ Dispatch points rebound (reference file:line of the call site):
   planner.repair_conflicts       planner.py:259    K2 detection + mover placement
   planner.validate_layout        planner.py:260    K2
   ordering.weight_update_cost    ordering.py:310   event sweep once per (graph, bounds)
+  planner/ordering.place_weight_updates  ordering.py:387-467  the branch loop in libroam
+                                 C++ (rm_place_weight_updates) over one activation sweep
   ordering.asap_alap             ordering.py:405   C++ closure bitsets (graph.py:365-372)
   segmentation._region_between / _format_ig_ok / linearize (+ planner.linearize,
   ordering.linearize)            segmentation.py:174-201, 500-572: numpy over the
@@ -261,6 +263,8 @@ def install(mp=None):
         (ordm, "linearize"): fast_linearize,
         (pl, "build_window_problems"): build_window_problems,
         (ordm, "weight_update_cost"): _weight_update_cost_factory(mp),
+        (ordm, "place_weight_updates"): T(_ctl.place_weight_updates_factory(mp)),
+        (pl, "place_weight_updates"): T(_ctl.place_weight_updates_factory(mp)),
         (ordm, "asap_alap"): _asap_alap_factory(mp),
         (mp.segmentation, "_region_between"): _ctl.region_between_factory(),
         (mp.segmentation, "_format_ig_ok"): _ctl.format_ig_ok_factory(mp),

@@ -132,7 +132,9 @@ _BANNED = [("ordering", "exact_order"), ("planner", "exact_order"), ("ordering",
            ("layout", "llfb_layout"), ("ordering", "build_window_problems"), ("graph", "asap_alap"),
            ("graph", "predecessor_masks"), ("segmentation", "predecessor_masks"),
            ("graph", "successor_masks"), ("segmentation", "successor_masks"),
-           ("graph", "live_bytes_by_timestep"), ("graph", "peak_memory"), ("layout", "layout_violations")]
+           ("graph", "live_bytes_by_timestep"), ("graph", "peak_memory"), ("layout", "layout_violations"),
+           ("ordering", "place_weight_updates"), ("planner", "place_weight_updates"),
+           ("ordering", "weight_update_cost"), ("layout", "repair_conflicts"), ("planner", "repair_conflicts")]
 
 
 def _ban_reference_solvers(monkeypatch):

@@ -50,6 +50,11 @@ def test_device_entry_points_fail_loudly_without_gpu():
         exact_order(OrderingProblem(g, (0, 1, 2, 3)))
     with pytest.raises(_lib.RoamError):
         greedy_order(OrderingProblem(g, (0, 1, 2, 3)))
+    from paper_2310_19295_b200.layout import LayoutItem, repair_conflicts
+    from types import SimpleNamespace
+    with pytest.raises(_lib.RoamError):
+        repair_conflicts(SimpleNamespace(offsets={0: 0, 1: 0}, capacity=4),
+                         SimpleNamespace(items=(LayoutItem(0, 4, 0, 1), LayoutItem(1, 4, 0, 1))))
 
 
 def k1_numpy(meta: dict, n: int, order) -> tuple[int, int, bool]:

@@ -22,7 +22,8 @@ def test_install_uninstall_roundtrip():
               (mp.ordering, "weight_update_branches"), (mp.planner, "assign_shared_tensors"),
               (mp.planner, "classify_tensors"), (mp.graph, "classify_tensors"),
               (mp.ordering, "weight_update_cost"), (mp.ordering, "asap_alap"),
-              (mp.planner, "build_window_problems"),
+              (mp.planner, "build_window_problems"), (mp.planner, "place_weight_updates"),
+              (mp.ordering, "place_weight_updates"),
               (mp.simulator, "peak_memory")]
     before = {k: getattr(*k) for k in names}
     plug.install(mp)
@@ -47,22 +48,54 @@ def test_errors_translate_to_reference_classes():
 
 
 @pytest.mark.skipif(mp is None, reason="reference memplan not importable")
-def test_repair_mover_placement_matches_reference(monkeypatch):
-    """repair_conflicts' host mover placement (the part that is not K2) against
-    the reference, with K2's pair detection stood in by the oracle's pair
-    predicate so this runs without a GPU."""
+def test_repair_mover_placement_matches_reference():
+    """repair_conflicts' mover placement (rm_repair_place, host C++ in
+    libroam) against the reference: the rounds are driven here with the
+    oracle's pair predicate and mover election standing in for the device
+    detection (no GPU), placement goes through the C ABI."""
+    import ctypes as C
     import random
 
+    import numpy as np
+
     from oracle import memplan_oracle as O
-    from paper_2310_19295_b200 import layout as L
+    from paper_2310_19295_b200._lib import check, lib, ptr
 
-    def cpu_pairs(items, offsets):
+    def repair(m, p):
+        items = sorted(p.items, key=lambda i: i.tensor)
         rows = [(i.tensor, i.size, i.start, i.end, i.is_activation) for i in items]
-        return [(a, b) for a in range(len(rows)) for b in range(a + 1, len(rows))
-                if O.overlaps(rows[a], rows[b]) and offsets[rows[a][0]] < offsets[rows[b][0]] + rows[b][1]
-                and offsets[rows[b][0]] < offsets[rows[a][0]] + rows[a][1]]
+        N = len(rows)
+        st = np.array([r[2] for r in rows], np.int32)
+        en = np.array([r[3] for r in rows], np.int32)
+        sz = np.array([r[1] for r in rows], np.int64)
+        off = np.array([m.offsets[r[0]] for r in rows], np.int64)
+        has = np.ones(N, np.uint8)
+        cap = C.c_int64(m.capacity)
 
-    monkeypatch.setattr(L, "conflict_pairs", cpu_pairs)
+        def pairs():
+            return [(a, b) for a in range(N) for b in range(a + 1, N)
+                    if O.overlaps(rows[a], rows[b]) and off[a] < off[b] + sz[b] and off[b] < off[a] + sz[a]]
+
+        def mover(a, b):
+            if rows[a][4] != rows[b][4]:
+                return b if rows[a][4] else a
+            ka = (sz[a], en[a] - st[a], -rows[a][0])
+            kb = (sz[b], en[b] - st[b], -rows[b][0])
+            return a if ka < kb else b
+
+        for _ in range(N + 1):
+            ps = pairs()
+            if not ps:
+                break
+            mv = np.array(sorted({mover(a, b) for a, b in ps},
+                                 key=lambda k: (sz[k], en[k] - st[k], rows[k][0])), np.int64)
+            check(lib().rm_repair_place(N, ptr(st), ptr(en), ptr(sz), ptr(has), ptr(off), C.byref(cap),
+                                        len(mv), ptr(mv)), "rm_repair_place")
+        assert not pairs()
+        offs = dict(m.offsets)
+        offs.update({r[0]: int(o) for r, o in zip(rows, off)})
+        return offs, cap.value
+
     rng = random.Random(11)
     for trial in range(150):
         n = rng.randint(1, 40)
@@ -76,8 +109,8 @@ def test_repair_mover_placement_matches_reference(monkeypatch):
         m = mp.layout.MemoryLayout(offsets=offs, capacity=cap)
         p = mp.layout.LayoutProblem(items=tuple(items))
         want = mp.layout.repair_conflicts(m, p)
-        got = L.repair_conflicts(m, p)
-        assert got == want
+        got_offs, got_cap = repair(m, p)
+        assert (got_offs, got_cap) == (want.offsets, want.capacity), trial
 
 
 @pytest.mark.skipif(mp is None, reason="reference memplan not importable")
@@ -350,3 +383,45 @@ def test_segment_tree_dropin_matches_reference():
             assert _tree_key(fast_tree(g, limit)) == _tree_key(seg.build_segment_tree(g, limit))
     with pytest.raises(mp.graph.ConfigError, match="node_limit"):
         fast_tree(graphs[0], 1)
+
+
+@pytest.mark.skipif(mp is None, reason="reference memplan not importable")
+def test_place_weight_updates_matches_reference(monkeypatch):
+    """rm_place_weight_updates (host C++) returns the reference's
+    WeightUpdatePlan exactly -- placements, delays, targets, ratios and
+    projected uses bit for bit -- for every call the planner makes, and for
+    the same trees under other delay radii, alpha maps and force_immediate;
+    an unresolvable alpha raises the reference's ConfigError message."""
+    import memplan.graphgen as rgen
+
+    from paper_2310_19295_b200 import control as ctl
+    from paper_2310_19295_b200 import graphgen as gg
+    fast = ctl.place_weight_updates_factory(mp)
+    orig = mp.ordering.place_weight_updates
+    calls, delayed = [], []
+
+    def both(g, tree, r, alpha=None, *, force_immediate=False):
+        want = orig(g, tree, r, alpha, force_immediate=force_immediate)
+        assert fast(g, tree, r, alpha, force_immediate=force_immediate) == want
+        for rr in (0.0, 0.25, 1.0, 3.0):
+            for al in (None, {"adam": 0.5, "sgd": 9.0}, {"default": 2.5, "ad": 1.0}, {"default": 40.0},
+                       {"default": 400.0, "adam.": 3000.0}):
+                for fi in (False, True):
+                    assert fast(g, tree, rr, al, force_immediate=fi) == orig(g, tree, rr, al, force_immediate=fi)
+        if want.placements:
+            with pytest.raises(mp.graph.ConfigError) as e_ref:
+                orig(g, tree, r, {"nomatch": 1.0})
+            with pytest.raises(mp.graph.ConfigError) as e_got:
+                fast(g, tree, r, {"nomatch": 1.0})
+            assert str(e_got.value) == str(e_ref.value)
+        calls.append(len(want.placements))
+        delayed.append(sum(p.delayed for p in orig(g, tree, 0.0, {"default": 400.0}).placements))
+        return want
+
+    monkeypatch.setattr(mp.planner, "place_weight_updates", both)
+    mp.planner.plan(mp.graph.load_graph(gg.config_doc("gpt2-small")))
+    for arch in ("mlp", "residual", "transformer_block"):
+        for opt in ("sgd", "adam"):
+            mp.planner.plan(rgen.gen_training_graph(arch, 4, optimizer=opt))
+    assert len(calls) >= 7 and sum(calls) > 100
+    assert sum(delayed) > 20      # the delay rule and the later-window scan are exercised
