@@ -142,6 +142,7 @@ SIGNATURES = {
     "rm_set_timing": (C.c_int, [C.c_int]),
     "rm_set_k1_variant": (C.c_int, [C.c_int]),
     "rm_set_sm_reserve": (C.c_int, [C.c_int]),
+    "rm_set_gen_form": (C.c_int, [C.c_int]),
     "rm_graph_asap_alap": (C.c_int, [vp, vp, vp]),
     "rm_graph_ancestors": (C.c_int, [vp, vp]),
     "rm_eval_select_key": (C.c_int, [vp, vp, C.c_int64, C.c_int64, C.c_int32, C.c_uint32, vp, vp, vp, vp, vp]),

@@ -639,6 +639,7 @@ int rm_graph_create(const RmGraphDesc* d, uint32_t flags, RmGraph** out) {
     return st;
   }
 
+  build_gen_meta(*g);
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess) {
     cudaGetLastError();
@@ -676,6 +677,9 @@ int rm_graph_create(const RmGraphDesc* d, uint32_t flags, RmGraph** out) {
     if (!e && g->k5v.ok) e = up(g->k5v.g4, g->h5_g4);
     if (!e && g->k5v.ok) e = up(g->k5v.gptr, g->h5_gptr);
     if (!e && g->k5v.ok) e = up(g->k5v.gcons, g->h5_gcons);
+    if (!e && g->gen.ok) e = up(g->gen.eptr, g->gen.h_eptr);
+    if (!e && g->gen.ok) e = up(g->gen.edges, g->gen.h_edges);
+    if (!e && g->gen.ok) e = up(g->gen.zero, g->gen.h_zero);
     if (!e) e = up(g->d_size, g->size);
     if (!e) e = up(g->d_producer, g->producer);
     if (!e) e = up(g->d_cons_ptr, g->cons_ptr);

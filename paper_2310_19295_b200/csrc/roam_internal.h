@@ -156,6 +156,23 @@ struct K1V5Meta {
   DevBuf base, tab, dpair, dtgt, g4, gptr, gcons;
 };
 
+// Thread-per-candidate generator metadata (k_gen.cu, k_gen_thread): per op
+// its direct successors as one u32 each, w | bitoff << 16 | kind << 29, where
+// kind 0 = w has one predecessor (ready at once), 1 = two (a toggle bit at
+// bitoff of the thread's counter words), k >= 2 = k + 1 predecessors (an
+// arrival counter of ceil(log2(k + 1)) bits at bitoff, never straddling a
+// word); zero = the ops without predecessors.  ok = 0 when n > 65536, an op
+// has more than 8 predecessors or the counters need more than 8192 bits.
+struct GenMeta {
+  int ok = 0;
+  int words = 0;   // counter words per candidate
+  int n_zero = 0;
+  std::vector<uint32_t> h_eptr, h_edges;
+  std::vector<uint16_t> h_zero;
+  DevBuf eptr, edges, zero;
+};
+void build_gen_meta(RmGraph& g);
+
 }  // namespace roam
 
 struct RmGraph {
@@ -178,6 +195,7 @@ struct RmGraph {
   roam::K1V2Meta k2v;
   roam::K1V4Meta k4v;
   roam::K1V5Meta k5v;
+  roam::GenMeta gen;
   std::vector<int32_t> h2_opv;     // 2n
   std::vector<uint32_t> h2_edges, h2_mpair, h2_mptr, h2_msz;
   std::vector<uint16_t> h2_mcons;

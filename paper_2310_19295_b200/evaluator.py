@@ -407,6 +407,12 @@ def set_sm_reserve(sms: int) -> None:
     check(lib().rm_set_sm_reserve(int(sms)), "rm_set_sm_reserve")
 
 
+def set_gen_form(form: int) -> None:
+    """Candidate generator form on this thread: 0 auto (thread per candidate
+    where the graph qualifies), 1 warp per candidate (rm_set_gen_form)."""
+    check(lib().rm_set_gen_form(int(form)), "rm_set_gen_form")
+
+
 def set_k1_variant(variant: int) -> None:
     """0 auto, 1 generic evaluator, 2 unit-packed interleaved (v2); per thread."""
     check(lib().rm_set_k1_variant(int(variant)), "rm_set_k1_variant")

@@ -96,6 +96,47 @@ def test_generator_matches_python_restatement():
         assert orders[k].tolist() == O.kahn_candidate(len(g.ops), preds, succs, 99, 5 + k)
 
 
+@pytest.mark.parametrize("name", ["gpt2-small", "bert-large", "gpt2-xl", "layered", "wide", "fan-in"])
+def test_generator_thread_form_equals_warp_form(name):
+    """The thread-per-candidate generator (heap + counters per thread, rows it
+    cannot finish rewritten by the warp form) gives the warp form's rows
+    exactly: training graphs, the layered DAG (ready sets above the heap's
+    32 entries: the hand-over path), a 300-wide antichain and an op with 12
+    predecessors (the warp form only); a sample of
+    rows against the Python restatement."""
+    from paper_2310_19295_b200.evaluator import set_gen_form
+    if name == "wide":
+        doc = {"ops": [{"id": 0, "name": "s", "kind": "forward", "inputs": [], "outputs": list(range(300))}]
+               + [{"id": 1 + k, "name": f"w{k}", "kind": "forward", "inputs": [k], "outputs": []}
+                  for k in range(300)],
+               "tensors": [{"id": k, "size_bytes": 4} for k in range(300)]}
+    elif name == "fan-in":
+        doc = {"ops": [{"id": k, "name": f"p{k}", "kind": "forward", "inputs": [], "outputs": [k]} for k in range(12)]
+               + [{"id": 12, "name": "j", "kind": "forward", "inputs": list(range(12)), "outputs": []}],
+               "tensors": [{"id": k, "size_bytes": 4} for k in range(12)]}
+    else:
+        doc = gg.config_doc(name)
+    g = load_graph(doc)
+    B = 3000 if name in ("gpt2-xl", "bert-large") else 5000
+    got = generate_orders(g, 17, 123, B).cpu().numpy()
+    set_gen_form(1)
+    try:
+        want = generate_orders(g, 17, 123, B).cpu().numpy()
+    finally:
+        set_gen_form(0)
+    assert np.array_equal(got, want)
+    if name in ("gpt2-xl", "layered"):   # the other heap capacities (A/B settings)
+        for cap in (32, 48, 64):
+            set_gen_form(cap)
+            try:
+                assert np.array_equal(generate_orders(g, 17, 123, B).cpu().numpy(), want), cap
+            finally:
+                set_gen_form(0)
+    preds, succs = O.direct_preds(g), O.direct_succs(g)
+    for k in (0, 1, B // 2, B - 1):
+        assert got[k].tolist() == O.kahn_candidate(len(g.ops), preds, succs, 17, 123 + k)
+
+
 def test_argmin_ties_and_none_valid():
     peak = np.array([7, 3, 3, 1, 3], np.int64)
     valid = np.array([1, 1, 1, 0, 1], bool)

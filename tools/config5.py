@@ -23,7 +23,7 @@ sys.path.insert(0, str(ROOT))
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--total", type=int, default=1 << 20)
-    ap.add_argument("--chunk", type=int, default=1 << 16)
+    ap.add_argument("--chunk", type=int, default=1 << 18)
     ap.add_argument("--graph", default="gpt2-xl")
     a = ap.parse_args()
     import torch
