@@ -17,15 +17,16 @@
 //                           twice by one op is never freed by this solver.)
 //
 // Host (C++, this file): builds every window's local problem from the graph
-// handle's CSR in O(window + its consumer entries).  Device: each op's score
-// (out - bytes its inputs would free) is kept in shared memory and updated
-// incrementally -- a tracked tensor's count only falls when an op runs, and
-// when it reaches 1 the one op still holding an entry (found in the tensor's
-// local consumer list) now frees it -- so per step each thread only compares
-// the scores of its ready ops, a block (score, index) argmin picks the op, and
-// one warp applies it (counts, the score updates, frees, successor pred
-// counts).  Mutable state lives in shared memory when it fits, else in a
-// per-window global scratch.
+// handle's CSR in O(window + its consumer entries).  Device: one warp per
+// window.  Each op's score (out - bytes its inputs would free) is kept in
+// shared memory and updated incrementally -- a tracked tensor's count only
+// falls when an op runs, and when it reaches 1 the one op still holding an
+// entry (found in the tensor's local consumer list) now frees it -- and the
+// ready ops sit in a compact list, so a step compares only the ready ops'
+// scores (a warp (score, index) argmin), then applies the pick (counts, score
+// updates, frees, successor pred counts, newly ready ops appended): no block
+// barrier per step.  Mutable state lives in shared memory when it fits, else
+// in a per-window global scratch.
 #include <algorithm>
 #include <climits>
 
@@ -59,18 +60,17 @@ struct K4Args {
 
 __host__ __device__ inline size_t k4_bytes(int64_t n_ops, int64_t n_ten) {
   auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
-  return al(8 * size_t(n_ops)) + al(4 * size_t(n_ops)) + al(size_t(n_ops)) + al(4 * size_t(n_ten));
+  return al(8 * size_t(n_ops)) + al(4 * size_t(n_ops)) + al(size_t(n_ops)) + al(4 * size_t(n_ten)) +
+         al(4 * size_t(n_ops));
 }
 
-template <int NT>
-__global__ void __launch_bounds__(NT) k4_greedy(const K4Args a) {
+// One warp per window.  The ready ops (all predecessors scheduled) sit in a
+// compact list -- a training window's ready set is tens of ops, so a step
+// scores only those instead of sweeping the whole window -- and everything
+// runs inside the warp: no block barrier anywhere on the step's critical path.
+__global__ void __launch_bounds__(32) k4_greedy(const K4Args a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ long long s_wv[NT / 32];
-  __shared__ int s_wi[NT / 32];
-  __shared__ int s_pick;
-  __shared__ long long s_live, s_peak;
-  constexpr int NW = NT / 32;
-  const int w = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int w = blockIdx.x, lane = threadIdx.x;
   const int64_t ob = a.op_base[w], tb = a.ten_base[w];
   const int n = a.nops[w];
   const int nt = (int)(a.ten_base[w + 1] - tb);
@@ -80,120 +80,121 @@ __global__ void __launch_bounds__(NT) k4_greedy(const K4Args a) {
   int* npred = reinterpret_cast<int*>(ws + al(8 * size_t(n)));
   unsigned char* done = ws + al(8 * size_t(n)) + al(4 * size_t(n));
   int* cnt = reinterpret_cast<int*>(ws + al(8 * size_t(n)) + al(4 * size_t(n)) + al(size_t(n)));
+  int* ready = reinterpret_cast<int*>(ws + al(8 * size_t(n)) + al(4 * size_t(n)) + al(size_t(n)) +
+                                      al(4 * size_t(nt)));
   const int64_t* tc_ptr = a.tc_ptr + tb;
   const int64_t* out = a.out + ob;
   const int64_t* in_ptr = a.in_ptr + ob;
   const int64_t* succ_ptr = a.succ_ptr + ob;
   const int64_t* tsize = a.tsize + tb;
-  for (int i = tid; i < n; i += NT) {
-    npred[i] = a.npred0[ob + i];
-    done[i] = 0;
-    // the score is kept up to date instead of recomputed every step: an
-    // input frees when its count is 1, and counts only fall when an op runs
-    long long freed = 0;
-    for (int64_t k = in_ptr[i]; k < in_ptr[i + 1]; ++k) {
-      const int t = __ldg(a.in_idx + k);
-      if (a.count0[tb + t] == 1) freed += tsize[t];
+  const unsigned lt = (1u << lane) - 1u;
+  int R = 0;
+  for (int i0 = 0; i0 < n; i0 += 32) {
+    const int i = i0 + lane;
+    bool rd = false;
+    if (i < n) {
+      const int np = a.npred0[ob + i];
+      npred[i] = np;
+      done[i] = 0;
+      // the score is kept up to date instead of recomputed every step: an
+      // input frees when its count is 1, and counts only fall when an op runs
+      long long freed = 0;
+      for (int64_t k = in_ptr[i]; k < in_ptr[i + 1]; ++k) {
+        const int t = __ldg(a.in_idx + k);
+        if (a.count0[tb + t] == 1) freed += tsize[t];
+      }
+      delta[i] = out[i] - freed;
+      rd = np == 0;
     }
-    delta[i] = out[i] - freed;
+    const unsigned m = __ballot_sync(0xffffffffu, rd);
+    if (rd) ready[R + __popc(m & lt)] = i;
+    R += __popc(m);
   }
-  for (int t = tid; t < nt; t += NT) cnt[t] = a.count0[tb + t];
-  if (tid == 0) {
-    s_live = a.start_live[w];
-    s_peak = a.start_live[w];
-  }
-  __syncthreads();
+  for (int t = lane; t < nt; t += 32) cnt[t] = a.count0[tb + t];
+  long long live = a.start_live[w], peak = live;
+  __syncwarp();
 
   for (int step = 0; step < n; ++step) {
-    // ---- score ready ops: delta = out - bytes freed by last uses
+    if (R == 0) {  // no ready op: the window's precedence has a cycle
+      if (lane == 0) a.status[w] = 2;
+      return;
+    }
+    // ---- score the ready ops: min (delta, local index) -- the reference's
+    // strict < over ascending local index
     long long bv = LLONG_MAX;
-    int bi = INT_MAX;
-    for (int i = tid; i < n; i += NT) {
-      if (done[i] || npred[i]) continue;
+    int bi = INT_MAX, bs = -1;
+    for (int j = lane; j < R; j += 32) {
+      const int i = ready[j];
       const long long d = delta[i];
-      if (d < bv) {  // ascending i per thread: strict < keeps the smallest
+      if (d < bv || (d == bv && i < bi)) {
         bv = d;
         bi = i;
+        bs = j;
       }
     }
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
       const long long ov = __shfl_xor_sync(0xffffffffu, bv, d);
       const int oi = __shfl_xor_sync(0xffffffffu, bi, d);
+      const int os = __shfl_xor_sync(0xffffffffu, bs, d);
       if (ov < bv || (ov == bv && oi < bi)) {
         bv = ov;
         bi = oi;
+        bs = os;
       }
     }
-    if (lane == 0) {
-      s_wv[warp] = bv;
-      s_wi[warp] = bi;
-    }
-    __syncthreads();
-    // ---- warp 0 applies the pick
-    if (warp == 0) {
-      bv = lane < NW ? s_wv[lane] : LLONG_MAX;
-      bi = lane < NW ? s_wi[lane] : INT_MAX;
-#pragma unroll
-      for (int d = 16; d > 0; d >>= 1) {
-        const long long ov = __shfl_xor_sync(0xffffffffu, bv, d);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, d);
-        if (ov < bv || (ov == bv && oi < bi)) {
-          bv = ov;
-          bi = oi;
-        }
-      }
-      if (bi == INT_MAX) {
-        if (lane == 0) s_pick = -1;
-      } else {
-        long long freed = 0;
-        for (int64_t k = in_ptr[bi] + lane; k < in_ptr[bi + 1]; k += 32) {
-          const int t = __ldg(a.in_idx + k);
-          const int c = --cnt[t];  // distinct inputs: no races
-          if (c == 0) freed += tsize[t];
-          if (c == 1) {
-            // one consumer entry left: its op (not run yet) now frees t
-            for (int64_t q = tc_ptr[t]; q < tc_ptr[t + 1]; ++q) {
-              const int j = __ldg(a.tc_idx + q);
-              if (j != bi && !done[j]) {
-                atomicAdd(reinterpret_cast<unsigned long long*>(delta + j),
-                          (unsigned long long)(-tsize[t]));
-                break;
-              }
-            }
+    // ---- apply the pick: inputs' counts (a count reaching 1 moves the free
+    // to the one consumer entry left), successors' predecessor counts
+    long long freed = 0;
+    for (int64_t k = in_ptr[bi] + lane; k < in_ptr[bi + 1]; k += 32) {
+      const int t = __ldg(a.in_idx + k);
+      const int c = --cnt[t];  // distinct inputs: no races
+      if (c == 0) freed += tsize[t];
+      if (c == 1) {
+        for (int64_t q = tc_ptr[t]; q < tc_ptr[t + 1]; ++q) {
+          const int j = __ldg(a.tc_idx + q);
+          if (j != bi && !done[j]) {
+            atomicAdd(reinterpret_cast<unsigned long long*>(delta + j), (unsigned long long)(-tsize[t]));
+            break;
           }
         }
-        for (int64_t k = succ_ptr[bi] + lane; k < succ_ptr[bi + 1]; k += 32)
-          npred[__ldg(a.succ_idx + k)] -= 1;     // distinct successors
-#pragma unroll
-        for (int d = 16; d > 0; d >>= 1) freed += __shfl_xor_sync(0xffffffffu, freed, d);
-        if (lane == 0) {
-          const long long live = s_live + out[bi];
-          s_peak = max(s_peak, live);
-          s_live = live - freed;
-          done[bi] = 1;
-          a.order[ob + step] = a.gop[ob + bi];
-          s_pick = bi;
-        }
       }
     }
-    __syncthreads();
-    if (s_pick < 0) {  // no ready op: the window's precedence has a cycle
-      if (tid == 0) a.status[w] = 2;
-      return;
+    __syncwarp();
+    if (lane == 0) {
+      done[bi] = 1;
+      ready[bs] = ready[R - 1];  // the list is unordered: the last entry fills the hole
     }
+    --R;
+    __syncwarp();
+    for (int64_t k = succ_ptr[bi]; k < succ_ptr[bi + 1]; k += 32) {
+      bool rd = false;
+      int sv = 0;
+      if (k + lane < succ_ptr[bi + 1]) {
+        sv = __ldg(a.succ_idx + k + lane);
+        rd = --npred[sv] == 0;  // distinct successors
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, rd);
+      if (rd) ready[R + __popc(m & lt)] = sv;
+      R += __popc(m);
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) freed += __shfl_xor_sync(0xffffffffu, freed, d);
+    live += out[bi];
+    peak = max(peak, live);
+    live -= freed;
+    if (lane == 0) a.order[ob + step] = a.gop[ob + bi];
+    __syncwarp();
   }
-  if (tid == 0) {
-    a.peak[w] = s_peak;
+  if (lane == 0) {
+    a.peak[w] = peak;
     a.status[w] = 0;
   }
 }
 
-template <int NT>
-static int launch_k4_t(const K4Args& a, size_t smem, cudaStream_t s) {
-  auto kern = k4_greedy<NT>;
-  RM_CUDA(smem_optin(kern));
-  kern<<<a.W, NT, smem, s>>>(a);
+static int launch_k4(const K4Args& a, size_t smem, cudaStream_t s) {
+  RM_CUDA(smem_optin(k4_greedy));
+  k4_greedy<<<a.W, 32, smem, s>>>(a);
   RM_LAUNCH_CHECK("k4_greedy launch");
   return RM_OK;
 }
@@ -408,9 +409,7 @@ extern "C" int rm_greedy_windows(RmGraph* g, int32_t W, const int64_t* win_ptr,
   K4Args a{W, d_ob, d_nops, d_tb, d_gop, d_out, d_np, d_inp, d_ini, d_sup, d_sui, d_c0, d_tcp, d_tci,
            d_tsz, d_sl, d_ord, d_peak, d_st, d_g, d_goff};
   // wide windows: more threads, fewer ops per thread in each step's score scan
-  int64_t max_ops = 0;
-  for (int w = 0; w < W; ++w) max_ops = std::max<int64_t>(max_ops, op_base[w + 1] - op_base[w]);
-  int rc = max_ops > 2048 ? launch_k4_t<1024>(a, smem, s) : launch_k4_t<256>(a, smem, s);
+  int rc = launch_k4(a, smem, s);
   if (rc) return rc;
   std::vector<int32_t> ord_w(opb_dev[W]), st_dev(W);
   if (opb_dev[W])

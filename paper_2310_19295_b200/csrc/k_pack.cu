@@ -146,6 +146,62 @@ struct K3Block {
     *total = all;
     return before + inc - v;
   }
+  // One-barrier forms for the placement loop: each uses its own slots
+  // (xw / mk), and between two uses of one form every thread passes the
+  // other form's barrier, so no barrier is needed to protect the slots.  The
+  // NW per-warp partials are combined with shuffles, not a loop.
+  __device__ long long excl_max1(long long v, long long* total, long long* xw) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    long long inc = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const long long t = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc = max(inc, t);
+    }
+    long long ex = __shfl_up_sync(0xffffffffu, inc, 1);
+    if (lane == 0) ex = LLONG_MIN;
+    if (lane == 31) xw[w] = inc;
+    __syncthreads();
+    long long q = lane < NW ? xw[lane] : LLONG_MIN;  // inclusive scan over the warps
+#pragma unroll
+    for (int d = 1; d < NW; d <<= 1) {
+      const long long t = __shfl_up_sync(0xffffffffu, q, d);
+      if (lane >= d) q = max(q, t);
+    }
+    const long long before = __shfl_sync(0xffffffffu, q, w > 0 ? w - 1 : 0);
+    *total = __shfl_sync(0xffffffffu, q, NW - 1);
+    return w > 0 ? max(before, ex) : ex;
+  }
+  __device__ int min_key1(int key, long long val, long long* out_val, int* mi, long long* mv) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      const int ok = __shfl_xor_sync(0xffffffffu, key, d);
+      const long long ov = __shfl_xor_sync(0xffffffffu, val, d);
+      if (ok < key) {
+        key = ok;
+        val = ov;
+      }
+    }
+    if (lane == 0) {
+      mi[w] = key;
+      mv[w] = val;
+    }
+    __syncthreads();
+    key = lane < NW ? mi[lane] : INT_MAX;
+    val = lane < NW ? mv[lane] : 0;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {  // over all 32 lanes: every lane gets the answer
+      const int ok = __shfl_xor_sync(0xffffffffu, key, d);
+      const long long ov = __shfl_xor_sync(0xffffffffu, val, d);
+      if (ok < key) {
+        key = ok;
+        val = ov;
+      }
+    }
+    *out_val = val;
+    return key;
+  }
   // (min key, its value) over the block; key INT_MAX = none
   __device__ int min_key(int key, long long val, long long* out_val) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -298,6 +354,8 @@ __global__ void __launch_bounds__(NT) k3_llfb(const K3Args a) {
     // with timesteps >= 65535 elsewhere), so the list fits 128 registers
     constexpr bool PK = NT > 256;
     __shared__ long long s_plo[2][NT / 32], s_phi[2][NT / 32];
+    __shared__ long long s_xw[NT / 32], s_mv[NT / 32];
+    __shared__ int s_mi[NT / 32];
     __shared__ int s_pst[2][NT / 32], s_pen[2][NT / 32];
     const int lane = tid & 31, w = tid >> 5;
     long long rlo[MAXC], rhi[MAXC];
@@ -342,33 +400,45 @@ __global__ void __launch_bounds__(NT) k3_llfb(const K3Args a) {
         fl_nx = flo[i_nx];
       }
       const int buf = k & 1;
-      if (lane == 31) {
+      // a warp whose first slot lies past the list's end after this
+      // insertion (index P_k) holds only empty slots: it skips the slot work
+      // (warp-uniform) and only joins the block reductions -- the list fills
+      // from the front, so on average half the warps sit this out
+      const bool wlive = w * 32 * MAXC <= P + (k - A);
+      if (wlive && lane == 31) {
         s_plo[buf][w] = rlo[MAXC - 1];
         s_phi[buf][w] = rhi[MAXC - 1];
         s_pst[buf][w] = rst[MAXC - 1];
         if (!PK) s_pen[buf][w] = ren[PK ? 0 : MAXC - 1];
       }
       long long mx = LLONG_MIN;
+      if (wlive) {
 #pragma unroll
-      for (int m = 0; m < MAXC; ++m)
-        if (t_st(m) <= ei && si <= t_en(m)) mx = max(mx, rhi[m]);
+        for (int m = 0; m < MAXC; ++m)
+          if (t_st(m) <= ei && si <= t_en(m)) mx = max(mx, rhi[m]);
+      }
       long long all_mx;
-      long long M = max(fl, blk.excl_max(mx, &all_mx));
+      long long M = max(fl, blk.excl_max1(mx, &all_mx, s_xw));
       int brk = INT_MAX;
       long long at = 0;
+      if (wlive) {
 #pragma unroll
-      for (int m = 0; m < MAXC; ++m) {
-        if (t_st(m) <= ei && si <= t_en(m) && brk == INT_MAX) {
-          if (M + szi <= rlo[m]) {
-            brk = tid * MAXC + m;
-            at = M;
-          } else {
-            M = max(M, rhi[m]);
+        for (int m = 0; m < MAXC; ++m) {
+          if (t_st(m) <= ei && si <= t_en(m) && brk == INT_MAX) {
+            if (M + szi <= rlo[m]) {
+              brk = tid * MAXC + m;
+              at = M;
+            } else {
+              M = max(M, rhi[m]);
+            }
           }
         }
       }
       long long res;
-      if (blk.min_key(brk, at, &res) == INT_MAX) res = max(fl, all_mx);
+      if (blk.min_key1(brk, at, &res, s_mi, s_mv) == INT_MAX) res = max(fl, all_mx);
+      if (tid == 0) off[i] = res;
+      cap_rest = max(cap_rest, res + szi);
+      if (!wlive) continue;
       // the slot before this thread's first one
       long long plo = __shfl_up_sync(0xffffffffu, rlo[MAXC - 1], 1);
       long long phi = __shfl_up_sync(0xffffffffu, rhi[MAXC - 1], 1);
@@ -403,8 +473,6 @@ __global__ void __launch_bounds__(NT) k3_llfb(const K3Args a) {
         pst = ost;
         pen = oen;
       }
-      if (tid == 0) off[i] = res;
-      cap_rest = max(cap_rest, res + szi);
     }
     __syncthreads();
   } else {
@@ -638,8 +706,11 @@ extern "C" int rm_llfb_batch(int32_t P, const int64_t* item_ptr, const int32_t* 
   for (int64_t k = 0; k < NI && times16; ++k)
     times16 = start[k] >= 0 && end[k] >= 0 && start[k] < 65535 && end[k] < 65535;
   int rc;
-  // the register-resident placed list holds NT * 16 - 1 placed items
-  if (maxN < 4096)
+  // the register-resident placed list holds NT * MAXC - 1 placed items; fewer
+  // slots per thread shorten the per-item chain between the block barriers
+  if (maxN < 4096 && times16)
+    rc = launch_k3_t<512, 8>(a, P, smem, s);
+  else if (maxN < 4096)
     rc = launch_k3_t<256, 16>(a, P, smem, s);
   else if (maxN < 8192 && times16)
     rc = launch_k3_t<512, 16>(a, P, smem, s);
