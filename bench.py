@@ -550,6 +550,12 @@ def main() -> None:
                                     2: "k1v2_eval_orders"}.get(info["k1_variant"],
                                                                                     "k1_eval_orders"),
                          "k1_ms": k1_avg,
+                         "k1_ms_is": ("back-to-back K1 throughput: the launching stream's interval over the K "
+                                      "launches / K (" + ("selection fused into each K1 launch; " if use_key
+                                                          else "includes the argmin kernel after each K1; ")
+                                      + ("nothing else on the stream at N=1)" if world == 1 else
+                                         "includes the per-step exchange events at N>1, where PDL overlap "
+                                         "does not apply)")),
                          "alg_bytes_per_launch": alg_bytes,
                          "alg_bytes_formula": "B*(4n+16) + graph metadata",
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst)" if "_fallback" not in peaks

@@ -156,6 +156,21 @@ int rm_eval_select_key(RmGraph* g, const void* orders, int64_t B, int64_t id_bas
                        uint32_t flags, int64_t* peak, int32_t* argmax, uint8_t* valid,
                        int64_t* out_key, void* stream);
 
+/* Multi-GPU selection exchange (one process per GPU): each rank's
+ * rm_eval_select_key key (device int64[1], (peak << id_bits) | global id,
+ * INT64_MAX when the rank has no valid candidate) becomes the global first
+ * strict minimum on every rank with ONE 8-byte ncclAllReduce(MIN), async on
+ * stream (replaces the planner's sequential first-strict-min scan,
+ * planner.py:209-216, across ranks).  NCCL is dlopen'ed (libnccl.so.2) on
+ * first use; the communicator comes from rm_nccl_comm_init (rank 0 makes the
+ * id with rm_nccl_unique_id and ships its RM_NCCL_ID_BYTES to the others) or
+ * is any ncclComm_t the host already has. */
+#define RM_NCCL_ID_BYTES 128
+int rm_nccl_unique_id(uint8_t* id, int64_t id_bytes);
+int rm_nccl_comm_init(int32_t nranks, const uint8_t* id, int32_t rank, void** comm);
+int rm_nccl_comm_destroy(void* comm);
+int rm_nccl_select_key(void* comm, int64_t* key_dev, void* stream);
+
 /* Counter-RNG candidate generator: row c is the Kahn topological order that
  * breaks ties by the smallest (splitmix64(seed ^ splitmix64(id)) ^ op, op)
  * key with id = first_id + c (oracle: oracle/memplan_oracle.py kahn_candidate).

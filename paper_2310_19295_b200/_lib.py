@@ -21,7 +21,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB_PATH = PKG / "libroam.so"
-SOURCES = ("roam_graph.cpp", "layout_search.cpp", "order_search.cpp", "wu_place.cpp", "k_eval.cu", "k_eval_v2.cu", "k_eval_v4.cu", "k_eval_v5.cu", "k_gen.cu", "k_layout.cu", "k_repair.cu", "k_pack.cu", "k_greedy.cu", "k_exact.cu")
+SOURCES = ("roam_graph.cpp", "layout_search.cpp", "order_search.cpp", "wu_place.cpp", "nccl_select.cpp", "k_eval.cu", "k_eval_v2.cu", "k_eval_v4.cu", "k_eval_v5.cu", "k_gen.cu", "k_layout.cu", "k_repair.cu", "k_pack.cu", "k_greedy.cu", "k_exact.cu")
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 
 
@@ -63,7 +63,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     with ThreadPoolExecutor(max_workers=len(srcs)) as ex:
         objs = list(ex.map(compile_one, srcs))
     tmp = LIB_PATH.with_suffix(".so.tmp")
-    r = subprocess.run([nvcc, ARCH, "-shared", "-o", str(tmp)] + [str(o) for o in objs],
+    r = subprocess.run([nvcc, ARCH, "-shared", "-o", str(tmp)] + [str(o) for o in objs] + ["-ldl"],
                        capture_output=True, text=True)
     if r.returncode != 0:
         raise RoamError(f"nvcc link failed:\n{r.stderr}")
@@ -143,6 +143,10 @@ SIGNATURES = {
     "rm_set_k1_variant": (C.c_int, [C.c_int]),
     "rm_set_sm_reserve": (C.c_int, [C.c_int]),
     "rm_set_gen_form": (C.c_int, [C.c_int]),
+    "rm_nccl_unique_id": (C.c_int, [vp, C.c_int64]),
+    "rm_nccl_comm_init": (C.c_int, [C.c_int32, vp, C.c_int32, C.POINTER(vp)]),
+    "rm_nccl_comm_destroy": (C.c_int, [vp]),
+    "rm_nccl_select_key": (C.c_int, [vp, vp, vp]),
     "rm_graph_asap_alap": (C.c_int, [vp, vp, vp]),
     "rm_graph_ancestors": (C.c_int, [vp, vp]),
     "rm_eval_select_key": (C.c_int, [vp, vp, C.c_int64, C.c_int64, C.c_int32, C.c_uint32, vp, vp, vp, vp, vp]),

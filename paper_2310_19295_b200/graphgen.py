@@ -78,11 +78,15 @@ class TransformerShape:
     batch: int
     vocab: int
     decoder: bool          # GPT (pre-LN, causal mask, tanh GELU) vs BERT (post-LN, erf GELU)
+    traced: bool = False   # op granularity of a traced eager training step: LayerNorm as its
+                           # aten decomposition, Adam's per-parameter update unfused
 
 
 GPT2_SMALL = TransformerShape("gpt2-small", 12, 768, 12, 1024, 8, 50257, True)
 BERT_LARGE = TransformerShape("bert-large", 24, 1024, 16, 512, 8, 30522, False)
-GPT2_XL = TransformerShape("gpt2-xl", 48, 1600, 25, 1024, 1, 50257, True)
+# GPT2-XL at the paper's granularity (">10 thousand operators"):
+# 10,544 ops / 10,290 tensors
+GPT2_XL = TransformerShape("gpt2-xl", 48, 1600, 25, 1024, 1, 50257, True, traced=True)
 SHAPES = {s.name: s for s in (GPT2_SMALL, BERT_LARGE, GPT2_XL)}
 
 
@@ -152,7 +156,24 @@ class _Builder:
                               gouts + [resolve(i) for i in saved], [gx])
                     grads.setdefault(x, []).append(gx)
 
-    def adam(self) -> None:
+    def adam(self, traced: bool = False) -> None:
+        if traced:
+            # torch.optim.Adam (foreach=False) as traced per parameter:
+            # exp_avg.mul_(b1).add_(g, alpha=1-b1); exp_avg_sq.mul_(b2).addcmul_(g, g,
+            # value=1-b2); denom = (exp_avg_sq.sqrt() / bc2_sqrt).add_(eps);
+            # param.addcdiv_(exp_avg, denom, value=-step_size)
+            for k, (_pname, gw) in enumerate(self.params):
+                sz = self.sizes[gw]
+                m1, m2, v1, v2, sq, dn, de = (self.tensor(sz) for _ in range(7))
+                self.emit(f"adam.m_mul{k}", "weight_update", [gw], [m1])
+                self.emit(f"adam.m_add{k}", "weight_update", [m1, gw], [m2])
+                self.emit(f"adam.v_mul{k}", "weight_update", [gw], [v1])
+                self.emit(f"adam.v_addcmul{k}", "weight_update", [v1, gw], [v2])
+                self.emit(f"adam.sqrt{k}", "weight_update", [v2], [sq])
+                self.emit(f"adam.div{k}", "weight_update", [sq], [dn])
+                self.emit(f"adam.add_eps{k}", "weight_update", [dn], [de])
+                self.emit(f"adam.addcdiv{k}", "weight_update", [m2, de], [])
+            return
         # one 4-op branch per parameter gradient, reference graphgen.py:63-74
         for k, (_pname, gw) in enumerate(self.params):
             sz = self.sizes[gw]
@@ -182,6 +203,16 @@ def transformer_training_doc(shape: TransformerShape) -> dict:
     x = b.fwd("embed.add", [wte, wpe], [act], rule=[(0, []), (1, [])])[0]
 
     def layer_norm(pfx: str, x: int) -> int:
+        if shape.traced:   # aten decomposition of native_layer_norm
+            mu = b.fwd(f"{pfx}.mean", [x], [B * S * f4], rule=[(0, [])])[0]
+            xc = b.fwd(f"{pfx}.sub", [x, mu], [act], rule=[(0, []), (1, [])])[0]
+            sq = b.fwd(f"{pfx}.pow", [xc], [act], rule=[(0, [0])])[0]
+            var = b.fwd(f"{pfx}.var", [sq], [B * S * f4], rule=[(0, [])])[0]
+            ve = b.fwd(f"{pfx}.add_eps", [var], [B * S * f4], rule=[(0, [])])[0]
+            rs = b.fwd(f"{pfx}.rsqrt", [ve], [B * S * f4], rule=[(0, [OUT(0)])])[0]
+            xhat = b.fwd(f"{pfx}.mul", [xc, rs], [act], rule=[(0, [1]), (1, [0])])[0]
+            y = b.fwd(f"{pfx}.mul_gamma", [xhat], [act], rule=[(("gamma", D * f4), [0]), (0, [])])[0]
+            return b.fwd(f"{pfx}.add_beta", [y], [act], rule=[(("beta", D * f4), []), (0, [])])[0]
         mu = b.fwd(f"{pfx}.mean", [x], [B * S * f4], rule=[(0, [])])[0]
         var = b.fwd(f"{pfx}.var", [x, mu], [B * S * f4], rule=[(0, [0, 1])])[0]
         xhat = b.fwd(f"{pfx}.normalize", [x, mu, var], [act], rule=[(0, [OUT(0), 2])])[0]
@@ -263,7 +294,7 @@ def transformer_training_doc(shape: TransformerShape) -> dict:
     b.fwd("loss.nll", [lsm, labels], [f4], rule=[(0, [1])], kind="loss")
     # the loss op emits the seed gradient d(loss)/d(log_softmax) ...
     b.backward(lsm, B * S * V * f4)
-    b.adam()
+    b.adam(shape.traced)
     return b.doc()
 
 

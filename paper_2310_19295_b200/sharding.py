@@ -126,3 +126,44 @@ def evaluate_sharded(g, total: int, seed: int = 0, group=None, stream=None,
         best = allgather_best(best, group)
     b = [int(x) for x in best.cpu().tolist()]
     return ShardResult(b[0], b[1], (lo, hi), int(n_valid.item()))
+
+
+class NcclSelect:
+    """libroam's own selection exchange (rm_nccl_select_key): an NCCL
+    communicator over the ranks and one 8-byte ncclAllReduce(MIN) of each
+    rank's packed key, for hosts that do not run torch.distributed (the
+    C-ABI path a C/C++ planner host binds).  ``uid`` is rank 0's
+    ``NcclSelect.unique_id()``, shipped to the other ranks out of band."""
+
+    def __init__(self, nranks: int, uid: bytes, rank: int):
+        import ctypes as C
+
+        from ._lib import check, lib
+        self._lib = lib()
+        buf = (C.c_uint8 * len(uid)).from_buffer_copy(uid)
+        comm = C.c_void_p()
+        check(self._lib.rm_nccl_comm_init(int(nranks), buf, int(rank), C.byref(comm)), "rm_nccl_comm_init")
+        self.comm = comm
+
+    @staticmethod
+    def unique_id() -> bytes:
+        import ctypes as C
+
+        from ._lib import check, lib
+        buf = (C.c_uint8 * 128)()
+        check(lib().rm_nccl_unique_id(buf, 128), "rm_nccl_unique_id")
+        return bytes(buf)
+
+    def select(self, key, stream=None):
+        """In place: key (device int64[1]) <- the min over the ranks' keys."""
+        from ._lib import check
+        from .evaluator import _stream_handle
+        check(self._lib.rm_nccl_select_key(self.comm, key.data_ptr(), _stream_handle(stream)),
+              "rm_nccl_select_key")
+        return key
+
+    def close(self):
+        from ._lib import check
+        if self.comm:
+            check(self._lib.rm_nccl_comm_destroy(self.comm), "rm_nccl_comm_destroy")
+            self.comm = None

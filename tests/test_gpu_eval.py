@@ -418,3 +418,36 @@ def test_host_staged_calls_from_two_threads():
     for w, r in zip(want, got):
         assert np.array_equal(w[0], r[0]) and np.array_equal(w[1], r[1])
         assert np.array_equal(w[2], r[2]) and w[3] == r[3]
+
+
+def test_nccl_select_key_single_rank():
+    """rm_nccl_select_key through a one-rank NCCL communicator made by
+    libroam itself (rm_nccl_unique_id / rm_nccl_comm_init): the fused K1 key
+    survives the 8-byte all-reduce(MIN) unchanged and decodes to the oracle's
+    first strict minimum; a rank with no valid candidate (INT64_MAX) loses."""
+    import torch
+
+    from paper_2310_19295_b200.evaluator import evaluate_select_key
+    from paper_2310_19295_b200.sharding import NcclSelect
+    g = load_graph(gg.config_doc("layered"))
+    orders = generate_orders(g, 3, 0, 700)
+    host = orders.cpu().numpy()
+    host[5] = host[6]                                  # an invalid row
+    orders = torch.from_numpy(host).cuda()
+    id_bits = 20
+    _, _, _, key = evaluate_select_key(g, orders, 0, id_bits)
+    want = coracle.eval_orders(coracle.CGraph(g), host)
+    best = O.first_strict_min(want[0].tolist(), want[2].tolist())
+    sel = NcclSelect(1, NcclSelect.unique_id(), 0)
+    try:
+        k = key.clone()
+        sel.select(k)
+        torch.cuda.synchronize()
+        assert int(k.item()) == int(key.item())
+        assert (int(k.item()) >> id_bits, int(k.item()) & ((1 << id_bits) - 1)) == best
+        none = torch.full((1,), 2**63 - 1, dtype=torch.int64, device="cuda")
+        sel.select(none)
+        torch.cuda.synchronize()
+        assert int(none.item()) == 2**63 - 1
+    finally:
+        sel.close()
