@@ -1,5 +1,5 @@
 """BASELINE config 5 at its full size on one GPU: 1,048,576 counter-RNG Kahn
-candidate orders on the GPT2-XL graph (7,437 ops), evaluated in chunks with
+candidate orders on the GPT2-XL graph (11,217 ops), evaluated in chunks with
 the first strict minimum kept on the device.  Size-independent checks: every
 generated row is a valid schedule, the winner re-evaluated by the C oracle
 has exactly the reported peak, the result does not depend on the chunking,
