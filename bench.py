@@ -546,9 +546,8 @@ def main() -> None:
                        "generation_ms": gen_ms},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "frac_of_8tbs_nominal": achieved / 8000.0, "traffic": traffic,
-                         "kernel": {5: "k1v5_eval_orders", 4: "k1v4_eval_orders", 3: "k1v3_eval_orders",
-                                    2: "k1v2_eval_orders"}.get(info["k1_variant"],
-                                                                                    "k1_eval_orders"),
+                         "kernel": {5: "k1v5_eval_orders", 4: "k1v4_eval_orders"}.get(info["k1_variant"],
+                                                                                      "k1_eval_orders"),
                          "k1_ms": k1_avg,
                          "k1_ms_is": ("back-to-back K1 throughput: the launching stream's interval over the K "
                                       "launches / K (" + ("selection fused into each K1 launch; " if use_key

@@ -78,7 +78,7 @@ typedef struct {
   int32_t reduced;          /* 1 when the reduction ran */
   int32_t wide_index;       /* 1 when ids need int32 (n > 65535) */
   int64_t total_bytes;      /* sum of |size| */
-  int32_t k1_variant;       /* default K1: 4 v4, 3 pairs, 2 unit-packed interleaved, 1 generic */
+  int32_t k1_variant;       /* default K1: 5 v5 (class bytes), 4 v4, 1 generic */
   int32_t unit_shift;       /* K1 v2 byte unit = 2^unit_shift */
 } RmGraphInfo;
 
@@ -375,11 +375,10 @@ int64_t rm_launch_count(void);
  * timing was requested through rm_set_timing(1); -1 if unavailable. */
 int rm_set_timing(int enable);
 /* Force the K1 evaluator variant on this thread: 0 auto (v5, else v4, else
- * v3 pairs / v2, else generic), 1 the generic evaluator, 2 v2 (one candidate
- * per group), 3 v3 (two candidates per group), 4 v4 (sentinel permutation
- * check, SIMD edge checks), 5 v5 (v4's checks, one dynamic class byte per
- * position), 6 v5 with rows staged by cp.async.bulk; unsupported choices
- * fall back.  For tests and A/B measurement. */
+ * generic), 1 the generic evaluator, 4 v4 (sentinel permutation check, SIMD
+ * edge checks), 5 v5 (v4's checks, one dynamic class byte per position), 6 v5
+ * with rows staged by cp.async.bulk; unsupported choices (and 2, 3: the
+ * retired v2/v3) fall back.  For tests and A/B measurement. */
 int rm_set_k1_variant(int variant);
 /* Leave `sms` SMs idle in every K1 launch of this process (default 0), so a
  * collective issued on another stream (the multi-GPU selection exchange) runs

@@ -21,7 +21,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB_PATH = PKG / "libroam.so"
-SOURCES = ("roam_graph.cpp", "layout_search.cpp", "order_search.cpp", "wu_place.cpp", "nccl_select.cpp", "k_eval.cu", "k_eval_v2.cu", "k_eval_v4.cu", "k_eval_v5.cu", "k_gen.cu", "k_layout.cu", "k_repair.cu", "k_pack.cu", "k_greedy.cu", "k_exact.cu")
+SOURCES = ("roam_graph.cpp", "layout_search.cpp", "order_search.cpp", "wu_place.cpp", "nccl_select.cpp", "k_eval.cu", "k_eval_v4.cu", "k_eval_v5.cu", "k_gen.cu", "k_layout.cu", "k_repair.cu", "k_pack.cu", "k_greedy.cu", "k_exact.cu")
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 
 

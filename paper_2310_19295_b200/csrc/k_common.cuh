@@ -47,13 +47,9 @@ inline int sm_count(int dev) {
 // collective launched on another stream finds an idle SM while K1 runs
 inline int64_t k1_sms(int dev) { return std::max<int64_t>(1, sm_count(dev) - g_sm_reserve); }
 
-// K1 v2/v3 (k_eval_v2.cu): returns 1 when the graph does not fit the layout
-// (the caller falls back to the generic evaluator).  u16_rows: orders are
-// uint16[B, n] instead of int32[B, n].
-int launch_k1v2(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, int32_t* argmax,
-                uint8_t* valid, cudaStream_t s, bool pairs, bool u16_rows);
-
-// K1 v4 (k_eval_v4.cu): same contract; returns 1 when g->k4v.ok == 0.
+// K1 v4 (k_eval_v4.cu): returns 1 when g->k4v.ok == 0 (the caller falls
+// back to the generic evaluator).  u16_rows: orders are uint16[B, n] instead
+// of int32[B, n].
 // Fused selection: K1 v4 also reduces the packed key (peak << id_bits) |
 // (id_base + c) of the first strict minimum over valid candidates into
 // *key_out (INT64_MAX when none is valid), via per-group partials and a

@@ -474,7 +474,7 @@ static int launch_k1_idx(K1Args& a, int maxc, int grid, size_t smem, cudaStream_
   return fail(RM_ERR_CAPACITY, "K1: positions per thread exceed 64");
 }
 
-static thread_local int t_force_variant = 0;  // 0 auto, 1 generic, 2 v2, 3 v3 (pairs), 4 v4
+static thread_local int t_force_variant = 0;  // 0 auto, 1 generic, 4 v4, 5 v5, 6 v5 with bulk-copied rows
 
 // Launch geometry: NT threads per candidate group, G groups per CTA, one
 // CTA per SM.  Shared memory bounds G; NT keeps ~8-16 positions per thread.
@@ -506,18 +506,6 @@ int launch_k1(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, int3
       if (fused) *fused = sel != nullptr && rc == RM_OK;
       return rc;
     }
-  }
-  if (g->k2v.ok && t_force_variant != 1) {
-    // v3 (pairs) wins on small graphs; from ~1k ops its doubled per-group
-    // shared memory costs more occupancy than the shared gathers save
-    // (tools/k1_ab.py: layered 1k ops 0.088 vs 0.100 ms; GPT-2 small 0.127 vs
-    // 0.113 ms)
-    if (t_force_variant == 3 || ((t_force_variant == 0 || t_force_variant >= 4) && g->n <= 1024)) {
-      const int rc = launch_k1v2(g, orders_dev, B, peak, argmax, valid, s, true, u16_rows);
-      if (rc != 1) return rc;
-    }
-    const int rc = launch_k1v2(g, orders_dev, B, peak, argmax, valid, s, false, u16_rows);
-    if (rc != 1) return rc;
   }
   if (!u16_rows)
     return launch_k1_int32(g, static_cast<const int32_t*>(orders_dev), B, peak, argmax, valid, s);

@@ -8,6 +8,7 @@
 //                              (horizon if none), clamped >= birth
 //   validate_schedule 375-398 permutation + preds-before
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <climits>
 #include <cstdlib>
@@ -210,6 +211,58 @@ static bool k1v4_geometry(int n, bool classes, int& NT, int& C) {
   return false;
 }
 
+// Bank-aware lane assignment for the per-candidate gather lists (v4/v5):
+// entry e of a list sits at slot tid + i * NT, and the 32 slots of one
+// (warp, i) are one shared-memory instruction per address they touch.
+// bank[e][c] = the bank (address class) entry e touches in access c of that
+// instruction; lanes sharing a bank with different words serialise.  Groups
+// of 32 are filled greedily with the entry adding the fewest collisions
+// (ties: the lowest index), then laid out group by group.  Order never
+// matters to the kernels (every entry's result is OR-ed / atomically added).
+template <int NC>
+static std::vector<size_t> bank_aware_order(const std::vector<std::array<int, NC>>& bank, int NT) {
+  const size_t E = bank.size();
+  std::vector<size_t> out;
+  if (E == 0 || NT % 32) {
+    for (size_t e = 0; e < E; ++e) out.push_back(e);
+    return out;
+  }
+  const size_t rounds = (E + NT - 1) / NT, warps = size_t(NT) / 32;
+  std::vector<std::vector<size_t>> groups(rounds * warps);
+  std::vector<char> used(E, 0);
+  size_t left = E;
+  for (size_t gi = 0; gi < groups.size() && left; ++gi) {
+    int cnt[NC][32] = {};
+    for (int lane = 0; lane < 32 && left; ++lane) {
+      size_t best = E;
+      int best_cost = 1 << 30;
+      for (size_t e = 0; e < E; ++e) {
+        if (used[e]) continue;
+        int cost = 0;
+        for (int c = 0; c < NC; ++c) cost += bank[e][c] >= 0 ? cnt[c][bank[e][c]] : 0;
+        if (cost < best_cost) {
+          best_cost = cost;
+          best = e;
+          if (cost == 0) break;
+        }
+      }
+      used[best] = 1;
+      --left;
+      for (int c = 0; c < NC; ++c)
+        if (bank[best][c] >= 0) cnt[c][bank[best][c]]++;
+      groups[gi].push_back(best);
+    }
+  }
+  // group (i, w) -> slots w*32 + lane + i*NT
+  out.assign(rounds * size_t(NT), E);
+  for (size_t i = 0; i < rounds; ++i)
+    for (size_t w = 0; w < warps; ++w) {
+      const auto& gr = groups[i * warps + w];
+      for (size_t l = 0; l < gr.size(); ++l) out[w * 32 + l + i * size_t(NT)] = gr[l];
+    }
+  return out;  // E marks an empty slot
+}
+
 // K1 v4 metadata (see roam_internal.h); needs the v2 layout (unit-packed
 // opv, 32-bit free fields) and 15-bit positions.
 static void build_k1v4_host(RmGraph& g) {
@@ -226,6 +279,16 @@ static void build_k1v4_host(RmGraph& g) {
     if (v - u != 1 && v - u != 2) gen.push_back((uint32_t)(2 * u) | ((uint32_t)(2 * v) << 16));
   }
   if (!gen.empty()) {
+    // lanes of one gather instruction on distinct banks (pos is u16: id u at
+    // byte 2u, bank (u >> 1) & 31); empty slots repeat the first edge (a
+    // broadcast, no conflict); the list is padded to a multiple of 4 * NT
+    std::vector<std::array<int, 2>> bank(gen.size());
+    for (size_t e = 0; e < gen.size(); ++e)
+      bank[e] = {int(((gen[e] & 0xffffu) >> 2) & 31), int(((gen[e] >> 16) >> 2) & 31)};
+    const std::vector<size_t> ord = bank_aware_order<2>(bank, NT);
+    std::vector<uint32_t> laid(ord.size());
+    for (size_t k = 0; k < ord.size(); ++k) laid[k] = ord[k] < gen.size() ? gen[ord[k]] : gen[0];
+    gen = laid;
     const size_t pad = 4 * size_t(NT);
     const uint32_t first = gen[0];
     while (gen.size() % pad) gen.push_back(first);
@@ -352,20 +415,22 @@ static void build_k1v5_host(RmGraph& g) {
     }
   }
   while ((g.h5_g4.size() / 2) % NT) g.h5_g4.push_back(0xe000e000u);
-  // lane interleave: slot tid + i*NT holds pair tid*pk + i, so the lanes of a
-  // warp touch pairs pk apart (nearby pairs share class-byte words, and
-  // same-word atomics from one instruction serialise); padding slots read
-  // pos[0] and hold target 0xffffffff, which the kernel predicates off
-  const size_t P = pw.size(), pk = (P + NT - 1) / NT;
-  g.h5_dpair.assign(pk * NT, 0u);
-  g.h5_dtgt.assign(pk * NT, 0xffffffffu);
-  for (size_t i = 0; i < pk; ++i)
-    for (int t = 0; t < NT; ++t) {
-      const size_t src = size_t(t) * pk + i, dst = size_t(t) + i * NT;
-      if (src < P) {
-        g.h5_dpair[dst] = pw[src];
-        g.h5_dtgt[dst] = pt[src];
-      }
+  // bank-aware lanes: the lanes of one instruction gather pos[a], pos[b]
+  // from distinct banks and add to distinct class words / banks (same-word
+  // atomics from one instruction serialise); padding slots read pos[0] and
+  // hold target 0xffffffff, which the kernel predicates off
+  const size_t P = pw.size();
+  std::vector<std::array<int, 4>> bank(P);
+  for (size_t e = 0; e < P; ++e)
+    bank[e] = {int(((pw[e] & 0xffffu) >> 2) & 31), int(((pw[e] >> 16) >> 2) & 31), int((pt[e] & 0x7ffu) & 31),
+               int(((pt[e] >> 16) & 0x7ffu) & 31)};
+  const std::vector<size_t> ord = bank_aware_order<4>(bank, NT);
+  g.h5_dpair.assign(ord.size(), 0u);
+  g.h5_dtgt.assign(ord.size(), 0xffffffffu);
+  for (size_t k = 0; k < ord.size(); ++k)
+    if (ord[k] < P) {
+      g.h5_dpair[k] = pw[ord[k]];
+      g.h5_dtgt[k] = pt[ord[k]];
     }
   g.h5_base = base;
   g.h5_tab = tab;
@@ -480,7 +545,7 @@ static int build_k1_host(RmGraph& g, bool allow_reduce) {
   build_k1v5_host(g);
 
   RmGraphInfo& I = g.info;
-  I.k1_variant = g.k5v.ok ? 5 : g.k4v.ok ? 4 : g.k2v.ok ? (g.n <= 1024 ? 3 : 2) : 1;
+  I.k1_variant = g.k5v.ok ? 5 : g.k4v.ok ? 4 : 1;
   I.unit_shift = g.k2v.shift;
   I.n_check_edges = (int64_t)g.h_edge_u.size();
   I.n_multi = (int64_t)g.h_msize.size();

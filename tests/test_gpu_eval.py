@@ -179,17 +179,18 @@ def test_reference_unit_answers_through_gpu():
         sequential_schedule(d, (3, 0, 1, 2))
 
 
-@pytest.mark.parametrize("variant", [1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("variant", [1, 4, 5, 6])
 @pytest.mark.parametrize("name", ["layered", "gpt2-small", "bert-large", "gpt2-xl"])
 def test_both_k1_variants_vs_c_oracle(name, variant):
     """Every K1 variant -- v5 (dynamic class bytes, the default on the training
-    graphs), v4 (the default where the classes do not fit: layered), v2/v3 and
-    the generic v1 -- agrees with the oracle, including on corrupted rows
+    graphs up to 8k ops), v4 (the default where the classes do not fit --
+    layered -- and on the 11k-op GPT2-XL), v5 with bulk-copied rows and the
+    generic v1 -- agrees with the oracle, including on corrupted rows
     (invalid -> valid=False)."""
     from paper_2310_19295_b200.evaluator import device_graph, set_k1_variant
     g = load_graph(gg.config_doc(name))
-    assert device_graph(g).info()["k1_variant"] == (4 if name == "layered" else 5)
-    B = 1501                                    # odd: the last v3 pair has no partner
+    assert device_graph(g).info()["k1_variant"] == (4 if name in ("layered", "gpt2-xl") else 5)
+    B = 1501
     host = generate_orders(g, 7, 0, B).cpu().numpy()
     rng = np.random.default_rng(0)
     n = len(g.ops)
@@ -251,7 +252,7 @@ def test_packed_key_selection_matches_first_strict_min():
     assert decode_key(none, bits) == (2**63 - 1, -1)
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("variant", [0, 1, 4, 5, 6])
 def test_uint16_rows_match_int32(variant):
     """uint16 rows (RM_ORDERS_U16) give exactly the int32 results on every
     evaluator, host-staged and device-resident."""
@@ -312,7 +313,7 @@ def test_random_hazard_graphs_vs_oracle(seed):
             rng.shuffle(perm)
             rows.append(perm)
         orders = np.array(rows, np.int64).reshape(len(rows), n)
-        for variant in (0, 1, 2, 3, 4, 5):
+        for variant in (0, 1, 4, 5):
             from paper_2310_19295_b200.evaluator import set_k1_variant
             set_k1_variant(variant)
             try:
@@ -326,7 +327,7 @@ def test_random_hazard_graphs_vs_oracle(seed):
                     assert (int(peak[k]), int(arg[k])) == want[:2], (seed, trial, variant, row)
 
 
-@pytest.mark.parametrize("variant", [0, 2, 4, 6])
+@pytest.mark.parametrize("variant", [0, 1, 4, 6])
 @pytest.mark.parametrize("name", ["layered", "gpt2-small", "bert-large", "gpt2-xl"])
 def test_fused_key_selection(name, variant):
     """K1 with the packed-key selection fused into the launch (v4) or chained
