@@ -59,6 +59,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=3.0, help="wall budget of the CPU baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/cpu)")
+    ap.add_argument("--k1-variant", type=int, default=0, help="A/B: rm_set_k1_variant (0 = auto)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo lets N ranks share one GPU to exercise the N>1 path (testing only)")
     return ap.parse_args()
@@ -305,6 +306,8 @@ def main() -> None:
     B = args.batch or DEFAULT_BATCH[args.config]
     g = graph_for(args.config)
     dg = ev.device_graph(g)
+    if args.k1_variant:
+        ev.set_k1_variant(args.k1_variant)
     info = dg.info()
     n = info["n_ops"]
     first_id, _ = shard_range(world * B, world, rank)   # weak scaling: B ids per rank
