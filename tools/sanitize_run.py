@@ -5,7 +5,8 @@ Covers K1 (default variant and the generic v1, int32 and uint16 rows,
 corrupted rows, the fused packed-key selection launched back to back so
 programmatic dependent launch overlaps the launches), the generator, the
 argmin kernels, the single-schedule kernels, K2, K3 (plain, constrained,
-components), K4, K5 and the whole plug-in path through the reference's own
+components), K4, K5, the thread- and warp-form generators, the
+repair_conflicts rounds and the whole plug-in path through the reference's own
 plan() on small graphs.  Sizes are small: racecheck slows shared-memory
 kernels by two to three orders of magnitude."""
 
@@ -48,6 +49,12 @@ def main(which: str = "all") -> None:
         ev.evaluate_orders(g, bad)
         ev.set_k1_variant(0)
         torch.cuda.synchronize()
+    if which in ("all", "gen"):
+        # the thread-per-candidate generator, and the warp form it hands the
+        # rows over to (layered: ready sets above the heap's capacity)
+        ev.generate_orders(g, 3, 0, 64)
+        ev.generate_orders(load_graph(gg.layered_dag_doc(layers=12, width=20)), 3, 0, 40)
+        torch.cuda.synchronize()
     if which in ("all", "plan"):
         mp = plug.load_memplan()
         small = [mp.graph.load_graph(gg.layered_dag_doc(layers=6, width=8)),
@@ -64,6 +71,9 @@ def main(which: str = "all") -> None:
             lay.pack_batch([items, items[:40]], mode)
         offs = {i.tensor: (13 * i.tensor) % 50 for i in items}
         lay.layout_violations(items, offs, 40)
+        # repair_conflicts: device pair test + mover election over several rounds
+        lay.repair_conflicts(mp.layout.MemoryLayout(offsets=offs, capacity=60),
+                             mp.layout.LayoutProblem(items=tuple(items)))
     torch.cuda.synchronize()
     print(f"sanitize_run {which} ok; libroam launches={ev.launch_count()}")
 
