@@ -104,6 +104,12 @@ int rm_graph_k1_export(const RmGraph* g, int32_t* vidx, int32_t* slot, int64_t* 
  * helpers of the planner plug-in (region filters, linearisation ranks). */
 int rm_graph_ancestors(const RmGraph* g, uint64_t* rows);
 
+/* counts[r] = popcount(rows[r] & mask) over `words` 64-bit words per row (mask
+ * NULL = all bits): the masked ancestor counts of the plug-in's tree build
+ * (segmentation.py:108-117 _mi_over, 408-418 residual ranks).  Host-only. */
+int rm_popcount_rows(const uint64_t* rows, int64_t n_rows, int64_t words, const uint64_t* mask,
+                     int64_t* counts);
+
 /* Schedule bounds (replaces graph.py:365-372 asap_alap): asap[v] = number of
  * transitive predecessors, alap[v] = n-1 - number of transitive successors,
  * from closure bitsets in C++.  Host-only (no device needed); control-plane

@@ -149,6 +149,7 @@ SIGNATURES = {
     "rm_nccl_select_key": (C.c_int, [vp, vp, vp]),
     "rm_graph_asap_alap": (C.c_int, [vp, vp, vp]),
     "rm_graph_ancestors": (C.c_int, [vp, vp]),
+    "rm_popcount_rows": (C.c_int, [vp, C.c_int64, C.c_int64, vp, vp]),
     "rm_eval_select_key": (C.c_int, [vp, vp, C.c_int64, C.c_int64, C.c_int32, C.c_uint32, vp, vp, vp, vp, vp]),
     "rm_last_kernel_ms": (C.c_double, []),
 }

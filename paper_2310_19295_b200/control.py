@@ -43,11 +43,26 @@ def closure(g) -> dict:
             check(lib().rm_graph_ancestors(dg.handle, ptr(rows)), "rm_graph_ancestors")
         anc = rows.view(np.uint8).reshape(n, -1)
         a = graph_arrays(g)
-        c = {"n": n, "anc": anc, "count": np.bitwise_count(anc).sum(axis=1, dtype=np.int64),
+        c = {"n": n, "anc": anc, "rows": rows, "count": masked_counts(rows, None),
              "producer": np.asarray(a.producer, np.int64),
              "cons_ptr": np.asarray(a.cons_ptr, np.int64), "cons_idx": np.asarray(a.cons_idx, np.int64)}
         ent["closure"] = c
     return c
+
+
+def masked_counts(rows, mask_bytes, sel=None) -> np.ndarray:
+    """popcount(row & mask) per row of a uint64 bit matrix (rm_popcount_rows,
+    C++): mask_bytes a little-endian uint8 bitmask (None = all bits), sel an
+    optional row index array."""
+    r = rows if sel is None else np.ascontiguousarray(rows[sel])
+    out = np.empty(r.shape[0], np.int64)
+    m = None
+    if mask_bytes is not None:
+        mb = np.zeros(r.shape[1] * 8, np.uint8)
+        mb[:len(mask_bytes)] = mask_bytes
+        m = mb.view(np.uint64)
+    check(lib().rm_popcount_rows(ptr(r), r.shape[0], r.shape[1], ptr(m), ptr(out)), "rm_popcount_rows")
+    return out
 
 
 def _bit(anc, rows, cols):
@@ -184,7 +199,7 @@ def _mi_full(g, c):
     mimask = np.zeros(anc.shape[1] * 8, bool)
     if mi:
         mimask[np.asarray(mi, np.int64)] = True
-    gap = np.bitwise_count(anc & np.packbits(mimask, bitorder="little")).sum(axis=1, dtype=np.int64)
+    gap = masked_counts(c["rows"], np.packbits(mimask, bitorder="little"))
     return mi, mi_mask, gap
 
 
@@ -263,7 +278,7 @@ def subgraph_tree_factory(mp):
         # _mi_over(g, core) (segmentation.py:108-117): ancestors within the core
         # + descendants within the core == |core| - 1, ordered by position
         cbytes = np.packbits(np.append(is_core, np.zeros(anc.shape[1] * 8 - n, bool)), bitorder="little")
-        n_anc = np.bitwise_count(anc & cbytes).sum(axis=1, dtype=np.int64)
+        n_anc = masked_counts(c["rows"], cbytes)
         # descendants within the core = all descendants (n-1-alap, libroam C++)
         # minus the floating ones (column sums over the few floating rows)
         from .evaluator import asap_alap
@@ -287,7 +302,7 @@ def subgraph_tree_factory(mp):
         mimask = np.zeros(anc.shape[1] * 8, bool)
         if mi_core:
             mimask[np.asarray(mi_core, np.int64)] = True
-        gap = np.bitwise_count(anc & np.packbits(mimask, bitorder="little")).sum(axis=1, dtype=np.int64)
+        gap = masked_counts(c["rows"], np.packbits(mimask, bitorder="little"))
         other = np.nonzero(is_core & ~mi_mask)[0]
         order = np.argsort(gap[other], kind="stable")
         bucket_ops = other[order]
@@ -354,7 +369,7 @@ def subgraph_tree_factory(mp):
             umask = np.zeros(anc.shape[1] * 8, bool)
             if sorted_used:
                 umask[np.asarray(sorted_used, np.int64)] = True
-            rank = np.bitwise_count(anc[unc] & np.packbits(umask, bitorder="little")).sum(axis=1)
+            rank = masked_counts(c["rows"], np.packbits(umask, bitorder="little"), sel=unc)
             for r in sorted(set(rank.tolist())):
                 lo = sorted_used[r - 1] if r > 0 else None
                 hi = sorted_used[r] if r < len(sorted_used) else None
@@ -498,7 +513,7 @@ def _linearize_factory(mp):
         if boundaries:
             bmask[np.asarray(boundaries, np.int64)] = True
         bbytes = np.packbits(bmask, bitorder="little")
-        rank = np.bitwise_count(anc & bbytes).sum(axis=1, dtype=np.int64) if n else np.zeros(0, np.int64)
+        rank = masked_counts(c["rows"], bbytes) if n else np.zeros(0, np.int64)
         skip = np.zeros(n, bool)
         for v in boundary_set | floating:
             skip[v] = True

@@ -796,6 +796,22 @@ int rm_graph_k1_export(const RmGraph* g, int32_t* vidx, int32_t* slot, int64_t* 
   return RM_OK;
 }
 
+int rm_popcount_rows(const uint64_t* rows, int64_t n_rows, int64_t words, const uint64_t* mask,
+                     int64_t* counts) {
+  if (n_rows < 0 || words < 0 || (n_rows > 0 && (!rows || !counts)))
+    return fail(RM_ERR_INVALID_ARG, "bad rm_popcount_rows arguments");
+  for (int64_t r = 0; r < n_rows; ++r) {
+    const uint64_t* row = rows + r * words;
+    int64_t c = 0;
+    if (mask)
+      for (int64_t i = 0; i < words; ++i) c += __builtin_popcountll(row[i] & mask[i]);
+    else
+      for (int64_t i = 0; i < words; ++i) c += __builtin_popcountll(row[i]);
+    counts[r] = c;
+  }
+  return RM_OK;
+}
+
 int rm_graph_ancestors(const RmGraph* g, uint64_t* rows) {
   // rows[v * words + i]: bit j of word i set iff op 64*i+j is a transitive
   // predecessor of v (graph.py:335-347 predecessor_masks as bitsets), words =
