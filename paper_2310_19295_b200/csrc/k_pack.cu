@@ -232,7 +232,7 @@ struct K3Block {
   }
 };
 
-template <int NT, int MAXC>
+template <int NT, int MAXC, int MS = 0>
 __global__ void __launch_bounds__(NT) k3_llfb(const K3Args a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ long long s_wv[NT / 32];
@@ -345,43 +345,64 @@ __global__ void __launch_bounds__(NT) k3_llfb(const K3Args a) {
   // ---- sequential placement, parallel _lowest_fit
   long long cap_rest = LLONG_MIN;
   if constexpr (NT * MAXC <= 8192) {
-    // Placed list in registers: thread t owns list slots [t*MAXC, (t+1)*MAXC)
+    // Placed list in registers: thread t owns list slots [t*TOT, (t+1)*TOT)
     // as {lo, hi, start, end}; empty slots never overlap and sort last.  An
     // insertion shifts the suffix with lo > res one slot right: within a
     // thread by register selects, across threads by one shuffle (lane 0
     // reads the previous warp's last slot, double-buffered by item parity).
     // NT = 512: start | end << 16 in one register (the host routes problems
-    // with timesteps >= 65535 elsewhere), so the list fits 128 registers
+    // with timesteps >= 65535 elsewhere), so the list fits 128 registers.
+    // MS > 0 (leaves of 8k-16k items): each thread's last MS slots live in
+    // shared memory, lane-interleaved ([m][tid]: conflict-free whatever slot
+    // a warp touches), the working set in global scratch (the host routes
+    // every problem of such a launch there).
     constexpr bool PK = NT > 256;
+    constexpr int TOT = MAXC + MS;
+    static_assert(MS == 0 || PK, "shared-memory slots use the packed start | end form");
     __shared__ long long s_plo[2][NT / 32], s_phi[2][NT / 32];
     __shared__ long long s_xw[NT / 32], s_mv[NT / 32];
     __shared__ int s_mi[NT / 32];
     __shared__ int s_pst[2][NT / 32], s_pen[2][NT / 32];
+    long long* sl_lo = reinterpret_cast<long long*>(smem);            // [MS][NT]
+    long long* sl_hi = sl_lo + size_t(MS) * NT;                       // [MS][NT]
+    int* sl_se = reinterpret_cast<int*>(sl_hi + size_t(MS) * NT);     // [MS][NT]
     const int lane = tid & 31, w = tid >> 5;
     long long rlo[MAXC], rhi[MAXC];
     int rst[MAXC], ren[PK ? 1 : MAXC];
-    auto t_st = [&](int m) { return PK ? (rst[m] & 0xffff) : rst[m]; };
-    auto t_en = [&](int m) { return PK ? ((unsigned)rst[m] >> 16) : ren[PK ? 0 : m]; };
+    // slot m of this thread: registers below MAXC, shared memory above (m is
+    // a compile-time constant in every unrolled loop)
+    auto g_lo = [&](int m) -> long long { return m < MAXC ? rlo[m < MAXC ? m : 0] : sl_lo[(m - MAXC) * NT + tid]; };
+    auto g_hi = [&](int m) -> long long { return m < MAXC ? rhi[m < MAXC ? m : 0] : sl_hi[(m - MAXC) * NT + tid]; };
+    auto g_st = [&](int m) -> int { return m < MAXC ? rst[m < MAXC ? m : 0] : sl_se[(m - MAXC) * NT + tid]; };
+    auto g_en = [&](int m) -> int { return PK ? 0 : ren[PK ? 0 : m]; };
+    auto p_slot = [&](int m, long long lo, long long hi, int se, int en) {
+      if (m < MAXC) {
+        rlo[m < MAXC ? m : 0] = lo;
+        rhi[m < MAXC ? m : 0] = hi;
+        rst[m < MAXC ? m : 0] = se;
+        if (!PK) ren[PK ? 0 : m] = en;
+      } else {
+        sl_lo[(m - MAXC) * NT + tid] = lo;
+        sl_hi[(m - MAXC) * NT + tid] = hi;
+        sl_se[(m - MAXC) * NT + tid] = se;
+      }
+    };
+    auto t_st = [&](int m) { return PK ? (g_st(m) & 0xffff) : g_st(m); };
+    auto t_en = [&](int m) { return PK ? ((unsigned)g_st(m) >> 16) : (unsigned)g_en(m); };
 #pragma unroll
-    for (int m = 0; m < MAXC; ++m) {
-      const int j = tid * MAXC + m;
+    for (int m = 0; m < TOT; ++m) {
+      const int j = tid * TOT + m;
       int a0 = INT_MAX, a1 = INT_MIN;
+      long long lo = LLONG_MAX, hi = LLONG_MIN;
       if (j < P) {
         const int q = ord[j];
-        rlo[m] = off[q];
-        rhi[m] = off[q] + sz[q];
+        lo = off[q];
+        hi = off[q] + sz[q];
         a0 = st[q];
         a1 = en[q];
-      } else {
-        rlo[m] = LLONG_MAX;
-        rhi[m] = LLONG_MIN;
       }
-      if (PK) {
-        rst[m] = j < P ? (a0 | (a1 << 16)) : 0xffff;  // empty: start 65535 > every end
-      } else {
-        rst[m] = a0;
-        ren[PK ? 0 : m] = a1;
-      }
+      // PK: empty slots hold start 65535 > every end
+      p_slot(m, lo, hi, PK ? (j < P ? (a0 | (a1 << 16)) : 0xffff) : a0, a1);
     }
     // the next item's record is fetched one placement ahead (the working set
     // of a large leaf lives in global scratch: its loads are the critical path)
@@ -404,18 +425,18 @@ __global__ void __launch_bounds__(NT) k3_llfb(const K3Args a) {
       // insertion (index P_k) holds only empty slots: it skips the slot work
       // (warp-uniform) and only joins the block reductions -- the list fills
       // from the front, so on average half the warps sit this out
-      const bool wlive = w * 32 * MAXC <= P + (k - A);
+      const bool wlive = w * 32 * TOT <= P + (k - A);
       if (wlive && lane == 31) {
-        s_plo[buf][w] = rlo[MAXC - 1];
-        s_phi[buf][w] = rhi[MAXC - 1];
-        s_pst[buf][w] = rst[MAXC - 1];
-        if (!PK) s_pen[buf][w] = ren[PK ? 0 : MAXC - 1];
+        s_plo[buf][w] = g_lo(TOT - 1);
+        s_phi[buf][w] = g_hi(TOT - 1);
+        s_pst[buf][w] = g_st(TOT - 1);
+        if (!PK) s_pen[buf][w] = g_en(TOT - 1);
       }
       long long mx = LLONG_MIN;
       if (wlive) {
 #pragma unroll
-        for (int m = 0; m < MAXC; ++m)
-          if (t_st(m) <= ei && si <= t_en(m)) mx = max(mx, rhi[m]);
+        for (int m = 0; m < TOT; ++m)
+          if (t_st(m) <= ei && si <= t_en(m)) mx = max(mx, g_hi(m));
       }
       long long all_mx;
       long long M = max(fl, blk.excl_max1(mx, &all_mx, s_xw));
@@ -423,13 +444,13 @@ __global__ void __launch_bounds__(NT) k3_llfb(const K3Args a) {
       long long at = 0;
       if (wlive) {
 #pragma unroll
-        for (int m = 0; m < MAXC; ++m) {
+        for (int m = 0; m < TOT; ++m) {
           if (t_st(m) <= ei && si <= t_en(m) && brk == INT_MAX) {
-            if (M + szi <= rlo[m]) {
-              brk = tid * MAXC + m;
+            if (M + szi <= g_lo(m)) {
+              brk = tid * TOT + m;
               at = M;
             } else {
-              M = max(M, rhi[m]);
+              M = max(M, g_hi(m));
             }
           }
         }
@@ -440,10 +461,10 @@ __global__ void __launch_bounds__(NT) k3_llfb(const K3Args a) {
       cap_rest = max(cap_rest, res + szi);
       if (!wlive) continue;
       // the slot before this thread's first one
-      long long plo = __shfl_up_sync(0xffffffffu, rlo[MAXC - 1], 1);
-      long long phi = __shfl_up_sync(0xffffffffu, rhi[MAXC - 1], 1);
-      int pst = __shfl_up_sync(0xffffffffu, rst[MAXC - 1], 1);
-      int pen = PK ? 0 : __shfl_up_sync(0xffffffffu, ren[PK ? 0 : MAXC - 1], 1);
+      long long plo = __shfl_up_sync(0xffffffffu, g_lo(TOT - 1), 1);
+      long long phi = __shfl_up_sync(0xffffffffu, g_hi(TOT - 1), 1);
+      int pst = __shfl_up_sync(0xffffffffu, g_st(TOT - 1), 1);
+      int pen = PK ? 0 : __shfl_up_sync(0xffffffffu, g_en(TOT - 1), 1);
       if (lane == 0) {
         if (w == 0) {
           plo = LLONG_MIN;  // list start: the item goes first if slot 0 moves
@@ -456,17 +477,14 @@ __global__ void __launch_bounds__(NT) k3_llfb(const K3Args a) {
       }
       const int ist = PK ? (si | (ei << 16)) : si;
 #pragma unroll
-      for (int m = 0; m < MAXC; ++m) {
+      for (int m = 0; m < TOT; ++m) {
         // slots with lo <= res stay; the first other slot takes the item, the
         // rest take their predecessor
-        const long long olo = rlo[m], ohi = rhi[m];
-        const int ost = rst[m], oen = PK ? 0 : ren[PK ? 0 : m];
+        const long long olo = g_lo(m), ohi = g_hi(m);
+        const int ost = g_st(m), oen = g_en(m);
         if (olo > res) {
           const bool first = plo <= res;
-          rlo[m] = first ? res : plo;
-          rhi[m] = first ? res + szi : phi;
-          rst[m] = first ? ist : pst;
-          if (!PK) ren[PK ? 0 : m] = first ? ei : pen;
+          p_slot(m, first ? res : plo, first ? res + szi : phi, first ? ist : pst, first ? ei : pen);
         }
         plo = olo;
         phi = ohi;
@@ -610,9 +628,9 @@ static int sm_max_smem(int dev) {
   return v;
 }
 
-template <int NT, int MAXC>
+template <int NT, int MAXC, int MS = 0>
 static int launch_k3_t(const K3Args& a, int grid, size_t smem, cudaStream_t s) {
-  auto kern = k3_llfb<NT, MAXC>;
+  auto kern = k3_llfb<NT, MAXC, MS>;
   RM_CUDA(smem_optin(kern));
   kern<<<grid, NT, smem, s>>>(a);
   RM_LAUNCH_CHECK("k3_llfb launch");
@@ -656,13 +674,22 @@ extern "C" int rm_llfb_batch(int32_t P, const int64_t* item_ptr, const int32_t* 
   // shared memory holds any problem up to the opt-in limit; larger ones work
   // out of a global scratch region (L1/L2 cached)
   const size_t limit = (size_t)sm_max_smem(dev) - 1024;
+  // NT = 512 / 1024 pack start | end << 16 per placed item
+  bool times16 = true;
+  for (int64_t k = 0; k < NI && times16; ++k)
+    times16 = start[k] >= 0 && end[k] >= 0 && start[k] < 65535 && end[k] < 65535;
+  // leaves of 8k-10k items: a 1024-thread list with 4 register and 6
+  // shared-memory slots per thread; shared memory then holds the list and
+  // every working set goes to global scratch
+  constexpr int kHyNT = 1024, kHyMR = 4, kHyMS = 6;
+  const bool hybrid = maxN >= 8192 && maxN < kHyNT * (kHyMR + kHyMS) && times16;
   std::vector<int64_t> goff(P, -1);
-  size_t gbytes = 0, smem = 0;
+  size_t gbytes = 0, smem = hybrid ? size_t(kHyMS) * kHyNT * 20 : 0;
   for (int p = 0; p < P; ++p) {
     const int n = (int)(item_ptr[p + 1] - item_ptr[p]);
     if (n == 0) continue;
     const size_t b = K3Layout(n).bytes;
-    if (b <= limit) {
+    if (b <= limit && !hybrid) {
       smem = std::max(smem, b);
     } else {
       goff[p] = (int64_t)gbytes;
@@ -701,10 +728,6 @@ extern "C" int rm_llfb_batch(int32_t P, const int64_t* item_ptr, const int32_t* 
   }
   K3Args a{P, d_ptr, d_t, d_s, d_e, d_sz, d_act, mode, d_off, d_cap, d_met, d_comp, d_ccap, d_g,
            d_goff};
-  // NT = 512 packs start | end << 16 per placed item
-  bool times16 = true;
-  for (int64_t k = 0; k < NI && times16; ++k)
-    times16 = start[k] >= 0 && end[k] >= 0 && start[k] < 65535 && end[k] < 65535;
   int rc;
   // the register-resident placed list holds NT * MAXC - 1 placed items; fewer
   // slots per thread shorten the per-item chain between the block barriers
@@ -714,6 +737,8 @@ extern "C" int rm_llfb_batch(int32_t P, const int64_t* item_ptr, const int32_t* 
     rc = launch_k3_t<256, 16>(a, P, smem, s);
   else if (maxN < 8192 && times16)
     rc = launch_k3_t<512, 16>(a, P, smem, s);
+  else if (hybrid)
+    rc = launch_k3_t<kHyNT, kHyMR, kHyMS>(a, P, smem, s);
   else
     rc = launch_k3_t<1024, 16>(a, P, smem, s);
   if (rc) return rc;

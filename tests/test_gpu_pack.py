@@ -109,15 +109,23 @@ def test_large_problem_global_scratch():
     assert (b.offsets, b.capacity) == O.constrained_llfb_layout(rows)
 
 
-@pytest.mark.parametrize("n,horizon", [(5000, 1500), (8191, 3000), (8192, 3000), (6000, 70000)])
+@pytest.mark.parametrize("n,horizon", [(5000, 1500), (8191, 3000), (8192, 3000), (9035, 4000), (10239, 3000),
+                                       (10240, 3000), (6000, 70000)])
 def test_register_list_geometries(n, horizon):
     """Placed lists of 4k-8k items (512 threads, start | end packed in 16 bits),
-    the first size past it (1024 threads, shared-memory list) and timesteps
-    beyond 16 bits (routed to the 1024-thread path)."""
+    8k-10k items (1024 threads, 4 register + 6 shared-memory slots each, every
+    working set in global scratch; a small leaf rides in the same launch),
+    the first size past it (the shared-memory list) and timesteps beyond 16
+    bits (routed to the 1024-thread path)."""
     rng = random.Random(n + horizon)
     rows = _rand_rows(rng, n, horizon, 0.2)
-    b = pack_batch([_items(rows)], CONSTRAINED)[0]
+    small = _rand_rows(rng, 40, 30, 0.2)
+    b, c = pack_batch([_items(rows), _items(small)], CONSTRAINED)
     assert (b.offsets, b.capacity) == O.constrained_llfb_layout(rows)
+    assert (c.offsets, c.capacity) == O.constrained_llfb_layout(small)
+    if n in (9035, 10239):
+        p = pack_batch([_items(rows)], PLAIN)[0]
+        assert (p.offsets, p.capacity) == O.llfb_layout(rows)
 
 
 def test_components_vs_oracle():
