@@ -162,6 +162,16 @@ int rm_eval_select_key(RmGraph* g, const void* orders, int64_t B, int64_t id_bas
                        uint32_t flags, int64_t* peak, int32_t* argmax, uint8_t* valid,
                        int64_t* out_key, void* stream);
 
+/* Batched live_bytes_by_timestep (graph.py:452-458) over sequential
+ * schedules: live[b * n + k] = bytes alive at step k of row b (int64[B, n]),
+ * valid[b] = the row is a permutation respecting every direct pred
+ * (graph.py:375-398); rows with valid == 0 leave their live row unwritten.
+ * max_k live[b, k] and its first index equal rm_eval_orders' peak / argmax.
+ * Flags: RM_DEVICE_PTRS, RM_ORDERS_U16.  Graphs whose 12 n bytes exceed one
+ * CTA's shared memory fail with RM_ERR_CAPACITY. */
+int rm_eval_live(RmGraph* g, const void* orders, int64_t B, uint32_t flags, int64_t* live, uint8_t* valid,
+                 void* stream);
+
 /* Multi-GPU selection exchange (one process per GPU): each rank's
  * rm_eval_select_key key (device int64[1], (peak << id_bits) | global id,
  * INT64_MAX when the rank has no valid candidate) becomes the global first

@@ -21,7 +21,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB_PATH = PKG / "libroam.so"
-SOURCES = ("roam_graph.cpp", "layout_search.cpp", "order_search.cpp", "wu_place.cpp", "nccl_select.cpp", "k_eval.cu", "k_eval_v4.cu", "k_eval_v5.cu", "k_gen.cu", "k_layout.cu", "k_repair.cu", "k_pack.cu", "k_greedy.cu", "k_exact.cu")
+SOURCES = ("roam_graph.cpp", "layout_search.cpp", "order_search.cpp", "wu_place.cpp", "nccl_select.cpp", "k_eval.cu", "k_eval_v4.cu", "k_eval_v5.cu", "k_gen.cu", "k_layout.cu", "k_repair.cu", "k_live.cu", "k_pack.cu", "k_greedy.cu", "k_exact.cu")
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 
 
@@ -150,6 +150,7 @@ SIGNATURES = {
     "rm_graph_asap_alap": (C.c_int, [vp, vp, vp]),
     "rm_graph_ancestors": (C.c_int, [vp, vp]),
     "rm_popcount_rows": (C.c_int, [vp, C.c_int64, C.c_int64, vp, vp]),
+    "rm_eval_live": (C.c_int, [vp, vp, C.c_int64, C.c_uint32, vp, vp, vp]),
     "rm_eval_select_key": (C.c_int, [vp, vp, C.c_int64, C.c_int64, C.c_int32, C.c_uint32, vp, vp, vp, vp, vp]),
     "rm_last_kernel_ms": (C.c_double, []),
 }

@@ -269,6 +269,37 @@ def evaluate_orders(g, orders, stream=None):
     return peak, arg, val.astype(bool)
 
 
+def evaluate_live(g, orders, stream=None):
+    """Batched ``live_bytes_by_timestep(g, sequential_schedule(g, o))``
+    (graph.py:452-458) over rows of orders (rm_eval_live): ``(live int64[B,
+    n], valid bool[B])`` of the input's kind (numpy for host rows, CUDA
+    tensors for CUDA rows).  Rows with valid=False have unspecified live
+    values (the reference raises for them)."""
+    dg = device_graph(g)
+    n = dg.n_ops
+    kind, flags = _row_kind(orders)
+    if kind == "dev":
+        import torch
+        if orders.dim() != 2 or orders.shape[1] != n:
+            raise ValueError(f"orders must be [B, {n}]")
+        with _on(stream):
+            orders = orders.contiguous()
+            B = orders.shape[0]
+            live = torch.empty((B, n), dtype=torch.int64, device=orders.device)
+            val = torch.empty(B, dtype=torch.uint8, device=orders.device)
+            check(lib().rm_eval_live(dg.handle, ptr(orders), B, flags, ptr(live), ptr(val),
+                                     _stream_handle(stream)), "rm_eval_live")
+        return live, val.view(torch.bool)
+    _lib.require_device()
+    o, flags = _host_rows(orders, n)
+    B = o.shape[0]
+    live = np.empty((B, n), np.int64)
+    val = np.empty(B, np.uint8)
+    check(lib().rm_eval_live(dg.handle, ptr(o), B, flags, ptr(live), ptr(val), _stream_handle(stream)),
+          "rm_eval_live")
+    return live, val.astype(bool)
+
+
 def evaluate_and_select(g, orders, id_base: int = 0, stream=None):
     """evaluate_orders + first-strict-minimum selection in one libroam call
     (rm_eval_select).  Returns (peak, argmax, valid, best) where best is a

@@ -452,3 +452,34 @@ def test_nccl_select_key_single_rank():
         assert int(none.item()) == 2**63 - 1
     finally:
         sel.close()
+
+
+@pytest.mark.parametrize("name", ["layered", "gpt2-small", "bert-large"])
+def test_batched_live_matches_reference_semantics(name):
+    """rm_eval_live: per-candidate live_bytes_by_timestep (graph.py:452-458)
+    equal to the Python restatement on sampled rows, its max / first argmax
+    equal to K1's peak / argmax on every valid row, validity equal to K1's
+    (corrupted rows included), for int32 and uint16 rows, host and device."""
+    import torch
+
+    from paper_2310_19295_b200.evaluator import evaluate_live
+    g = load_graph(gg.config_doc(name))
+    n = len(g.ops)
+    B = 600
+    host = generate_orders(g, 21, 0, B).cpu().numpy()
+    rng = np.random.default_rng(1)
+    for r in range(0, B, 37):
+        i, j = rng.integers(0, n, 2)
+        host[r, [i, j]] = host[r, [j, i]]
+    host[3, 4] = host[3, 5]
+    pk, ag, vl = evaluate_orders(g, host)
+    live, val = evaluate_live(g, host)
+    assert np.array_equal(val, vl)
+    v = np.flatnonzero(vl)
+    assert np.array_equal(live[v].max(axis=1), pk[v]) and np.array_equal(live[v].argmax(axis=1), ag[v])
+    for k in v[:: max(1, len(v) // 6)]:
+        assert live[k].tolist() == O.live_bytes_by_timestep(g, O.sequential_timesteps(n, host[k].tolist()))
+    dl, dv = evaluate_live(g, torch.from_numpy(host).cuda())
+    assert np.array_equal(dl.cpu().numpy()[v], live[v]) and np.array_equal(dv.cpu().numpy(), val)
+    hl, hv = evaluate_live(g, host.astype(np.uint16))
+    assert np.array_equal(hl[v], live[v]) and np.array_equal(hv, val)

@@ -48,6 +48,7 @@ def main(which: str = "all") -> None:
         ev.set_k1_variant(1)
         ev.evaluate_orders(g, bad)
         ev.set_k1_variant(0)
+        ev.evaluate_live(g, bad)      # batched live bytes, corrupted rows included
         torch.cuda.synchronize()
     if which in ("all", "gen"):
         # the thread-per-candidate generator, and the warp form it hands the
