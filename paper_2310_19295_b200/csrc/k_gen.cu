@@ -124,8 +124,8 @@ __global__ void __launch_bounds__(256) k_gen_orders(int n, uint64_t seed, int64_
 // second arrival; an arrival counter is cleared at its last), so nothing is
 // reset between candidates.
 //
-// Heap entries per candidate: GEN_CAP (a template parameter, 32-64), walked
-// with GEN_DEPTH unrolled predicated levels.  A ready set above GEN_CAP (or a
+// Heap entries per candidate: GEN_CAP (a template parameter, 32-64) in a
+// 4-ary heap, walked with GEN_DEPTH = 3 unrolled predicated levels.  A ready set above GEN_CAP (or a
 // cycle) hands the candidate to the warp form, which rewrites its row.
 
 __device__ __forceinline__ uint64_t unmix64(uint64_t y) {
@@ -140,7 +140,7 @@ __device__ __forceinline__ uint64_t unmix64(uint64_t y) {
 // The successor table (eptr as PtrT, edges as u32) is staged in shared memory
 // once per CTA: the per-step lookups are dependent loads, which from L2 would
 // cost ~700 cycles each (the per-thread state leaves L1 almost no room).
-template <typename PtrT, int GEN_CAP, int GEN_DEPTH = (GEN_CAP <= 32 ? 5 : 6)>
+template <typename PtrT, int GEN_CAP, int GEN_DEPTH = 3>
 __global__ void __launch_bounds__(1024) k_gen_thread(int n, uint64_t seed, int64_t first_id, int64_t B,
                                                      const uint32_t* __restrict__ eptr_g,
                                                      const uint32_t* __restrict__ edges_g, int n_edges,
@@ -166,8 +166,9 @@ __global__ void __launch_bounds__(1024) k_gen_thread(int n, uint64_t seed, int64
     int32_t* row = out + c * int64_t(n);
     int R = 0;
     bool over = false;
-    // insert key x at slot R and sift it up (predicated moves over the
-    // levels above it)
+    // 4-ary min-heap (children of i: 4i+1 .. 4i+4): GEN_DEPTH = 3 levels hold
+    // 85 entries, half the levels of a binary heap on every walk
+    // insert key x at slot R and sift it up (predicated moves)
     auto push = [&](uint64_t x) {
       over |= R == GEN_CAP;
       int i = min(R, GEN_CAP - 1);
@@ -175,7 +176,7 @@ __global__ void __launch_bounds__(1024) k_gen_thread(int n, uint64_t seed, int64
       bool go = true;
 #pragma unroll
       for (int L = 0; L < GEN_DEPTH; ++L) {
-        const int p = (i - 1) >> 1;
+        const int p = (i - 1) >> 2;
         const uint64_t e = heap[max(p, 0) * 32];
         go = go && i > 0 && x < e;
         if (go) {
@@ -196,15 +197,24 @@ __global__ void __launch_bounds__(1024) k_gen_thread(int n, uint64_t seed, int64
         bool go = true;
 #pragma unroll
         for (int L = 0; L < GEN_DEPTH; ++L) {
-          const int ch = 2 * i + 1;
-          const uint64_t a = heap[min(ch, GEN_CAP - 1) * 32];   // ch may pass R on the last level
-          const uint64_t b = heap[min(ch + 1, GEN_CAP - 1) * 32];
-          const bool right = ch + 1 < R && b < a;
-          const uint64_t m = right ? b : a;
+          const int ch = 4 * i + 1;  // children may pass R (or the heap) on the last level
+          const uint64_t a0 = heap[min(ch, GEN_CAP - 1) * 32];
+          const uint64_t a1 = heap[min(ch + 1, GEN_CAP - 1) * 32];
+          const uint64_t a2 = heap[min(ch + 2, GEN_CAP - 1) * 32];
+          const uint64_t a3 = heap[min(ch + 3, GEN_CAP - 1) * 32];
+          // min of the children below R, as a two-level tree
+          const bool t1 = ch + 1 < R && a1 < a0;
+          const uint64_t m01 = t1 ? a1 : a0;
+          const int i01 = t1 ? 1 : 0;
+          const bool v2 = ch + 2 < R, t3 = ch + 3 < R && a3 < a2;
+          const uint64_t m23 = t3 ? a3 : a2;
+          const int i23 = t3 ? 3 : 2;
+          const bool tr = v2 && m23 < m01;
+          const uint64_t m = tr ? m23 : m01;
           go = go && ch < R && m < x;
           if (go) {
             heap[i * 32] = m;
-            i = ch + (right ? 1 : 0);
+            i = ch + (tr ? i23 : i01);
           }
         }
         heap[i * 32] = x;
@@ -291,7 +301,7 @@ void build_gen_meta(RmGraph& g) {
 }
 
 static thread_local int t_gen_form = 0;  // 0 auto, 1 warp form only
-static thread_local int t_gen_cap = 40;  // thread form heap entries: 32, 40, 48 or 64
+static thread_local int t_gen_cap = 0;   // thread form heap entries: 32, 40, 48, 64; 0 = by graph size
 
 static int launch_gen_warp(RmGraph* g, uint64_t seed, int64_t first_id, int64_t B, int32_t* out,
                            const int32_t* redo, const unsigned* n_redo, cudaStream_t s) {
@@ -332,10 +342,12 @@ int launch_gen(RmGraph* g, uint64_t seed, int64_t first_id, int64_t B, int32_t* 
   const bool narrow = n_edges < 65536;
   auto a16 = [](size_t x) { return (x + 15) & ~size_t(15); };
   const size_t table = a16(4 * size_t(n_edges)) + a16((narrow ? 2 : 4) * (size_t(g->n) + 1));
-  // heap capacity (rm_set_gen_form 32/40/48/64 for A/B; default 40: measured
-  // best on GPT-2 small and GPT2-XL, whose ready sets reach ~37 -- the rare
-  // candidate that outgrows it is rewritten by the warp form)
-  const int cap = t_gen_cap;
+  // heap capacity (rm_set_gen_form 32/40/48/64 for A/B).  Default 40 below
+  // 8k ops (GPT-2 small / BERT-large: ready sets reach ~37), 64 above (the
+  // 11k-op GPT2-XL's reach further: 40 entries hand ~1 % of its rows to the
+  // slow warp form, 3.25 vs 3.50 M/s measured); a candidate that outgrows the
+  // heap is rewritten by the warp form
+  const int cap = t_gen_cap > 0 ? t_gen_cap : (g->n >= 8192 ? 64 : 40);
   const size_t per_warp = (size_t(m.words) * 4 + size_t(cap) * 8) * 32;
   const int warps = m.ok && size_t(max_smem) > table ? (int)std::min<size_t>(32, (size_t(max_smem) - table) / per_warp) : 0;
   if (t_gen_form == 1 || warps < 4 || B > INT32_MAX)
@@ -380,7 +392,7 @@ extern "C" int rm_set_gen_form(int form) {
   }
   if (form < 0 || form > 1) return roam::fail(RM_ERR_INVALID_ARG, "gen form must be 0 (auto) or 1 (warp)");
   roam::t_gen_form = form;
-  if (form == 0) roam::t_gen_cap = 40;
+  if (form == 0) roam::t_gen_cap = 0;
   return RM_OK;
 }
 
