@@ -330,8 +330,9 @@ int rm_llfb_batch(int32_t P, const int64_t* item_ptr, const int32_t* tensor,
  * over all components; node_cap < 0 = none; deadline = CLOCK_MONOTONIC seconds
  * checked every 4096 nodes, <= 0 = none).  Outputs: offset[item], capacity,
  * nodes (the reference's LayoutStats.nodes) and optimal (0 when a budget
- * stopped a search).  Host code (the search is sequential); components of
- * more than 64 items fail with RM_ERR_CAPACITY. */
+ * stopped a search).  Host code (the search is sequential); item masks of
+ * as many 64-bit words as a component needs (components of more than 16,384
+ * items fail with RM_ERR_CAPACITY). */
 int rm_layout_search(int32_t n, const int32_t* tensor, const int32_t* start, const int32_t* end,
                      const int64_t* size, const uint8_t* is_act, int32_t bottom,
                      const int64_t* incumbent, int64_t node_cap, double deadline, int64_t* offset,
@@ -345,7 +346,8 @@ int rm_layout_search(int32_t n, const int32_t* tensor, const int32_t* start, con
  * status: 0 searched (order[n_ops] global ids, peak, nodes), 1 ConfigError
  * (bad_tensor: live-in tensor without a window consumer), 2 precedence cycle,
  * 4 budget -- the reference then returns its greedy incumbent.  Host code;
- * windows of more than 64 ops fail with RM_ERR_CAPACITY. */
+ * scheduled-op masks of as many 64-bit words as the window needs (windows
+ * of more than 16,384 ops fail with RM_ERR_CAPACITY). */
 int rm_exact_order_search(RmGraph* g, int32_t n_ops, const int32_t* ops, int64_t n_lin,
                           const int32_t* lin, int64_t n_lout, const int32_t* lout, int64_t node_cap,
                           double deadline, int32_t* order, int64_t* peak, int64_t* nodes,
