@@ -450,6 +450,7 @@ static int launch_k1v4_nt(K1V4Args& a, int NT, int C, bool cls, int grid, size_t
   RM_K1V4_CLS(1024, 16)
   RM_K1V4_CLS(128, 32)
   RM_K1V4_CLS(256, 32)
+  RM_K1V4_CLS(512, 32)
 #undef RM_K1V4_CLS
   if (cls) return 1;
 #define RM_K1V4_CASE(nt, cc) \
@@ -475,6 +476,7 @@ static int launch_k1v4_nt(K1V4Args& a, int NT, int C, bool cls, int grid, size_t
   RM_K1V4_CASE(64, 32)
   RM_K1V4_CASE(128, 32)
   RM_K1V4_CASE(256, 32)
+  RM_K1V4_CASE(512, 32)
   RM_K1V4_CASE(32, 64)
   RM_K1V4_CASE(64, 64)
   RM_K1V4_CASE(128, 64)

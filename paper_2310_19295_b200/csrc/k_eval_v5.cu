@@ -44,13 +44,15 @@ struct K1V5Args {
   const uint32_t* em;  // SIMD edge-mask word per 8-id chunk (shared with v4)
   const uint32_t* edges;
   int n_edges;  // multiple of 4 * NT
+  // WIDE (more than 8,192 slots): every id / target field below doubles
+  // to 16 bits + its shift: g4 four u32, gcons u32, dtgt {ta, tb} u32 pairs
   const uint32_t* dpair;  // two-consumer tensors: pos byte offsets 2a | 2b << 16 ...
-  const uint32_t* dtgt;   // ... and class-bit targets ta | tb << 16, t = word | shift << 11
+  const void* dtgt;       // ... and class-bit targets ta | tb << 16, t = word | shift << 11
   int n_pair;             // multiple of NT (padding: target 0xffffffff)
-  const uint2* g4;       // 3-4 consumer tensors: four u16 (id | bit index << 13),
+  const void* g4;         // 3-4 consumer tensors: four u16 (id | bit index << 13),
   int n_g4;               // a short list repeating its first; multiple of NT, pads 0xe000
   const uint32_t* gptr;   // >= 5 consumer tensors: CSR of consumer id | bit index << 13
-  const uint16_t* gcons;
+  const void* gcons;
   int n_gen, n_gcons;
   int64_t* peak;
   int32_t* argmax;
@@ -91,8 +93,36 @@ __device__ __forceinline__ unsigned v5_bar_or(int id, unsigned p) {
   else return (unsigned)gbar_or(id, NT, (int)p);
 }
 
-template <typename RowT, int NT, int C, bool BULK>
+// the id / target encodings of one geometry: 13-bit ids (up to 8,192 slots)
+// or 16-bit ids (WIDE) with the fields widened
+template <bool WIDE>
+struct V5Enc {
+  using G4 = uint2;        // four u16 consumer entries
+  using GC = uint16_t;
+  using TG = uint32_t;     // ta | tb << 16
+  static constexpr unsigned IDB = 13, G4PAD = 0xe000u;
+  __device__ static unsigned pick(TG t2, bool b) { return __byte_perm(t2, 0u, b ? 0x4432u : 0x4410u); }
+  __device__ static bool pad(TG t2) { return t2 == 0xffffffffu; }
+  static constexpr unsigned TWB = 11;  // target: word | shift << TWB
+};
+template <>
+struct V5Enc<true> {
+  using G4 = uint4;        // four u32 consumer entries
+  using GC = uint32_t;
+  using TG = uint2;        // {ta, tb}
+  static constexpr unsigned IDB = 16, G4PAD = 0x70000u;
+  __device__ static unsigned pick(TG t2, bool b) { return b ? t2.y : t2.x; }
+  __device__ static bool pad(TG t2) { return t2.x == 0xffffffffu; }
+  static constexpr unsigned TWB = 16;
+};
+
+template <typename RowT, int NT, int C, bool BULK, bool WIDE = false>
 __global__ void __launch_bounds__((v5_cta_cap(C, BULK) / NT) * NT, 1) k1v5_eval_orders(const K1V5Args a) {
+  using E = V5Enc<WIDE>;
+  using G4T = typename E::G4;
+  using GCT = typename E::GC;
+  using TGT = typename E::TG;
+  constexpr unsigned IDM = (1u << E::IDB) - 1u;
   extern __shared__ __align__(16) unsigned char smem[];
   asm volatile("griddepcontrol.launch_dependents;");
   constexpr int SL = NT * C;
@@ -104,7 +134,8 @@ __global__ void __launch_bounds__((v5_cta_cap(C, BULK) / NT) * NT, 1) k1v5_eval_
   // positions j*NT + tid with j < JSAFE are always < n: the launcher runs the
   // C >= 32 instances only when n > SL / 2
   constexpr int JSAFE = (C >= 32 && NT >= 64) ? C / 2 : 0;
-  constexpr int PR = C >= 32 ? 6 : C / 4;  // two-consumer tensors per thread kept in registers
+  // two-consumer tensors per thread kept in registers (WIDE: 8-byte targets)
+  constexpr int PR = C >= 32 ? (WIDE ? 4 : 6) : C / 4;
   const int n = a.n;
   const RowT* orders = static_cast<const RowT*>(a.orders);
   const int lane = threadIdx.x & 31;
@@ -122,11 +153,11 @@ __global__ void __launch_bounds__((v5_cta_cap(C, BULK) / NT) * NT, 1) k1v5_eval_
     if (a.n_edges > (C / 4) * NT) cp16(a.edges, a.off_edges, 4 * size_t(a.n_edges));
     if (a.n_pair > PR * NT) {
       cp16(a.dpair, a.off_dpair, 4 * size_t(a.n_pair));
-      cp16(a.dtgt, a.off_dtgt, 4 * size_t(a.n_pair));
+      cp16(a.dtgt, a.off_dtgt, sizeof(TGT) * size_t(a.n_pair));
     }
-    cp16(a.g4, a.off_g4, 8 * size_t(a.n_g4));
+    cp16(a.g4, a.off_g4, sizeof(G4T) * size_t(a.n_g4));
     cp16(a.gptr, a.off_gptr, align16(4 * size_t(a.n_gen + 1)));
-    cp16(a.gcons, a.off_gcons, align16(2 * size_t(a.n_gcons)));
+    cp16(a.gcons, a.off_gcons, align16(sizeof(GCT) * size_t(a.n_gcons)));
   }
   __syncthreads();
   const uint8_t* base8 = smem + a.off_base;
@@ -136,10 +167,10 @@ __global__ void __launch_bounds__((v5_cta_cap(C, BULK) / NT) * NT, 1) k1v5_eval_
   const unsigned lane8 = (unsigned)lane * 8u;
   const uint32_t* edges = reinterpret_cast<const uint32_t*>(smem + a.off_edges);
   const uint32_t* dpair = reinterpret_cast<const uint32_t*>(smem + a.off_dpair);
-  const uint32_t* dtgt = reinterpret_cast<const uint32_t*>(smem + a.off_dtgt);
-  const uint2* g4 = reinterpret_cast<const uint2*>(smem + a.off_g4);
+  const TGT* dtgt = reinterpret_cast<const TGT*>(smem + a.off_dtgt);
+  const G4T* g4 = reinterpret_cast<const G4T*>(smem + a.off_g4);
   const uint32_t* gptr = reinterpret_cast<const uint32_t*>(smem + a.off_gptr);
-  const uint16_t* gcons = reinterpret_cast<const uint16_t*>(smem + a.off_gcons);
+  const GCT* gcons = reinterpret_cast<const GCT*>(smem + a.off_gcons);
 
   const int gid = threadIdx.x / NT;
   const int tid = threadIdx.x - gid * NT;
@@ -164,11 +195,15 @@ __global__ void __launch_bounds__((v5_cta_cap(C, BULK) / NT) * NT, 1) k1v5_eval_
   for (int i = 0; i < ER; ++i) er[i] = (ereg && i < ek) ? __ldg(a.edges + tid + i * NT) : 0u;
   const int pk = n_pair / NT;
   const bool preg = pk <= PR;
-  uint32_t pw[PR], pt[PR];
+  uint32_t pw[PR];
+  TGT pt[PR];
+  const TGT* gdtgt = static_cast<const TGT*>(a.dtgt);
 #pragma unroll
   for (int i = 0; i < PR; ++i) {
     pw[i] = (preg && i < pk) ? __ldg(a.dpair + tid + i * NT) : 0u;
-    pt[i] = (preg && i < pk) ? __ldg(a.dtgt + tid + i * NT) : K1V5_PAD;
+    if (preg && i < pk) pt[i] = gdtgt[tid + i * NT];
+    else if constexpr (WIDE) pt[i] = make_uint2(K1V5_PAD, K1V5_PAD);
+    else pt[i] = K1V5_PAD;
   }
   uint32_t em[QR];
 #pragma unroll
@@ -326,10 +361,10 @@ __global__ void __launch_bounds__((v5_cta_cap(C, BULK) / NT) * NT, 1) k1v5_eval_
     // sentinel; the bits stay in range either way)
     // pair (a, b): the later consumer's class byte gains the tensor's bit;
     // the target half t = class word | bit shift << 11 is picked by one PRMT
-    auto pair_free = [&](uint32_t t2, unsigned pa, unsigned pbv) {
-      const unsigned t = __byte_perm(t2, 0u, pbv > pa ? 0x4432u : 0x4410u);
-      if (t2 != K1V5_PAD)
-        atomicAdd(reinterpret_cast<unsigned*>(clsp) + (t & 0x7ffu), 1u << (t >> 11));
+    auto pair_free = [&](TGT t2, unsigned pa, unsigned pbv) {
+      const unsigned t = E::pick(t2, pbv > pa);
+      if (!E::pad(t2))
+        atomicAdd(reinterpret_cast<unsigned*>(clsp) + (t & ((1u << E::TWB) - 1u)), 1u << (t >> E::TWB));
     };
     int m_first = tid;
     if (preg) {
@@ -348,27 +383,31 @@ __global__ void __launch_bounds__((v5_cta_cap(C, BULK) / NT) * NT, 1) k1v5_eval_
       pair_free(dtgt[m], v5_lds_u16(posb, w & 0xffffu), v5_lds_u16(posb, w >> 16));
     }
     for (int m = tid; m < n_g4; m += NT) {
-      const uint2 e = g4[m];
-      const unsigned e0 = e.x & 0xffffu, e1 = e.x >> 16, e2 = e.y & 0xffffu, e3 = e.y >> 16;
-      const unsigned p0 = pos[e0 & 0x1fffu], p1 = pos[e1 & 0x1fffu], p2 = pos[e2 & 0x1fffu],
-                     p3 = pos[e3 & 0x1fffu];
+      const G4T e = g4[m];
+      unsigned e0, e1, e2, e3;
+      if constexpr (WIDE) {
+        e0 = e.x, e1 = e.y, e2 = e.z, e3 = e.w;
+      } else {
+        e0 = e.x & 0xffffu, e1 = e.x >> 16, e2 = e.y & 0xffffu, e3 = e.y >> 16;
+      }
+      const unsigned p0 = pos[e0 & IDM], p1 = pos[e1 & IDM], p2 = pos[e2 & IDM], p3 = pos[e3 & IDM];
       // first maximum, in list order (ties only in broken rows)
       const unsigned b01 = p1 > p0 ? e1 : e0, q01 = max(p0, p1);
       const unsigned b23 = p3 > p2 ? e3 : e2, q23 = max(p2, p3);
       const unsigned bw = q23 > q01 ? b23 : b01;
-      if (e0 != 0xe000u) add_bit(bw & 0x1fffu, 1u << (bw >> 13));
+      if (e0 != E::G4PAD) add_bit(bw & IDM, 1u << (bw >> E::IDB));
     }
     for (int m = tid; m < n_gen; m += NT) {
       const int q0 = gptr[m], q1 = gptr[m + 1];
       unsigned best = 0, bw = 0;
       for (int q = q0; q < q1; ++q) {
-        const unsigned e = gcons[q], p = pos[e & 0x1fffu];
+        const unsigned e = gcons[q], p = pos[e & IDM];
         if (q == q0 || p > best) {
           best = p;
           bw = e;
         }
       }
-      add_bit(bw & 0x1fffu, 1u << (bw >> 13));
+      add_bit(bw & IDM, 1u << (bw >> E::IDB));
     }
     unsigned bad = ((sent & 0x80008000u) != 0) | ((ok & 0x80008000u) != 0x80008000u) | (eacc < 0);
     v5_bar<NT>(bar_id);
@@ -511,9 +550,9 @@ __global__ void __launch_bounds__((v5_cta_cap(C, BULK) / NT) * NT, 1) k1v5_eval_
   }
 }
 
-template <typename RowT, int NT, int C, bool BULK>
+template <typename RowT, int NT, int C, bool BULK, bool WIDE = false>
 static int launch_k1v5_t(K1V5Args& a, int grid, size_t smem, cudaStream_t s) {
-  auto kern = k1v5_eval_orders<RowT, NT, C, BULK>;
+  auto kern = k1v5_eval_orders<RowT, NT, C, BULK, WIDE>;
   RM_CUDA(smem_optin(kern));
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (g_timing) {
@@ -548,7 +587,12 @@ static int launch_k1v5_t(K1V5Args& a, int grid, size_t smem, cudaStream_t s) {
 // the instance table must list every (NT, C) k1v4_geometry (roam_graph.cpp)
 // picks for a class-form graph
 template <typename RowT>
-static int launch_k1v5_nt(K1V5Args& a, int NT, int C, bool bulk, int grid, size_t smem, cudaStream_t s) {
+static int launch_k1v5_nt(K1V5Args& a, int NT, int C, bool bulk, bool wide, int grid, size_t smem,
+                          cudaStream_t s) {
+  if (wide) {  // 8,192 < slots <= 16,384: one 512-thread group per CTA
+    if (NT == 512 && C == 32 && !bulk) return launch_k1v5_t<RowT, 512, 32, false, true>(a, grid, smem, s);
+    return 1;
+  }
 #define RM_K1V5_CASE(nt, cc)                                                      \
   if (NT == nt && C == cc)                                                        \
     return bulk ? launch_k1v5_t<RowT, nt, cc, true>(a, grid, smem, s)             \
@@ -584,12 +628,12 @@ int launch_k1v5(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, in
   a.edges = m4.edges.as<uint32_t>();
   a.n_edges = (int)m4.n_edges;
   a.dpair = m.dpair.as<uint32_t>();
-  a.dtgt = m.dtgt.as<uint32_t>();
+  a.dtgt = m.dtgt.p;
   a.n_pair = (int)m.n_pair;
-  a.g4 = m.g4.as<uint2>();
+  a.g4 = m.g4.p;
   a.n_g4 = (int)m.n_g4;
   a.gptr = m.gptr.as<uint32_t>();
-  a.gcons = m.gcons.as<uint16_t>();
+  a.gcons = m.gcons.p;
   a.n_gen = (int)m.n_gen;
   a.n_gcons = (int)m.n_gcons;
   a.peak = peak;
@@ -602,11 +646,13 @@ int launch_k1v5(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, in
   a.off_base = 256 * size_t(a.ncls);
   a.off_edges = align16(a.off_base + size_t(SL + 16));
   a.off_dpair = align16(a.off_edges + 4 * size_t(a.n_edges));
+  const bool wide = SL > 8192;
+  const size_t fw = wide ? 2 : 1;  // WIDE doubles the target / entry fields
   a.off_dtgt = align16(a.off_dpair + 4 * size_t(a.n_pair));
-  a.off_g4 = align16(a.off_dtgt + 4 * size_t(a.n_pair));
-  a.off_gptr = align16(a.off_g4 + 8 * size_t(a.n_g4));
+  a.off_g4 = align16(a.off_dtgt + 4 * fw * size_t(a.n_pair));
+  a.off_gptr = align16(a.off_g4 + 8 * fw * size_t(a.n_g4));
   a.off_gcons = align16(a.off_gptr + 4 * size_t(a.n_gen + 1));
-  a.off_groups = align16(a.off_gcons + 2 * size_t(a.n_gcons));
+  a.off_groups = align16(a.off_gcons + 2 * fw * size_t(a.n_gcons));
   a.off_cls = align16(2 * size_t(SL + 8));
   a.off_xc = align16(a.off_cls + size_t(SL + 16));
   a.off_red = align16(a.off_xc + size_t(NT) * xs);
@@ -631,8 +677,8 @@ int launch_k1v5(RmGraph* g, const void* orders_dev, int64_t B, int64_t* peak, in
   a.G = G;
   const size_t smem = a.off_groups + size_t(G) * a.group_bytes;
   const int grid = (int)std::min<int64_t>(sms, (B + G - 1) / G);
-  return u16_rows ? launch_k1v5_nt<uint16_t>(a, NT, C, bulk, grid, smem, s)
-                  : launch_k1v5_nt<int32_t>(a, NT, C, bulk, grid, smem, s);
+  return u16_rows ? launch_k1v5_nt<uint16_t>(a, NT, C, bulk, wide, grid, smem, s)
+                  : launch_k1v5_nt<int32_t>(a, NT, C, bulk, wide, grid, smem, s);
 }
 
 }  // namespace roam

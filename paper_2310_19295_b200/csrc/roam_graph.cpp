@@ -179,9 +179,9 @@ static bool k1v4_geometry(int n, bool classes, int& NT, int& C) {
     const char* e = std::getenv("ROAM_K1_C");
     return e ? std::atoi(e) : 0;
   }();
-  const int want = cenv ? cenv : (n > 1024 && (n <= 2048 || (classes && n <= 8192)) ? 32 : 0);
+  const int want = cenv ? cenv : (n > 1024 && (n <= 2048 || (classes && n <= 16384)) ? 32 : 0);
   if (want == 32 || want == 64) {
-    static const int nts[] = {32, 64, 128, 256};
+    static const int nts[] = {32, 64, 128, 256, 512};
     for (int nt : nts)
       if (nt * want >= n && (want == 32 || nt <= 128)) {
         NT = nt;
@@ -348,7 +348,11 @@ static void build_k1v5_host(RmGraph& g) {
   g.k5v.ok = 0;
   if (!g.k4v.ok || !g.k2v.ok) return;
   const int n = g.n, SL = g.k4v.SL, NT = g.k4v.NT;
-  if (SL > 8192) return;  // a consumer id and a 3-bit bit index share 16 bits
+  if (SL > 16384) return;
+  // up to 8,192 slots a consumer id and its 3-bit bit index share 16 bits;
+  // beyond (WIDE) every entry is 32 bits: id | bit << 16, word | shift << 16
+  const bool wide = SL > 8192;
+  const uint32_t IDB = wide ? 16 : 13, TWB = wide ? 16 : 11;
   const int shift = g.k2v.shift;
   const size_t M = g.h_msize.size();
   std::vector<std::vector<int>> dyn(n);
@@ -385,60 +389,79 @@ static void build_k1v5_host(RmGraph& g) {
   auto idx_of = [&](int v, int t) {
     return (uint32_t)(std::find(dyn[v].begin(), dyn[v].end(), t) - dyn[v].begin());
   };
-  std::vector<uint32_t> pw, pt;
-  auto target = [&](int v, int t) {  // class word of v | bit shift << 11
-    return (uint32_t)(v >> 2) | ((uint32_t)(8 * (v & 3)) + idx_of(v, t)) << 11;
+  std::vector<uint32_t> pw;
+  auto target = [&](int v, int t) {  // class word of v | bit shift << TWB
+    return (uint32_t)(v >> 2) | ((uint32_t)(8 * (v & 3)) + idx_of(v, t)) << TWB;
   };
   g.h5_gptr.assign(1, 0);
   g.h5_gcons.clear();
+  g.h5_gcons32.clear();
   g.h5_g4.clear();
+  std::vector<uint64_t> pt;  // {ta, tb} per pair (packed ta | tb << 16 narrow, a u32 pair WIDE)
   for (size_t m = 0; m < M; ++m) {
     const int q0 = g.h_mptr[m], q1 = g.h_mptr[m + 1];
     if (q1 - q0 == 2) {
       const int a = g.h_mcons[q0], b = g.h_mcons[q0 + 1];
       pw.push_back((uint32_t)(2 * a) | ((uint32_t)(2 * b) << 16));
-      pt.push_back(target(a, (int)m) | (target(b, (int)m) << 16));
+      pt.push_back((uint64_t)target(a, (int)m) | ((uint64_t)target(b, (int)m) << 32));
     } else if (q1 - q0 <= 4) {
       uint32_t e[4];
       for (int q = q0; q < q0 + 4; ++q) {
         const int c = g.h_mcons[q < q1 ? q : q0];
-        e[q - q0] = (uint32_t)c | (idx_of(c, (int)m) << 13);
+        e[q - q0] = (uint32_t)c | (idx_of(c, (int)m) << IDB);
       }
-      g.h5_g4.push_back(e[0] | (e[1] << 16));
-      g.h5_g4.push_back(e[2] | (e[3] << 16));
+      if (wide) {
+        for (int q = 0; q < 4; ++q) g.h5_g4.push_back(e[q]);
+      } else {
+        g.h5_g4.push_back(e[0] | (e[1] << 16));
+        g.h5_g4.push_back(e[2] | (e[3] << 16));
+      }
     } else {
       for (int q = q0; q < q1; ++q) {
         const int c = g.h_mcons[q];
-        g.h5_gcons.push_back((uint16_t)(c | (idx_of(c, (int)m) << 13)));
+        const uint32_t e = (uint32_t)c | (idx_of(c, (int)m) << IDB);
+        if (wide) g.h5_gcons32.push_back(e);
+        else g.h5_gcons.push_back((uint16_t)e);
       }
-      g.h5_gptr.push_back((uint32_t)g.h5_gcons.size());
+      g.h5_gptr.push_back((uint32_t)(wide ? g.h5_gcons32.size() : g.h5_gcons.size()));
     }
   }
-  while ((g.h5_g4.size() / 2) % NT) g.h5_g4.push_back(0xe000e000u);
+  const size_t g4w = wide ? 4 : 2;  // u32 words per 3-4-consumer tensor
+  while ((g.h5_g4.size() / g4w) % NT) {
+    if (wide) g.h5_g4.insert(g.h5_g4.end(), 4, 0x70000u);  // id 0 | bit 7: never a real entry
+    else g.h5_g4.push_back(0xe000e000u);
+  }
   // bank-aware lanes: the lanes of one instruction gather pos[a], pos[b]
   // from distinct banks and add to distinct class words / banks (same-word
   // atomics from one instruction serialise); padding slots read pos[0] and
   // hold target 0xffffffff, which the kernel predicates off
   const size_t P = pw.size();
+  const uint32_t wmask = (1u << TWB) - 1u;
   std::vector<std::array<int, 4>> bank(P);
   for (size_t e = 0; e < P; ++e)
-    bank[e] = {int(((pw[e] & 0xffffu) >> 2) & 31), int(((pw[e] >> 16) >> 2) & 31), int((pt[e] & 0x7ffu) & 31),
-               int(((pt[e] >> 16) & 0x7ffu) & 31)};
+    bank[e] = {int(((pw[e] & 0xffffu) >> 2) & 31), int(((pw[e] >> 16) >> 2) & 31),
+               int(((uint32_t)pt[e] & wmask) & 31), int(((uint32_t)(pt[e] >> 32) & wmask) & 31)};
   const std::vector<size_t> ord = bank_aware_order<4>(bank, NT);
   g.h5_dpair.assign(ord.size(), 0u);
-  g.h5_dtgt.assign(ord.size(), 0xffffffffu);
+  g.h5_dtgt.assign(ord.size() * (wide ? 2 : 1), 0xffffffffu);
   for (size_t k = 0; k < ord.size(); ++k)
     if (ord[k] < P) {
+      const uint64_t t = pt[ord[k]];
       g.h5_dpair[k] = pw[ord[k]];
-      g.h5_dtgt[k] = pt[ord[k]];
+      if (wide) {
+        g.h5_dtgt[2 * k] = (uint32_t)t;
+        g.h5_dtgt[2 * k + 1] = (uint32_t)(t >> 32);
+      } else {
+        g.h5_dtgt[k] = (uint32_t)t | ((uint32_t)(t >> 32) << 16);
+      }
     }
   g.h5_base = base;
   g.h5_tab = tab;
   g.k5v.ncls = (int)(tab.size() / 2);
   g.k5v.n_pair = (int64_t)g.h5_dpair.size();
-  g.k5v.n_g4 = (int64_t)g.h5_g4.size() / 2;
+  g.k5v.n_g4 = (int64_t)(g.h5_g4.size() / g4w);
   g.k5v.n_gen = (int64_t)g.h5_gptr.size() - 1;
-  g.k5v.n_gcons = (int64_t)g.h5_gcons.size();
+  g.k5v.n_gcons = (int64_t)(wide ? g.h5_gcons32.size() : g.h5_gcons.size());
   g.k5v.ok = 1;
 }
 
@@ -741,7 +764,7 @@ int rm_graph_create(const RmGraphDesc* d, uint32_t flags, RmGraph** out) {
     if (!e && g->k5v.ok) e = up(g->k5v.dtgt, g->h5_dtgt);
     if (!e && g->k5v.ok) e = up(g->k5v.g4, g->h5_g4);
     if (!e && g->k5v.ok) e = up(g->k5v.gptr, g->h5_gptr);
-    if (!e && g->k5v.ok) e = up(g->k5v.gcons, g->h5_gcons);
+    if (!e && g->k5v.ok) e = g->h5_gcons32.empty() ? up(g->k5v.gcons, g->h5_gcons) : up(g->k5v.gcons, g->h5_gcons32);
     if (!e && g->gen.ok) e = up(g->gen.eptr, g->gen.h_eptr);
     if (!e && g->gen.ok) e = up(g->gen.edges, g->gen.h_edges);
     if (!e && g->gen.ok) e = up(g->gen.zero, g->gen.h_zero);

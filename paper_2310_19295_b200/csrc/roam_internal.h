@@ -206,6 +206,7 @@ struct RmGraph {
   std::vector<int32_t> h5_tab;
   std::vector<uint32_t> h5_dpair, h5_dtgt, h5_gptr, h5_g4;
   std::vector<uint16_t> h5_gcons;
+  std::vector<uint32_t> h5_gcons32;  // WIDE v5 (more than 8,192 slots)
   roam::DevBuf d_size, d_producer, d_cons_ptr, d_cons_idx, d_in_ptr, d_in_idx, d_out_ptr,
       d_out_idx, d_pred_ptr, d_pred_idx, d_succ_ptr, d_succ_idx;
 };

@@ -189,7 +189,7 @@ def test_both_k1_variants_vs_c_oracle(name, variant):
     (invalid -> valid=False)."""
     from paper_2310_19295_b200.evaluator import device_graph, set_k1_variant
     g = load_graph(gg.config_doc(name))
-    assert device_graph(g).info()["k1_variant"] == (4 if name in ("layered", "gpt2-xl") else 5)
+    assert device_graph(g).info()["k1_variant"] == (4 if name == "layered" else 5)
     B = 1501
     host = generate_orders(g, 7, 0, B).cpu().numpy()
     rng = np.random.default_rng(0)
