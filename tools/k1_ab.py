@@ -1,4 +1,4 @@
-"""A/B timing of the K1 evaluator variants (1 generic, 2 v2, 3 v3 pairs, 4 v4) on the
+"""A/B timing of the K1 evaluator variants (1 generic, 4 v4, 5 v5) on the
 config graphs: device-resident counter-RNG candidates, CUDA events on the
 launching stream, L2 flushed between launches.  Prints one JSON line per
 (graph, variant) with ms per launch and GB/s of algorithmic traffic."""
@@ -27,7 +27,7 @@ def main():
         B = 16384 if n < 4000 else 8192
         orders = ev.generate_orders(g, 0, 0, B)
         ref = None
-        for variant in (1, 2, 3, 4):
+        for variant in (1, 4, 5):
             ev.set_k1_variant(variant)
             out = ev.evaluate_orders(g, orders)
             torch.cuda.synchronize()
