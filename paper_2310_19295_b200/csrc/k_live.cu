@@ -40,13 +40,11 @@ __global__ void __launch_bounds__(KL_NT) k_live_batch(int n, int T, int64_t B, c
   long long* delta = reinterpret_cast<long long*>(smem);               // [n + 1]
   int* pos = reinterpret_cast<int*>(smem + 8 * (size_t(n) + 1));        // [n]
   __shared__ long long wsum[KL_NT / 32];
-  __shared__ int s_bad;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int64_t c = blockIdx.x; c < B; c += gridDim.x) {
     const RowT* row = orders + c * int64_t(n);
     for (int k = tid; k < n; k += KL_NT) pos[k] = -1;
     for (int k = tid; k <= n; k += KL_NT) delta[k] = 0;
-    if (tid == 0) s_bad = 0;
     __syncthreads();
     int bad = 0;
     for (int k = tid; k < n; k += KL_NT) {
@@ -54,22 +52,21 @@ __global__ void __launch_bounds__(KL_NT) k_live_batch(int n, int T, int64_t B, c
       if (o < 0 || o >= n) bad = 1;
       else if (atomicExch(pos + o, k) != -1) bad = 1;  // a duplicate: some id stays -1
     }
-    if (bad) s_bad = 1;
-    __syncthreads();
+    bad = __syncthreads_or(bad);
     // every direct predecessor strictly earlier (pos -1 = missing id: invalid)
-    bad = 0;
-    for (int v = tid; v < n && !s_bad; v += KL_NT) {
-      const int pv = pos[v];
-      if (pv < 0) {
-        bad = 1;
-        break;
+    if (!bad) {
+      for (int v = tid; v < n && !bad; v += KL_NT) {
+        const int pv = pos[v];
+        if (pv < 0) {
+          bad = 1;
+          break;
+        }
+        for (int q = pred_ptr[v]; q < pred_ptr[v + 1]; ++q)
+          if (pos[pred_idx[q]] >= pv) bad = 1;
       }
-      for (int q = pred_ptr[v]; q < pred_ptr[v + 1]; ++q)
-        if (pos[pred_idx[q]] >= pv) bad = 1;
     }
-    if (bad) s_bad = 1;
-    __syncthreads();
-    const bool ok = !s_bad;
+    bad = __syncthreads_or(bad);
+    const bool ok = !bad;
     if (tid == 0) valid[c] = ok ? 1 : 0;
     if (ok) {
       for (int t = tid; t < T; t += KL_NT) {

@@ -53,6 +53,7 @@ def main():
     gen_ms = eval_ms = 0.0
     best = torch.tensor([NONE_PEAK, -1], dtype=torch.int64, device=dev)
     valid_total = 0
+    events = []
     if world > 1:
         dist.barrier()
     for c0 in range(lo, hi, a.chunk):
@@ -66,10 +67,13 @@ def main():
         take = (cb[1] >= 0) & ((best[1] < 0) | (cb[0] < best[0]))
         best = torch.where(take, cb, best)
         e[2].record()
-        torch.cuda.synchronize()
+        events.append(e)
+        valid_total = valid_total + valid.sum()   # on the device: no host sync per chunk
+    torch.cuda.synchronize()
+    for e in events:
         gen_ms += e[0].elapsed_time(e[1])
         eval_ms += e[1].elapsed_time(e[2])
-        valid_total += int(valid.sum().item())
+    valid_total = int(valid_total)
     x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     x0.record()
     if world > 1:
