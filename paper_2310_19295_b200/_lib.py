@@ -47,7 +47,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     nvcc = _nvcc()
     objdir = PKG / "build"
     objdir.mkdir(exist_ok=True)
-    common = [nvcc, "-std=c++17", "-O3", ARCH, "-lineinfo", "-Xcompiler", "-fPIC,-O3",
+    common = [nvcc, "-std=c++17", "-O3", ARCH, "-lineinfo", "-Xcompiler", "-fPIC,-O3,-mpopcnt",
               "-I", str(ROOT / "include")]
 
     def compile_one(src: Path) -> Path:

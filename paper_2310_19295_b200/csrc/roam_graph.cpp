@@ -884,14 +884,32 @@ int rm_graph_asap_alap(const RmGraph* g, int32_t* asap, int32_t* alap) {
     for (size_t i = 0; i < words; ++i) c += __builtin_popcountll(desc[size_t(v) * words + i]);
     alap[v] = n - 1 - c;
   }
-  // ancestors: column counts of the descendant matrix
-  std::vector<int32_t> cnt(n, 0);
-  for (int u = 0; u < n; ++u) {
-    const uint64_t* du = &desc[size_t(u) * words];
-    for (size_t i = 0; i < words; ++i)
-      for (uint64_t w = du[i]; w; w &= w - 1) ++cnt[i * 64 + __builtin_ctzll(w)];
+  // ancestors: the same sweep forward over direct_preds (reusing the buffer),
+  // popcounts per row -- not column counts of the descendant matrix, which
+  // visit every one of the O(n^2) closure bits
+  std::vector<int32_t> indeg(n), topo;
+  topo.reserve(n);
+  for (int v = 0; v < n; ++v) indeg[v] = g->pred_ptr[v + 1] - g->pred_ptr[v];
+  for (int v = 0; v < n; ++v)
+    if (!indeg[v]) topo.push_back(v);
+  for (size_t h = 0; h < topo.size(); ++h) {
+    const int u = topo[h];
+    for (int k = g->succ_ptr[u]; k < g->succ_ptr[u + 1]; ++k)
+      if (--indeg[g->succ_idx[k]] == 0) topo.push_back(g->succ_idx[k]);
   }
-  std::memcpy(asap, cnt.data(), sizeof(int32_t) * size_t(n));
+  std::fill(desc.begin(), desc.end(), 0ull);
+  for (const int v : topo) {
+    uint64_t* av = &desc[size_t(v) * words];
+    for (int k = g->pred_ptr[v]; k < g->pred_ptr[v + 1]; ++k) {
+      const int p = g->pred_idx[k];
+      const uint64_t* ap = &desc[size_t(p) * words];
+      for (size_t i = 0; i < words; ++i) av[i] |= ap[i];
+      av[p >> 6] |= 1ull << (p & 63);
+    }
+    int c = 0;
+    for (size_t i = 0; i < words; ++i) c += __builtin_popcountll(av[i]);
+    asap[v] = c;
+  }
   return RM_OK;
 }
 
