@@ -404,8 +404,9 @@ int rm_set_k1_variant(int variant);
 int rm_set_sm_reserve(int sms);
 /* Candidate generator form on this thread: 0 auto (one thread per candidate
  * when the graph qualifies, the rows it cannot finish rewritten by the warp
- * form), 1 the warp form only (one warp per candidate).  Same rows either
- * way; for tests and A/B measurement. */
+ * form), 1 the warp form only (one warp per candidate), 40 / 64 the thread
+ * form with that heap capacity.  Same rows either way; for tests and A/B
+ * measurement. */
 int rm_set_gen_form(int form);
 double rm_last_kernel_ms(void);
 

@@ -301,7 +301,7 @@ void build_gen_meta(RmGraph& g) {
 }
 
 static thread_local int t_gen_form = 0;  // 0 auto, 1 warp form only
-static thread_local int t_gen_cap = 0;   // thread form heap entries: 32, 40, 48, 64; 0 = by graph size
+static thread_local int t_gen_cap = 0;   // thread form heap entries: 40 or 64; 0 = by graph size
 
 static int launch_gen_warp(RmGraph* g, uint64_t seed, int64_t first_id, int64_t B, int32_t* out,
                            const int32_t* redo, const unsigned* n_redo, cudaStream_t s) {
@@ -342,7 +342,7 @@ int launch_gen(RmGraph* g, uint64_t seed, int64_t first_id, int64_t B, int32_t* 
   const bool narrow = n_edges < 65536;
   auto a16 = [](size_t x) { return (x + 15) & ~size_t(15); };
   const size_t table = a16(4 * size_t(n_edges)) + a16((narrow ? 2 : 4) * (size_t(g->n) + 1));
-  // heap capacity (rm_set_gen_form 32/40/48/64 for A/B).  Default 40 below
+  // heap capacity (rm_set_gen_form 40/64 for A/B).  Default 40 below
   // 8k ops (GPT-2 small / BERT-large: ready sets reach ~37), 64 above (the
   // 11k-op GPT2-XL's reach further: 40 entries hand ~1 % of its rows to the
   // slow warp form, 3.25 vs 3.50 M/s measured); a candidate that outgrows the
@@ -370,9 +370,9 @@ int launch_gen(RmGraph* g, uint64_t seed, int64_t first_id, int64_t B, int32_t* 
                                                       m.n_zero, m.words, table, out, redo, n_redo);     \
   }
   if (narrow) {
-    RM_GEN_CASE(uint16_t, 32) RM_GEN_CASE(uint16_t, 40) RM_GEN_CASE(uint16_t, 48) RM_GEN_CASE(uint16_t, 64)
+    RM_GEN_CASE(uint16_t, 40) RM_GEN_CASE(uint16_t, 64)
   } else {
-    RM_GEN_CASE(uint32_t, 32) RM_GEN_CASE(uint32_t, 40) RM_GEN_CASE(uint32_t, 48) RM_GEN_CASE(uint32_t, 64)
+    RM_GEN_CASE(uint32_t, 40) RM_GEN_CASE(uint32_t, 64)
   }
 #undef RM_GEN_CASE
   RM_LAUNCH_CHECK("k_gen_thread launch");
@@ -384,8 +384,8 @@ int launch_gen(RmGraph* g, uint64_t seed, int64_t first_id, int64_t B, int32_t* 
 }  // namespace roam
 
 extern "C" int rm_set_gen_form(int form) {
-  // 0 auto, 1 warp form; 32/40/48/64 = auto with that heap capacity (A/B)
-  if (form == 32 || form == 40 || form == 48 || form == 64) {
+  // 0 auto, 1 warp form; 40/64 = auto with that heap capacity (A/B)
+  if (form == 40 || form == 64) {
     roam::t_gen_form = 0;
     roam::t_gen_cap = form;
     return RM_OK;

@@ -126,7 +126,7 @@ def test_generator_thread_form_equals_warp_form(name):
         set_gen_form(0)
     assert np.array_equal(got, want)
     if name in ("gpt2-xl", "layered"):   # the other heap capacities (A/B settings)
-        for cap in (32, 48, 64):
+        for cap in (40, 64):
             set_gen_form(cap)
             try:
                 assert np.array_equal(generate_orders(g, 17, 123, B).cpu().numpy(), want), cap

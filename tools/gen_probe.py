@@ -15,7 +15,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--graphs", nargs="+", default=["gpt2-small", "gpt2-xl"])
 ap.add_argument("--B", type=int, default=65536)
 ap.add_argument("--once", action="store_true")
-ap.add_argument("--forms", type=int, nargs="+", default=[0, 1], help="0 auto, 1 warp form, 32/40/48/64 heap caps")
+ap.add_argument("--forms", type=int, nargs="+", default=[0, 1], help="0 auto, 1 warp form, 40/64 heap caps")
 a = ap.parse_args()
 for name in a.graphs:
     g = load_graph(gg.config_doc(name))
