@@ -58,30 +58,46 @@ struct K4Args {
   const int64_t* gscratch_off;  // [W] (-1: shared memory)
 };
 
-__host__ __device__ inline size_t k4_bytes(int64_t n_ops, int64_t n_ten) {
-  auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
-  return al(8 * size_t(n_ops)) + al(4 * size_t(n_ops)) + al(size_t(n_ops)) + al(4 * size_t(n_ten)) +
-         al(4 * size_t(n_ops));
-}
+// Working set of one window (all 16-byte aligned): delta int64[n], npred
+// int16[n] (-1 once the op ran), in / succ CSR starts u32[n + 1] each, ready
+// int32[n], counts u16[nt].  Compact so that an 8.6k-op window (GPT2-XL's)
+// still fits one CTA's shared memory with its CSR starts staged.
+struct K4Layout {
+  size_t o_delta, o_npred, o_inp, o_sup, o_ready, o_cnt, bytes;
+  __host__ __device__ K4Layout(int64_t n, int64_t nt) {
+    auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
+    o_delta = 0;
+    o_npred = al(o_delta + 8 * size_t(n));
+    o_inp = al(o_npred + 2 * size_t(n));
+    o_sup = al(o_inp + 4 * (size_t(n) + 1));
+    o_ready = al(o_sup + 4 * (size_t(n) + 1));
+    o_cnt = al(o_ready + 4 * size_t(n));
+    bytes = al(o_cnt + 2 * size_t(nt));
+  }
+};
+__host__ __device__ inline size_t k4_bytes(int64_t n_ops, int64_t n_ten) { return K4Layout(n_ops, n_ten).bytes; }
 
 // One warp per window.  The ready ops (all predecessors scheduled) sit in a
 // compact list -- a training window's ready set is tens of ops, so a step
 // scores only those instead of sweeping the whole window -- and everything
 // runs inside the warp: no block barrier anywhere on the step's critical path.
+// The pick is a REDUX argmin of the packed key (score << 16 | local index:
+// |score| < 2^47, local indices < 2^16), and the ops' CSR starts are staged in
+// the working set, so a step's first dependent loads are shared-memory ones.
 __global__ void __launch_bounds__(32) k4_greedy(const K4Args a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int w = blockIdx.x, lane = threadIdx.x;
   const int64_t ob = a.op_base[w], tb = a.ten_base[w];
   const int n = a.nops[w];
   const int nt = (int)(a.ten_base[w + 1] - tb);
-  auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
+  const K4Layout L(n, nt);
   unsigned char* ws = a.gscratch_off[w] < 0 ? smem : a.gscratch + a.gscratch_off[w];
-  long long* delta = reinterpret_cast<long long*>(ws);  // out - bytes freed if run now
-  int* npred = reinterpret_cast<int*>(ws + al(8 * size_t(n)));
-  unsigned char* done = ws + al(8 * size_t(n)) + al(4 * size_t(n));
-  int* cnt = reinterpret_cast<int*>(ws + al(8 * size_t(n)) + al(4 * size_t(n)) + al(size_t(n)));
-  int* ready = reinterpret_cast<int*>(ws + al(8 * size_t(n)) + al(4 * size_t(n)) + al(size_t(n)) +
-                                      al(4 * size_t(nt)));
+  long long* delta = reinterpret_cast<long long*>(ws + L.o_delta);  // out - bytes freed if run now
+  short* npred = reinterpret_cast<short*>(ws + L.o_npred);
+  uint32_t* inp = reinterpret_cast<uint32_t*>(ws + L.o_inp);
+  uint32_t* sup = reinterpret_cast<uint32_t*>(ws + L.o_sup);
+  int* ready = reinterpret_cast<int*>(ws + L.o_ready);
+  unsigned short* cnt = reinterpret_cast<unsigned short*>(ws + L.o_cnt);
   const int64_t* tc_ptr = a.tc_ptr + tb;
   const int64_t* out = a.out + ob;
   const int64_t* in_ptr = a.in_ptr + ob;
@@ -89,13 +105,19 @@ __global__ void __launch_bounds__(32) k4_greedy(const K4Args a) {
   const int64_t* tsize = a.tsize + tb;
   const unsigned lt = (1u << lane) - 1u;
   int R = 0;
+  for (int i0 = 0; i0 <= n; i0 += 32) {
+    const int i = i0 + lane;
+    if (i <= n) {
+      inp[i] = (uint32_t)in_ptr[i];
+      sup[i] = (uint32_t)succ_ptr[i];
+    }
+  }
   for (int i0 = 0; i0 < n; i0 += 32) {
     const int i = i0 + lane;
     bool rd = false;
     if (i < n) {
       const int np = a.npred0[ob + i];
-      npred[i] = np;
-      done[i] = 0;
+      npred[i] = (short)np;
       // the score is kept up to date instead of recomputed every step: an
       // input frees when its count is 1, and counts only fall when an op runs
       long long freed = 0;
@@ -110,7 +132,7 @@ __global__ void __launch_bounds__(32) k4_greedy(const K4Args a) {
     if (rd) ready[R + __popc(m & lt)] = i;
     R += __popc(m);
   }
-  for (int t = lane; t < nt; t += 32) cnt[t] = a.count0[tb + t];
+  for (int t = lane; t < nt; t += 32) cnt[t] = (unsigned short)a.count0[tb + t];
   long long live = a.start_live[w], peak = live;
   __syncwarp();
 
@@ -120,40 +142,36 @@ __global__ void __launch_bounds__(32) k4_greedy(const K4Args a) {
       return;
     }
     // ---- score the ready ops: min (delta, local index) -- the reference's
-    // strict < over ascending local index
-    long long bv = LLONG_MAX;
-    int bi = INT_MAX, bs = -1;
+    // strict < over ascending local index -- as one packed key, two REDUX
+    long long bk = LLONG_MAX;
+    int bs = -1;
     for (int j = lane; j < R; j += 32) {
       const int i = ready[j];
-      const long long d = delta[i];
-      if (d < bv || (d == bv && i < bi)) {
-        bv = d;
-        bi = i;
+      const long long key = (delta[i] << 16) | (long long)i;
+      if (key < bk) {
+        bk = key;
         bs = j;
       }
     }
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) {
-      const long long ov = __shfl_xor_sync(0xffffffffu, bv, d);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, d);
-      const int os = __shfl_xor_sync(0xffffffffu, bs, d);
-      if (ov < bv || (ov == bv && oi < bi)) {
-        bv = ov;
-        bi = oi;
-        bs = os;
-      }
-    }
+    const int khi = (int)(bk >> 32);
+    const unsigned klo = (unsigned)bk;
+    const int mhi = __reduce_min_sync(0xffffffffu, khi);
+    const unsigned mlo = __reduce_min_sync(0xffffffffu, khi == mhi ? klo : 0xffffffffu);
+    const unsigned win = __ballot_sync(0xffffffffu, khi == mhi && klo == mlo);
+    bs = __shfl_sync(0xffffffffu, bs, __ffs(win) - 1);
+    const int bi = (int)(mlo & 0xffffu);
     // ---- apply the pick: inputs' counts (a count reaching 1 moves the free
     // to the one consumer entry left), successors' predecessor counts
     long long freed = 0;
-    for (int64_t k = in_ptr[bi] + lane; k < in_ptr[bi + 1]; k += 32) {
+    const uint32_t i0 = inp[bi], i1 = inp[bi + 1];
+    for (uint32_t k = i0 + lane; k < i1; k += 32) {
       const int t = __ldg(a.in_idx + k);
-      const int c = --cnt[t];  // distinct inputs: no races
+      const int c = (int)--cnt[t];  // distinct inputs: no races
       if (c == 0) freed += tsize[t];
       if (c == 1) {
         for (int64_t q = tc_ptr[t]; q < tc_ptr[t + 1]; ++q) {
           const int j = __ldg(a.tc_idx + q);
-          if (j != bi && !done[j]) {
+          if (j != bi && npred[j] >= 0) {
             atomicAdd(reinterpret_cast<unsigned long long*>(delta + j), (unsigned long long)(-tsize[t]));
             break;
           }
@@ -162,15 +180,16 @@ __global__ void __launch_bounds__(32) k4_greedy(const K4Args a) {
     }
     __syncwarp();
     if (lane == 0) {
-      done[bi] = 1;
+      npred[bi] = -1;            // ran
       ready[bs] = ready[R - 1];  // the list is unordered: the last entry fills the hole
     }
     --R;
     __syncwarp();
-    for (int64_t k = succ_ptr[bi]; k < succ_ptr[bi + 1]; k += 32) {
+    const uint32_t s0 = sup[bi], s1 = sup[bi + 1];
+    for (uint32_t k = s0; k < s1; k += 32) {
       bool rd = false;
       int sv = 0;
-      if (k + lane < succ_ptr[bi + 1]) {
+      if (k + lane < s1) {
         sv = __ldg(a.succ_idx + k + lane);
         rd = --npred[sv] == 0;  // distinct successors
       }
@@ -380,6 +399,16 @@ extern "C" int rm_greedy_windows(RmGraph* g, int32_t W, const int64_t* win_ptr,
   };
   std::vector<int32_t> nops(W);
   for (int w = 0; w < W; ++w) nops[w] = (int32_t)(op_base[w + 1] - op_base[w]);
+  // the device's compact working set (K4Layout) and packed argmin key
+  for (int w = 0; w < W; ++w)
+    if (nops[w] >= 65536) return fail(RM_ERR_CAPACITY, "greedy window above 65,535 ops");
+  for (const int32_t c : count0)
+    if (c > 65535) return fail(RM_ERR_CAPACITY, "greedy window: a tensor with more than 65,535 local uses");
+  for (const int32_t d : npred0)
+    if (d > 32767) return fail(RM_ERR_CAPACITY, "greedy window: an op with more than 32,767 local preds");
+  if (in_idx.size() >= (size_t(1) << 32) || succ_idx.size() >= (size_t(1) << 32))
+    return fail(RM_ERR_CAPACITY, "greedy windows: CSR above 2^32 entries");
+  if (g->info.total_bytes >= (int64_t(1) << 46)) return fail(RM_ERR_CAPACITY, "greedy windows: scores above 2^46 bytes");
   int32_t* d_nops;
   RM_CUDA(up(&d_ob, opb_dev));
   RM_CUDA(up(&d_nops, nops));
