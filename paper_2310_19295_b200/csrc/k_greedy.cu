@@ -44,6 +44,7 @@ struct K4Args {
   const int32_t* npred0;    // [NO] distinct local preds
   const int64_t* in_ptr;    // [NO+1] into in_idx (window-local tensor index)
   const int32_t* in_idx;
+  const int64_t* in_sz;     // size of each in_idx entry's tensor (loaded in parallel with it)
   const int64_t* succ_ptr;  // [NO+1] into succ_idx (window-local op index)
   const int32_t* succ_idx;
   const int32_t* count0;    // [NT_] tracked consumer-entry counts
@@ -166,13 +167,14 @@ __global__ void __launch_bounds__(32) k4_greedy(const K4Args a) {
     const uint32_t i0 = inp[bi], i1 = inp[bi + 1];
     for (uint32_t k = i0 + lane; k < i1; k += 32) {
       const int t = __ldg(a.in_idx + k);
+      const long long tsz = __ldg(a.in_sz + k);
       const int c = (int)--cnt[t];  // distinct inputs: no races
-      if (c == 0) freed += tsize[t];
+      if (c == 0) freed += tsz;
       if (c == 1) {
         for (int64_t q = tc_ptr[t]; q < tc_ptr[t + 1]; ++q) {
           const int j = __ldg(a.tc_idx + q);
           if (j != bi && npred[j] >= 0) {
-            atomicAdd(reinterpret_cast<unsigned long long*>(delta + j), (unsigned long long)(-tsize[t]));
+            atomicAdd(reinterpret_cast<unsigned long long*>(delta + j), (unsigned long long)(-tsz));
             break;
           }
         }
@@ -246,6 +248,7 @@ extern "C" int rm_greedy_windows(RmGraph* g, int32_t W, const int64_t* win_ptr,
   std::vector<uint8_t> is_lin(T, 0), is_lout(T, 0);
   std::vector<int64_t> op_base(W + 1, 0), ten_base(W + 1, 0), start_live(W, 0);
   std::vector<int32_t> gop, npred0, in_idx, succ_idx, count0, tc_idx;
+  std::vector<int64_t> in_sz;
   std::vector<int64_t> out_b, in_ptr(1, 0), succ_ptr(1, 0), tsize, tc_ptr(1, 0);
   std::vector<int32_t> ops, rel, tmp;
   std::vector<std::vector<int32_t>> succ;
@@ -320,6 +323,7 @@ extern "C" int rm_greedy_windows(RmGraph* g, int32_t W, const int64_t* win_ptr,
       std::sort(tmp.begin(), tmp.end());
       tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
       in_idx.insert(in_idx.end(), tmp.begin(), tmp.end());
+      for (const int32_t t : tmp) in_sz.push_back(tsize[size_t(tb + t)]);
       in_ptr.push_back((int64_t)in_idx.size());
       tmp.clear();
       for (int k = g->in_ptr[v]; k < g->in_ptr[v + 1]; ++k) {
@@ -435,9 +439,10 @@ extern "C" int rm_greedy_windows(RmGraph* g, int32_t W, const int64_t* win_ptr,
   RM_CUDA(cudaMemsetAsync(d_st, 0, size_t(W) * 4, s));
   RM_CUDA(cudaMemsetAsync(d_ord, 0xff, size_t(std::max<int64_t>(opb_dev[W], 1)) * 4, s));
   if (gbytes) RM_CUDA(sc.alloc(&d_g, gbytes));
-  K4Args a{W, d_ob, d_nops, d_tb, d_gop, d_out, d_np, d_inp, d_ini, d_sup, d_sui, d_c0, d_tcp, d_tci,
+  int64_t* d_insz;
+  RM_CUDA(up(&d_insz, in_sz));
+  K4Args a{W, d_ob, d_nops, d_tb, d_gop, d_out, d_np, d_inp, d_ini, d_insz, d_sup, d_sui, d_c0, d_tcp, d_tci,
            d_tsz, d_sl, d_ord, d_peak, d_st, d_g, d_goff};
-  // wide windows: more threads, fewer ops per thread in each step's score scan
   int rc = launch_k4(a, smem, s);
   if (rc) return rc;
   std::vector<int32_t> ord_w(opb_dev[W]), st_dev(W);
