@@ -173,34 +173,19 @@ struct K3Block {
     return w > 0 ? max(before, ex) : ex;
   }
   __device__ int min_key1(int key, long long val, long long* out_val, int* mi, long long* mv) {
+    // keys are distinct slot indices (or INT_MAX): one redux.min, and the
+    // lane that holds the minimum publishes its value
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) {
-      const int ok = __shfl_xor_sync(0xffffffffu, key, d);
-      const long long ov = __shfl_xor_sync(0xffffffffu, val, d);
-      if (ok < key) {
-        key = ok;
-        val = ov;
-      }
-    }
-    if (lane == 0) {
-      mi[w] = key;
-      mv[w] = val;
-    }
+    const int wk = __reduce_min_sync(0xffffffffu, key);
+    const unsigned hit = __ballot_sync(0xffffffffu, key == wk);
+    if (lane == 0) mi[w] = wk;
+    if (key == wk && lane == __ffs(hit) - 1) mv[w] = val;
     __syncthreads();
     key = lane < NW ? mi[lane] : INT_MAX;
-    val = lane < NW ? mv[lane] : 0;
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) {  // over all 32 lanes: every lane gets the answer
-      const int ok = __shfl_xor_sync(0xffffffffu, key, d);
-      const long long ov = __shfl_xor_sync(0xffffffffu, val, d);
-      if (ok < key) {
-        key = ok;
-        val = ov;
-      }
-    }
-    *out_val = val;
-    return key;
+    const int bk = __reduce_min_sync(0xffffffffu, key);
+    const unsigned bw = __ballot_sync(0xffffffffu, key == bk);
+    *out_val = mv[__ffs(bw) - 1];  // every lane: the first warp holding the minimum
+    return bk;
   }
   // (min key, its value) over the block; key INT_MAX = none
   __device__ int min_key(int key, long long val, long long* out_val) {

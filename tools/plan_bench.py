@@ -71,7 +71,7 @@ def main():
             row["identical"] = got == ref
             row["speedup"] = row["reference_s"] / row["b200_s"]
         s = io.StringIO()
-        pstats.Stats(prof, stream=s).sort_stats("cumulative").print_stats(14)
+        pstats.Stats(prof, stream=s).sort_stats("cumulative").print_stats(30)
         row["b200_top_cumulative"] = [l.strip() for l in s.getvalue().splitlines()
                                       if l.strip() and l.strip()[0].isdigit()][:14]
         doc = json.loads(got)
