@@ -8,14 +8,14 @@ there is no CPU fallback.
 
 from .graph import (ConfigError, Graph, GraphError, GraphFormatError, OpKind, OpNode, Schedule,
                     ScheduleError, StructuralError, TensorCategory, TensorInfo, classify_tensors,
-                    graph_to_doc, load_graph, load_graph_json, validate_graph)
+                    load_graph)
 from .evaluator import (argmin_orders, evaluate_orders, generate_orders, live_bytes_by_timestep,
                         peak_memory, sequential_schedule, tensor_lifetimes, validate_schedule)
 
 __all__ = [
     "ConfigError", "Graph", "GraphError", "GraphFormatError", "OpKind", "OpNode", "Schedule",
     "ScheduleError", "StructuralError", "TensorCategory", "TensorInfo", "classify_tensors",
-    "graph_to_doc", "load_graph", "load_graph_json", "validate_graph", "argmin_orders",
+    "load_graph", "argmin_orders",
     "evaluate_orders", "generate_orders", "live_bytes_by_timestep", "peak_memory",
     "sequential_schedule", "tensor_lifetimes", "validate_schedule",
 ]

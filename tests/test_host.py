@@ -179,3 +179,49 @@ def test_bench_reference_arm_contract():
     assert cb["kind"] in ("port", "reference") and cb["cores"] >= 1 and cb["value"] == line["value"]
     assert line["e2e"] == {"value": line["value"], "unit": line["unit"], "h2d_bytes_per_step": 0,
                            "d2h_bytes_per_step": 0}
+
+
+def test_load_graph_matches_reference_loader():
+    """The CSR-first loader builds the reference's graph (graph.py:188-278):
+    same ops, tensors, consumer entries and categories on the config graphs
+    and the reference's own generators, and the same exception class and
+    message, in the same order, on malformed documents."""
+    import sys
+    from pathlib import Path
+    ref = Path(__file__).resolve().parents[1] / "baseline" / "_ref"
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    rg = pytest.importorskip("memplan.graph")
+    rgen = pytest.importorskip("memplan.graphgen")
+    from paper_2310_19295_b200 import graphgen as gg
+    docs = [gg.config_doc(n) for n in ("layered", "gpt2-small", "bert-large")]
+    docs += [rg.graph_to_doc(rgen.gen_training_graph(a, 3, optimizer=o))
+             for a in ("mlp", "residual", "transformer_block") for o in ("sgd", "adam")]
+    docs += [rg.graph_to_doc(rgen.gen_random_dag(12 + k, density=0.3, seed=k)) for k in range(6)]
+    for d in docs:
+        a, b = rg.load_graph(d), load_graph(d)
+        assert [(o.id, o.name, o.kind.value, o.inputs, o.outputs) for o in a.ops] == \
+               [(o.id, o.name, o.kind.value, o.inputs, o.outputs) for o in b.ops]
+        assert [(t.id, t.size, t.producer, t.consumers, t.category.value) for t in a.tensors] == \
+               [(t.id, t.size, t.producer, t.consumers, t.category.value) for t in b.tensors]
+    bad = [
+        {"tensors": []},
+        {"ops": [], "tensors": [{"id": 1, "size_bytes": 3}, {"id": 1, "size_bytes": 3}]},
+        {"ops": [{"id": "a"}], "tensors": []},
+        {"ops": [{"id": 0, "outputs": [5]}], "tensors": [{"id": 1, "size_bytes": 3}]},
+        {"ops": [{"id": 0, "outputs": [1]}, {"id": 1, "outputs": [1]}], "tensors": [{"id": 1, "size_bytes": 3}]},
+        {"ops": [{"id": 0, "outputs": [1, 1]}], "tensors": [{"id": 1, "size_bytes": 3}]},
+        {"ops": [{"id": 0, "outputs": [1, 7]}, {"id": 1, "outputs": [1]}], "tensors": [{"id": 1, "size_bytes": 3}]},
+        {"ops": [{"id": 0, "outputs": [1], "kind": "zz"}], "tensors": [{"id": 1, "size_bytes": 3}]},
+        {"ops": [{"id": 0, "outputs": []}], "tensors": [{"id": 1, "size_bytes": 3}]},
+        {"ops": [{"id": 0, "outputs": [1]}], "tensors": [{"id": 1, "size_bytes": "x"}]},
+        {"ops": [{"id": 0, "outputs": [1]}], "tensors": [{"id": 1, "size_bytes": 3, "category": "nope"}]},
+        {"ops": [{"id": 0, "outputs": [1], "inputs": [2]}, {"id": 1, "outputs": [2], "inputs": [1]}],
+         "tensors": [{"id": 1, "size_bytes": 3}, {"id": 2, "size_bytes": 3}]},
+    ]
+    for d in bad:
+        with pytest.raises(Exception) as want:
+            rg.load_graph(d)
+        with pytest.raises(Exception) as got:
+            load_graph(d)
+        assert (type(got.value).__name__, str(got.value)) == (type(want.value).__name__, str(want.value))
