@@ -1,12 +1,13 @@
-// K1 v4: the default candidate-order evaluator.
+// K1 v4: the candidate-order evaluator for unit-packed graphs whose classes
+// do not fit v5's one-byte form (the layered DAG).
 //
 // Reference: pkg/src/memplan/graph.py:375-468 (validate_schedule,
 // sequential_schedule, tensor_lifetimes, live_bytes_by_timestep, peak_memory).
 //
-// Same arithmetic as v2 (k_eval_v2.cu): live[k] = sum_{j<k}(out - free)(o_j)
-// + out(o_k) over unit-packed {fs, out} words, multi-consumer frees added at
-// the latest maximal consumer's position.  What changes is how little each
-// position costs:
+// live[k] = sum_{j<k}(out - free)(o_j) + out(o_k) over unit-packed {fs, out}
+// words (K1V2Meta's opv: byte counts in units of 2^shift), multi-consumer
+// frees added at the latest maximal consumer's position.  Against the generic
+// evaluator (k_eval.cu) what changes is how little each position costs:
 //   * compile-time geometry: SL = NT * C slots, every thread owns exactly C
 //     positions (padding slot k >= n holds op id k, zero bytes), so no loop
 //     carries a runtime guard;
