@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(256) k_gen_orders(int n, uint64_t seed, int64_
 
 // ---------------------------------------------------------------------------
 // Thread-per-candidate form (the default when the graph qualifies, GenMeta):
-// each thread runs one candidate's Kahn order alone, its ready set a binary
+// each thread runs one candidate's Kahn order alone, its ready set a 4-ary
 // min-heap of full 64-bit keys and its predecessor-arrival counters
 // lane-interleaved in shared memory (word k of lane l at [k * 32 + l]):
 // whatever heap slot or counter each thread of a warp touches, the warp's
