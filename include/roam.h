@@ -408,6 +408,11 @@ int rm_set_sm_reserve(int sms);
  * form with that heap capacity.  Same rows either way; for tests and A/B
  * measurement. */
 int rm_set_gen_form(int form);
+/* K3 placement form on this thread: 0 auto (DAG rounds for problems of
+ * 1,024 items or more, where they qualify), 1 the placed-list path only,
+ * 2 DAG rounds wherever they qualify.  Same offsets either way; for tests
+ * and A/B measurement. */
+int rm_set_pack_form(int form);
 double rm_last_kernel_ms(void);
 
 #ifdef __cplusplus

@@ -143,6 +143,7 @@ SIGNATURES = {
     "rm_set_k1_variant": (C.c_int, [C.c_int]),
     "rm_set_sm_reserve": (C.c_int, [C.c_int]),
     "rm_set_gen_form": (C.c_int, [C.c_int]),
+    "rm_set_pack_form": (C.c_int, [C.c_int]),
     "rm_nccl_unique_id": (C.c_int, [vp, C.c_int64]),
     "rm_nccl_comm_init": (C.c_int, [C.c_int32, vp, C.c_int32, C.POINTER(vp)]),
     "rm_nccl_comm_destroy": (C.c_int, [vp]),

@@ -47,6 +47,8 @@ struct K3Args {
   int64_t* comp_cap;
   unsigned char* gscratch;     // per-problem working set when it exceeds smem
   const int64_t* gscratch_off;  // [P] byte offsets (-1: use shared memory)
+  unsigned char* dscratch;      // per-problem obstacle lists of the DAG placement
+  const int64_t* dscratch_off;  // [P] byte offsets (-1: the placed-list path)
 };
 
 __host__ __device__ inline int k3_pow2(int n) {
@@ -217,6 +219,198 @@ struct K3Block {
   }
 };
 
+// ---- DAG placement.  _lowest_fit(item, placed, floor) reads only the placed
+// items that overlap the item in time, so item u's offset depends only on the
+// items before it in the placement order that overlap it (its obstacles), and
+// any order respecting that relation gives the reference's offsets.  On the
+// planner's leaves the relation is shallow (GPT2-XL's 9,035-item leaf: 8,020
+// items to place, at most 11 obstacles each, 18 levels), so the CTA places
+// every item whose obstacles are all placed in one round: 18 rounds instead of
+// 8,020 dependent placements.
+//
+// Per item the answer is the smallest candidate c in {floor} U {hi_o >= floor}
+// with no obstacle o such that lo_o < c + size and hi_o > c: the sweep's
+// candidate only ever takes the floor or an obstacle's hi, every value it
+// passes over fails that test against the span that moved it, and the value it
+// returns passes it (spans before the break end at or below it, spans after
+// start at or above its end).
+//
+// Obstacle lists: one pass over the earlier items per item (all lanes of a
+// warp read the same earlier item: broadcast loads), at most K3_DAG_K per item
+// -- a problem with an item over that (or a cycle-free chain too deep to be
+// worth rounds) keeps the placed-list path.
+constexpr int K3_DAG_K = 48;
+constexpr int K3_DAG_SHORT = 32;  // lifetime (end - start) of a short item
+
+struct K3DagLayout {
+  size_t o_se, o_lvl, o_cnt, o_lo, o_hi, o_key, o_idx, bytes;
+  __host__ __device__ K3DagLayout(int N) {
+    auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
+    const size_t n = size_t(N);
+    o_se = 0;                          // int2 {start, end} in placement order
+    o_lvl = al(o_se + 8 * n);          // round an item was placed in (-1: not yet)
+    o_cnt = al(o_lvl + 4 * n);         // obstacle count
+    o_lo = al(o_cnt + 4 * n);          // placed spans
+    o_hi = al(o_lo + 8 * n);
+    o_key = al(o_hi + 8 * n);          // short items sorted by start: start << 32 | position
+    o_idx = al(o_key + 8 * size_t(k3_pow2(N)));  // [n][K3_DAG_K] obstacle positions
+    bytes = al(o_idx + 4 * n * size_t(K3_DAG_K));
+  }
+};
+
+// Places items A..N-1 of the placement order; false (nothing written) when the
+// problem does not qualify.  *cap_rest = max(offset + size) over them.
+template <int NT>
+__device__ bool k3_dag_place(K3Block<NT>& blk, int N, int A, const int* ord, const int* st, const int* en,
+                             const long long* sz, const long long* flo, long long* off, unsigned char* ds,
+                             long long* cap_rest) {
+  const K3DagLayout D(N);
+  int2* se = reinterpret_cast<int2*>(ds + D.o_se);
+  int* lvl = reinterpret_cast<int*>(ds + D.o_lvl);
+  int* cnt = reinterpret_cast<int*>(ds + D.o_cnt);
+  long long* LO = reinterpret_cast<long long*>(ds + D.o_lo);
+  long long* HI = reinterpret_cast<long long*>(ds + D.o_hi);
+  int* idx = reinterpret_cast<int*>(ds + D.o_idx);
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int M = N - A;  // local position u = placement index - A
+  for (int u = tid; u < M; u += NT) {
+    const int q = ord[A + u];
+    se[u] = make_int2(st[q], en[q]);
+    lvl[u] = -1;
+  }
+  __syncthreads();
+  // Obstacle lists.  The placement order is by lifetime, longest first, so
+  // the items longer than K3_DAG_SHORT steps are a prefix [0, NL) and every
+  // obstacle of one of them is in it; an obstacle of a short item u is long,
+  // or short with its start in [start_u - K3_DAG_SHORT, end_u] -- a window of
+  // the short items sorted by start.  A warp takes 32 consecutive targets
+  // (lanes) and walks its candidates with every lane reading the same one.
+  int NL = 0;
+  {
+    int c = 0;
+    for (int u = tid; u < M; u += NT) c += (se[u].y - se[u].x > K3_DAG_SHORT) ? 1 : 0;
+    NL = (int)blk.reduce_sum(c);
+  }
+  const int NS = M - NL, P2 = k3_pow2(max(NS, 1));
+  long long* key = reinterpret_cast<long long*>(ds + D.o_key);
+  for (int j = tid; j < P2; j += NT)
+    key[j] = j < NS ? ((long long)se[NL + j].x << 32) | (unsigned)(NL + j) : LLONG_MAX;
+  __syncthreads();
+  for (int k = 2; k <= P2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = tid; t < (P2 >> 1); t += NT) {
+        const int i = ((t & ~(j - 1)) << 1) | (t & (j - 1));
+        const int l = i | j;
+        const long long x = key[i], y = key[l];
+        if (((i & k) == 0) == (y < x)) {
+          key[i] = y;
+          key[l] = x;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  int over = 0;
+  auto add = [&](int& c, int* mine, int i) {
+    if (c < K3_DAG_K) mine[c] = i;
+    ++c;
+  };
+  // long targets: the earlier long items
+  for (int b = w * 32; b < NL; b += NT) {
+    const int u = b + lane;
+    const bool have = u < NL;
+    const int2 me = have ? se[u] : make_int2(0, 0);
+    int* mine = idx + size_t(have ? u : 0) * K3_DAG_K;
+    int c = 0;
+    const int iend = min(b + 32, NL) - 1;
+    for (int i = 0; i < iend; ++i) {
+      const int2 o = se[i];
+      if (have && i < u && o.x <= me.y && me.x <= o.y) add(c, mine, i);
+    }
+    if (have) cnt[u] = c;
+    over |= c > K3_DAG_K;
+  }
+  // short targets in start order: every long item, then the start window
+  for (int b = w * 32; b < NS; b += NT) {
+    const int j = b + lane;
+    const bool have = j < NS;
+    const int u = have ? (int)(key[j] & 0xffffffffLL) : 0;
+    const int2 me = have ? se[u] : make_int2(0, 0);
+    int* mine = idx + size_t(u) * K3_DAG_K;
+    int c = 0;
+    for (int i = 0; i < NL; ++i) {
+      const int2 o = se[i];
+      if (have && o.x <= me.y && me.x <= o.y) add(c, mine, i);
+    }
+    const long long lo_s = (long long)__shfl_sync(0xffffffffu, me.x, 0) - K3_DAG_SHORT;  // lane 0: the block's first start
+    int hi_e = have ? me.y : INT_MIN;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) hi_e = max(hi_e, __shfl_xor_sync(0xffffffffu, hi_e, d));
+    // window [first key with start >= lo_s, first key with start > hi_e)
+    int lo = 0, hi = NS;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if ((key[mid] >> 32) < lo_s) lo = mid + 1;
+      else hi = mid;
+    }
+    int w0 = lo;
+    hi = NS;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if ((key[mid] >> 32) <= hi_e) lo = mid + 1;
+      else hi = mid;
+    }
+    for (int q = w0; q < lo; ++q) {
+      const int i = (int)(key[q] & 0xffffffffLL);
+      const int2 o = se[i];
+      if (have && i < u && o.x <= me.y && me.x <= o.y) add(c, mine, i);
+    }
+    if (have) cnt[u] = c;
+    over |= c > K3_DAG_K;
+  }
+  if (__syncthreads_or(over)) return false;
+  // rounds: every item whose obstacles were all placed in earlier rounds
+  long long cmax = LLONG_MIN;
+  for (int r = 0;; ++r) {
+    int left = 0;
+    for (int u = tid; u < M; u += NT) {
+      if (lvl[u] >= 0) continue;
+      const int* ob = idx + size_t(u) * K3_DAG_K;
+      const int k = cnt[u];
+      bool ready = true;
+      for (int q = 0; q < k && ready; ++q) {
+        const int l = lvl[ob[q]];  // -1, or r for an item placed this round: not yet
+        ready = l >= 0 && l < r;
+      }
+      if (!ready) {
+        left = 1;
+        continue;
+      }
+      const int qi = ord[A + u];
+      const long long s = sz[qi], fl = flo[qi];
+      long long best = LLONG_MAX;
+      for (int c = -1; c < k; ++c) {
+        const long long x = c < 0 ? fl : HI[ob[c]];
+        if (x < fl || x >= best) continue;
+        bool ok = true;
+        for (int q = 0; q < k && ok; ++q) {
+          const int o = ob[q];
+          ok = !(LO[o] < x + s && HI[o] > x);
+        }
+        if (ok) best = x;
+      }
+      LO[u] = best;
+      HI[u] = best + s;
+      off[qi] = best;
+      lvl[u] = r;
+      cmax = max(cmax, best + s);
+    }
+    if (!__syncthreads_or(left)) break;
+  }
+  *cap_rest = blk.reduce_max(cmax);
+  return true;
+}
+
 template <int NT, int MAXC, int MS = 0>
 __global__ void __launch_bounds__(NT) k3_llfb(const K3Args a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -327,9 +521,14 @@ __global__ void __launch_bounds__(NT) k3_llfb(const K3Args a) {
   for (int k = tid; k < P; k += NT) sidx[k] = ord[k];
   __syncthreads();
 
-  // ---- sequential placement, parallel _lowest_fit
+  // ---- placement: by DAG rounds where the problem qualifies, else
+  // sequential with a parallel _lowest_fit over the placed list
   long long cap_rest = LLONG_MIN;
-  if constexpr (NT * MAXC <= 8192) {
+  bool placed = false;
+  if (a.dscratch_off[p] >= 0)
+    placed = k3_dag_place<NT>(blk, N, A, ord, st, en, sz, flo, off, a.dscratch + a.dscratch_off[p], &cap_rest);
+  if (placed) {
+  } else if constexpr (NT * MAXC <= 8192) {
     // Placed list in registers: thread t owns list slots [t*TOT, (t+1)*TOT)
     // as {lo, hi, start, end}; empty slots never overlap and sort last.  An
     // insertion shifts the suffix with lo > res one slot right: within a
@@ -622,9 +821,18 @@ static int launch_k3_t(const K3Args& a, int grid, size_t smem, cudaStream_t s) {
   return RM_OK;
 }
 
+static thread_local int t_pack_form = 0;  // 0 auto, 1 placed list only, 2 DAG wherever it qualifies
+constexpr int K3_DAG_MIN_ITEMS = 1024;     // auto: DAG rounds for problems from this size
+
 }  // namespace roam
 
 using namespace roam;
+
+extern "C" int rm_set_pack_form(int form) {
+  if (form < 0 || form > 2) return fail(RM_ERR_INVALID_ARG, "pack form must be 0 (auto), 1 (list) or 2 (DAG)");
+  t_pack_form = form;
+  return RM_OK;
+}
 
 extern "C" int rm_llfb_batch(int32_t P, const int64_t* item_ptr, const int32_t* tensor,
                              const int32_t* start, const int32_t* end, const int64_t* size,
@@ -681,8 +889,18 @@ extern "C" int rm_llfb_batch(int32_t P, const int64_t* item_ptr, const int32_t* 
       gbytes += b;
     }
   }
+  // DAG placement scratch (obstacle lists) for the problems that try it
+  std::vector<int64_t> doff(P, -1);
+  size_t dbytes = 0;
+  for (int p = 0; p < P; ++p) {
+    const int n = (int)(item_ptr[p + 1] - item_ptr[p]);
+    if (n == 0 || t_pack_form == 1 || (t_pack_form == 0 && n < K3_DAG_MIN_ITEMS)) continue;
+    doff[p] = (int64_t)dbytes;
+    dbytes += K3DagLayout(n).bytes;
+  }
   Scratch sc(s);
-  int64_t *d_ptr, *d_sz, *d_off, *d_cap, *d_goff, *d_ccap = nullptr;
+  int64_t *d_ptr, *d_sz, *d_off, *d_cap, *d_goff, *d_doff, *d_ccap = nullptr;
+  unsigned char* d_ds = nullptr;
   int32_t *d_t, *d_s, *d_e, *d_comp = nullptr;
   uint8_t *d_act, *d_met = nullptr;
   unsigned char* d_g = nullptr;
@@ -702,6 +920,9 @@ extern "C" int rm_llfb_batch(int32_t P, const int64_t* item_ptr, const int32_t* 
     RM_CUDA(sc.alloc(&d_ccap, ni));
   }
   if (gbytes) RM_CUDA(sc.alloc(&d_g, gbytes));
+  RM_CUDA(sc.alloc(&d_doff, size_t(P)));
+  if (dbytes) RM_CUDA(sc.alloc(&d_ds, dbytes));
+  RM_CUDA(cudaMemcpyAsync(d_doff, doff.data(), size_t(P) * 8, cudaMemcpyHostToDevice, s));
   RM_CUDA(cudaMemcpyAsync(d_ptr, item_ptr, (size_t(P) + 1) * 8, cudaMemcpyHostToDevice, s));
   RM_CUDA(cudaMemcpyAsync(d_goff, goff.data(), size_t(P) * 8, cudaMemcpyHostToDevice, s));
   if (NI > 0) {
@@ -712,7 +933,7 @@ extern "C" int rm_llfb_batch(int32_t P, const int64_t* item_ptr, const int32_t* 
     RM_CUDA(cudaMemcpyAsync(d_act, is_act, size_t(NI), cudaMemcpyHostToDevice, s));
   }
   K3Args a{P, d_ptr, d_t, d_s, d_e, d_sz, d_act, mode, d_off, d_cap, d_met, d_comp, d_ccap, d_g,
-           d_goff};
+           d_goff, d_ds, d_doff};
   int rc;
   // the register-resident placed list holds NT * MAXC - 1 placed items; fewer
   // slots per thread shorten the per-item chain between the block barriers

@@ -163,6 +163,13 @@ class PackResult:
     comp_cap: dict[int, int] = field(default_factory=dict)  # component root -> incumbent cap
 
 
+def set_pack_form(form: int) -> None:
+    """K3 placement form on this thread: 0 auto (DAG rounds for problems of
+    1,024+ items), 1 the placed-list path only, 2 DAG rounds wherever they
+    qualify (rm_set_pack_form).  Same offsets either way."""
+    check(lib().rm_set_pack_form(int(form)), "rm_set_pack_form")
+
+
 def pack_batch(problems: Sequence[Sequence], mode: int) -> list[PackResult]:
     """Run K3 over many independent item lists in ONE launch (one CTA per
     problem): the batch form of the planner's ``_pool_map(_solve_layout)``

@@ -138,3 +138,87 @@ def test_components_vs_oracle():
         offs, cap, met, comps = O.component_incumbents(rows)
         assert r.offsets == offs and r.capacity == cap and r.bound_met == met
         assert r.comp_cap == {root: c[1] for root, c in comps.items()}
+
+
+# ---- K3 DAG placement (items placed in rounds over the time-overlap relation)
+
+@pytest.fixture
+def pack_form():
+    from paper_2310_19295_b200.layout import set_pack_form
+    yield set_pack_form
+    set_pack_form(0)
+
+
+def _planner_like_rows(rng, n, horizon, act_p, long_p=0.005):
+    """Mostly one-to-few-step temporaries plus a few long-lived tensors, sizes
+    with duplicates and zeros (ties in lo / hi), like the planner's leaves."""
+    rows = []
+    for t in rng.sample(range(4 * n), n):
+        s = rng.randint(0, horizon - 1)
+        ln = rng.randint(0, horizon // 8) if rng.random() < long_p else rng.choice([0, 0, 1, 1, 2, 3, 5])
+        e = min(horizon - 1, s + ln)
+        rows.append((t, rng.choice([0, 1, 3, 8, 64, 100]) * rng.choice([1, MB]), s, e, rng.random() < act_p))
+    return rows
+
+
+@pytest.mark.parametrize("form", [1, 2])
+def test_forms_on_golden_corpora(pack_form, form):
+    """The placed-list path (1) and the DAG rounds (2, every problem) give the
+    reference's golden layouts."""
+    pack_form(form)
+    cases = golden("layouts")["llfb"]
+    plain = pack_batch([_items(c["items"]) for c in cases], PLAIN)
+    cons = pack_batch([_items(c["items"]) for c in cases], CONSTRAINED)
+    for c, a, b in zip(cases, plain, cons):
+        assert a.offsets == _offs(c["llfb"]["offsets"]) and a.capacity == c["llfb"]["capacity"]
+        assert b.offsets == _offs(c["constrained"]["offsets"]) and b.capacity == c["constrained"]["capacity"]
+    spec = golden("layouts")["spec"][0]
+    m = pack_batch([_items(spec["items"])], PLAIN)[0]
+    assert m.offsets == _offs(spec["offsets"]) and m.capacity == 12
+
+
+@pytest.mark.parametrize("form", [0, 1, 2])
+@pytest.mark.parametrize("n,horizon", [(1, 3), (40, 20), (700, 300), (1023, 900), (1024, 900), (3000, 2500),
+                                       (9035, 8000), (10240, 9000)])
+def test_dag_rounds_vs_oracle(pack_form, form, n, horizon):
+    """Planner-like problems (shallow time-overlap relation: the DAG rounds
+    qualify) in every form, PLAIN and CONSTRAINED, with a small problem
+    riding in the same launch."""
+    pack_form(form)
+    key = (n, horizon)
+    if key not in _ORACLE:  # the same problems in every form: the oracle runs once
+        rng = random.Random(17 * n + horizon)
+        rows = _planner_like_rows(rng, n, horizon, 0.1)
+        small = _planner_like_rows(rng, 30, 12, 0.2)
+        _ORACLE[key] = (rows, small, O.constrained_llfb_layout(rows), O.constrained_llfb_layout(small),
+                        O.llfb_layout(rows))
+    rows, small, want_b, want_c, want_a = _ORACLE[key]
+    b, c = pack_batch([_items(rows), _items(small)], CONSTRAINED)
+    assert (b.offsets, b.capacity) == want_b
+    assert (c.offsets, c.capacity) == want_c
+    a = pack_batch([_items(rows)], PLAIN)[0]
+    assert (a.offsets, a.capacity) == want_a
+
+
+_ORACLE: dict = {}
+
+
+def test_dag_rounds_fall_back_on_dense_problems(pack_form):
+    """Heavily overlapping items (more obstacles per item than the lists
+    hold) keep the placed-list path: same answers."""
+    pack_form(2)
+    rng = random.Random(5)
+    rows = _rand_rows(rng, 2000, 600, 0.2)
+    b = pack_batch([_items(rows)], CONSTRAINED)[0]
+    assert (b.offsets, b.capacity) == O.constrained_llfb_layout(rows)
+
+
+def test_dag_rounds_components(pack_form):
+    pack_form(2)
+    rng = random.Random(4)
+    probs = [_planner_like_rows(rng, rng.randint(1, 40), rng.randint(3, 30), 0.3) for _ in range(200)]
+    res = pack_batch([_items(r) for r in probs], COMPONENTS)
+    for rows, r in zip(probs, res):
+        offs, cap, met, comps = O.component_incumbents(rows)
+        assert r.offsets == offs and r.capacity == cap and r.bound_met == met
+        assert r.comp_cap == {root: c[1] for root, c in comps.items()}

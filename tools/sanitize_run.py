@@ -70,6 +70,15 @@ def main(which: str = "all") -> None:
         items = [lay.LayoutItem(t, 1 + (7 * t) % 5, t % 9, t % 9 + 3, t % 4 == 0) for t in range(300)]
         for mode in (lay.PLAIN, lay.CONSTRAINED):
             lay.pack_batch([items, items[:40]], mode)
+        # K3's DAG rounds (every problem) and their fallback on a dense one
+        lay.set_pack_form(2)
+        try:
+            for mode in (lay.PLAIN, lay.CONSTRAINED, lay.COMPONENTS):
+                lay.pack_batch([items, items[:40]], mode)
+            dense = [lay.LayoutItem(t, 1 + t % 3, 0, 5, False) for t in range(80)]
+            lay.pack_batch([dense], lay.PLAIN)
+        finally:
+            lay.set_pack_form(0)
         offs = {i.tensor: (13 * i.tensor) % 50 for i in items}
         lay.layout_violations(items, offs, 40)
         # repair_conflicts: device pair test + mover election over several rounds
