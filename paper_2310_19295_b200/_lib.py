@@ -50,8 +50,13 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     common = [nvcc, "-std=c++17", "-O3", ARCH, "-lineinfo", "-Xcompiler", "-fPIC,-O3,-mpopcnt",
               "-I", str(ROOT / "include")]
 
+    hdr_t = max(p.stat().st_mtime for p in deps[len(srcs):])
+
     def compile_one(src: Path) -> Path:
         obj = objdir / (src.name + ".o")
+        # an object newer than its source and every header is reused
+        if not force and obj.exists() and obj.stat().st_mtime >= max(src.stat().st_mtime, hdr_t):
+            return obj
         cmd = common + ["-c", str(src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

@@ -21,14 +21,25 @@
 // window.  Each op's score (out - bytes its inputs would free) is kept in
 // shared memory and updated incrementally -- a tracked tensor's count only
 // falls when an op runs, and when it reaches 1 the one op still holding an
-// entry (found in the tensor's local consumer list) now frees it -- and the
-// ready ops sit in a compact list, so a step compares only the ready ops'
-// scores (a warp (score, index) argmin), then applies the pick (counts, score
-// updates, frees, successor pred counts, newly ready ops appended): no block
-// barrier per step.  Mutable state lives in shared memory when it fits, else
-// in a per-window global scratch.
+// entry now frees it -- and the ready ops sit in a compact list, so a step
+// compares only the ready ops' scores (a warp (score, index) argmin), then
+// applies the pick (counts, score updates, successor pred counts, newly ready
+// ops appended): no block barrier per step.  Two identities keep the step's
+// dependent chain short:
+//   * the bytes the pick frees are out - score: its score counts exactly the
+//     distinct tracked inputs whose count is 1, the ones that reach 0 now --
+//     no warp reduction of freed bytes;
+//   * each tracked tensor carries, beside its count, the XOR of (local index
+//     + 1) over its unrun consumer ENTRIES (an op removes its index once per
+//     odd multiplicity).  When the count reaches 1 with an unrun entry left,
+//     that entry is the only one, so the XOR names the op that now frees the
+//     tensor (0: none left) -- no walk of the tensor's consumer list.
+// Mutable state lives in shared memory when it fits, else in a per-window
+// global scratch.
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
+#include <unordered_set>
 
 #include "roam_internal.h"
 
@@ -42,14 +53,12 @@ struct K4Args {
   const int32_t* gop;       // [NO] global op id per local op
   const int64_t* out;       // [NO] out_bytes
   const int32_t* npred0;    // [NO] distinct local preds
-  const int64_t* in_ptr;    // [NO+1] into in_idx (window-local tensor index)
-  const int32_t* in_idx;
+  const int64_t* in_ptr;    // [NO+1] into in_idx
+  const uint32_t* in_idx;   // window-local tensor index | odd-multiplicity bit << 31
   const int64_t* in_sz;     // size of each in_idx entry's tensor (loaded in parallel with it)
   const int64_t* succ_ptr;  // [NO+1] into succ_idx (window-local op index)
   const int32_t* succ_idx;
-  const int32_t* count0;    // [NT_] tracked consumer-entry counts
-  const int64_t* tc_ptr;    // [NT_+1] local consumer ops of each tracked tensor
-  const int32_t* tc_idx;
+  const uint32_t* cw0;      // [NT_] tracked tensors: consumer-entry count | XOR(local op + 1) << 16
   const int64_t* tsize;     // [NT_]
   const int64_t* start_live;  // [W]
   int32_t* order;           // [NO] global op ids in schedule order
@@ -57,26 +66,31 @@ struct K4Args {
   int32_t* status;          // [W]
   unsigned char* gscratch;
   const int64_t* gscratch_off;  // [W] (-1: shared memory)
+  int shift;                // the 32-bit score form keeps scores in units of 2^shift bytes
 };
 
-// Working set of one window (all 16-byte aligned): delta int64[n], npred
-// int16[n] (-1 once the op ran), in / succ CSR starts u32[n + 1] each, ready
-// int32[n], counts u16[nt].  Compact so that an 8.6k-op window (GPT2-XL's)
+// Working set of one window (all 16-byte aligned): delta int64[n] (or int32
+// in units of 2^shift bytes when every op's scores fit: half the bytes, so a
+// GPT2-XL window leaves the L1 twice the room), npred
+// int16[n], in / succ CSR starts u32[n + 1] each, ready u16[n], tensor words
+// u32[nt] (count | XOR << 16).  Compact so that an 8.6k-op window (GPT2-XL's)
 // still fits one CTA's shared memory with its CSR starts staged.
 struct K4Layout {
-  size_t o_delta, o_npred, o_inp, o_sup, o_ready, o_cnt, bytes;
-  __host__ __device__ K4Layout(int64_t n, int64_t nt) {
+  size_t o_delta, o_npred, o_inp, o_sup, o_ready, o_cw, bytes;
+  __host__ __device__ K4Layout(int64_t n, int64_t nt, int dbytes) {
     auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
     o_delta = 0;
-    o_npred = al(o_delta + 8 * size_t(n));
+    o_npred = al(o_delta + size_t(dbytes) * size_t(n));
     o_inp = al(o_npred + 2 * size_t(n));
     o_sup = al(o_inp + 4 * (size_t(n) + 1));
     o_ready = al(o_sup + 4 * (size_t(n) + 1));
-    o_cnt = al(o_ready + 4 * size_t(n));
-    bytes = al(o_cnt + 2 * size_t(nt));
+    o_cw = al(o_ready + 2 * size_t(n));
+    bytes = al(o_cw + 4 * size_t(nt));
   }
 };
-__host__ __device__ inline size_t k4_bytes(int64_t n_ops, int64_t n_ten) { return K4Layout(n_ops, n_ten).bytes; }
+__host__ __device__ inline size_t k4_bytes(int64_t n_ops, int64_t n_ten, int dbytes) {
+  return K4Layout(n_ops, n_ten, dbytes).bytes;
+}
 
 // One warp per window.  The ready ops (all predecessors scheduled) sit in a
 // compact list -- a training window's ready set is tens of ops, so a step
@@ -84,26 +98,34 @@ __host__ __device__ inline size_t k4_bytes(int64_t n_ops, int64_t n_ten) { retur
 // runs inside the warp: no block barrier anywhere on the step's critical path.
 // The pick is a REDUX argmin of the packed key (score << 16 | local index:
 // |score| < 2^47, local indices < 2^16), and the ops' CSR starts are staged in
-// the working set, so a step's first dependent loads are shared-memory ones.
+// the working set, so a step's first dependent loads are shared-memory ones;
+// the pick's input, size and successor entries are then loaded together.
+template <bool SH, typename DT>
 __global__ void __launch_bounds__(32) k4_greedy(const K4Args a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int w = blockIdx.x, lane = threadIdx.x;
+  // SH: the working set is this CTA's shared memory (a pointer the compiler
+  // knows is shared: LDS / STS, not generic loads); else global scratch.  A
+  // launch of each form skips the other form's windows.
+  if (SH != (a.gscratch_off[w] < 0)) return;
   const int64_t ob = a.op_base[w], tb = a.ten_base[w];
   const int n = a.nops[w];
   const int nt = (int)(a.ten_base[w + 1] - tb);
-  const K4Layout L(n, nt);
-  unsigned char* ws = a.gscratch_off[w] < 0 ? smem : a.gscratch + a.gscratch_off[w];
-  long long* delta = reinterpret_cast<long long*>(ws + L.o_delta);  // out - bytes freed if run now
+  const K4Layout L(n, nt, (int)sizeof(DT));
+  constexpr bool D32 = sizeof(DT) == 4;
+  const int sh = D32 ? a.shift : 0;
+  unsigned char* ws = SH ? smem : a.gscratch + a.gscratch_off[w];
+  DT* delta = reinterpret_cast<DT*>(ws + L.o_delta);  // out - bytes freed if run now (>> sh)
   short* npred = reinterpret_cast<short*>(ws + L.o_npred);
   uint32_t* inp = reinterpret_cast<uint32_t*>(ws + L.o_inp);
   uint32_t* sup = reinterpret_cast<uint32_t*>(ws + L.o_sup);
-  int* ready = reinterpret_cast<int*>(ws + L.o_ready);
-  unsigned short* cnt = reinterpret_cast<unsigned short*>(ws + L.o_cnt);
-  const int64_t* tc_ptr = a.tc_ptr + tb;
+  unsigned short* ready = reinterpret_cast<unsigned short*>(ws + L.o_ready);
+  uint32_t* cw = reinterpret_cast<uint32_t*>(ws + L.o_cw);
   const int64_t* out = a.out + ob;
   const int64_t* in_ptr = a.in_ptr + ob;
   const int64_t* succ_ptr = a.succ_ptr + ob;
   const int64_t* tsize = a.tsize + tb;
+  const uint32_t* cw0 = a.cw0 + tb;
   const unsigned lt = (1u << lane) - 1u;
   int R = 0;
   for (int i0 = 0; i0 <= n; i0 += 32) {
@@ -123,22 +145,30 @@ __global__ void __launch_bounds__(32) k4_greedy(const K4Args a) {
       // input frees when its count is 1, and counts only fall when an op runs
       long long freed = 0;
       for (int64_t k = in_ptr[i]; k < in_ptr[i + 1]; ++k) {
-        const int t = __ldg(a.in_idx + k);
-        if (a.count0[tb + t] == 1) freed += tsize[t];
+        const uint32_t t = __ldg(a.in_idx + k) & 0x7fffffffu;
+        if ((cw0[t] & 0xffffu) == 1u) freed += tsize[t];
       }
-      delta[i] = out[i] - freed;
+      delta[i] = (DT)((out[i] - freed) >> sh);
       rd = np == 0;
     }
     const unsigned m = __ballot_sync(0xffffffffu, rd);
-    if (rd) ready[R + __popc(m & lt)] = i;
+    if (rd) ready[R + __popc(m & lt)] = (unsigned short)i;
     R += __popc(m);
   }
-  for (int t = lane; t < nt; t += 32) cnt[t] = (unsigned short)a.count0[tb + t];
+  for (int t = lane; t < nt; t += 32) cw[t] = cw0[t];
   long long live = a.start_live[w], peak = live;
   __syncwarp();
 
+  // the schedule is written as local indices during the steps (no dependent
+  // global load on a step's path) and mapped to global op ids at the end
+  int32_t* ord = a.order + ob;
+  auto map_order = [&](int steps) {
+    __syncwarp();
+    for (int i = lane; i < steps; i += 32) ord[i] = a.gop[ob + ord[i]];
+  };
   for (int step = 0; step < n; ++step) {
     if (R == 0) {  // no ready op: the window's precedence has a cycle
+      map_order(step);
       if (lane == 0) a.status[w] = 2;
       return;
     }
@@ -146,14 +176,20 @@ __global__ void __launch_bounds__(32) k4_greedy(const K4Args a) {
     // strict < over ascending local index -- as one packed key, two REDUX
     long long bk = LLONG_MAX;
     int bs = -1;
-    for (int j = lane; j < R; j += 32) {
+    if (lane < R) {  // the common case: at most 32 ready ops
+      const int i = ready[lane];
+      bk = ((long long)delta[i] << 16) | (long long)i;
+      bs = lane;
+    }
+    for (int j = lane + 32; j < R; j += 32) {
       const int i = ready[j];
-      const long long key = (delta[i] << 16) | (long long)i;
+      const long long key = ((long long)delta[i] << 16) | (long long)i;
       if (key < bk) {
         bk = key;
         bs = j;
       }
     }
+    const int last = ready[R - 1];
     const int khi = (int)(bk >> 32);
     const unsigned klo = (unsigned)bk;
     const int mhi = __reduce_min_sync(0xffffffffu, khi);
@@ -161,61 +197,76 @@ __global__ void __launch_bounds__(32) k4_greedy(const K4Args a) {
     const unsigned win = __ballot_sync(0xffffffffu, khi == mhi && klo == mlo);
     bs = __shfl_sync(0xffffffffu, bs, __ffs(win) - 1);
     const int bi = (int)(mlo & 0xffffu);
-    // ---- apply the pick: inputs' counts (a count reaching 1 moves the free
-    // to the one consumer entry left), successors' predecessor counts
-    long long freed = 0;
+    // the pick's score: out minus exactly the bytes it frees now
+    const long long dsel = ((long long)(((unsigned long long)(unsigned)mhi << 32) | mlo) >> 16) << sh;
+    // ---- the pick's CSR ranges, then its first 32 input / size / successor
+    // entries in one batch of independent loads
     const uint32_t i0 = inp[bi], i1 = inp[bi + 1];
-    for (uint32_t k = i0 + lane; k < i1; k += 32) {
-      const int t = __ldg(a.in_idx + k);
-      const long long tsz = __ldg(a.in_sz + k);
-      const int c = (int)--cnt[t];  // distinct inputs: no races
-      if (c == 0) freed += tsz;
-      if (c == 1) {
-        for (int64_t q = tc_ptr[t]; q < tc_ptr[t + 1]; ++q) {
-          const int j = __ldg(a.tc_idx + q);
-          if (j != bi && npred[j] >= 0) {
-            atomicAdd(reinterpret_cast<unsigned long long*>(delta + j), (unsigned long long)(-tsz));
-            break;
-          }
+    const uint32_t s0 = sup[bi], s1 = sup[bi + 1];
+    const long long ob_bi = out[bi];
+    const bool hin = i0 + lane < i1, hsu = s0 + lane < s1;
+    uint32_t e = hin ? __ldg(a.in_idx + i0 + lane) : 0u;
+    long long tsz = hin ? __ldg(a.in_sz + i0 + lane) : 0;
+    int sv = hsu ? __ldg(a.succ_idx + s0 + lane) : 0;
+    // the hole the pick leaves is filled by the list's last entry (unordered
+    // list); appends below start at the old last slot, so skip a self-move
+    if (lane == 0 && bs != R - 1) ready[bs] = (unsigned short)last;
+    --R;
+    // ---- inputs: count -= 1, XOR out the pick (odd multiplicity); a count
+    // reaching 1 with an unrun entry left moves the free to that op
+    const unsigned xb = (unsigned)(bi + 1) << 16;
+    for (uint32_t k = i0 + lane;;) {
+      if (k < i1) {
+        const uint32_t t = e & 0x7fffffffu;
+        const uint32_t wv = cw[t];
+        const uint32_t c = (wv - 1u) & 0xffffu;  // distinct inputs: no races
+        const uint32_t x = (wv ^ ((e >> 31) ? xb : 0u)) & 0xffff0000u;
+        cw[t] = x | c;
+        if (c == 1u && x != 0u)
+        {
+          if constexpr (D32)
+            atomicAdd(reinterpret_cast<int*>(delta) + ((x >> 16) - 1u), -(int)(tsz >> sh));
+          else
+            atomicAdd(reinterpret_cast<unsigned long long*>(delta) + ((x >> 16) - 1u), (unsigned long long)(-tsz));
         }
       }
+      k += 32;
+      if (k - lane >= i1) break;
+      if (k < i1) {
+        e = __ldg(a.in_idx + k);
+        tsz = __ldg(a.in_sz + k);
+      }
     }
-    __syncwarp();
-    if (lane == 0) {
-      npred[bi] = -1;            // ran
-      ready[bs] = ready[R - 1];  // the list is unordered: the last entry fills the hole
-    }
-    --R;
-    __syncwarp();
-    const uint32_t s0 = sup[bi], s1 = sup[bi + 1];
+    // ---- successors: predecessor counts, newly ready ops appended
     for (uint32_t k = s0; k < s1; k += 32) {
       bool rd = false;
-      int sv = 0;
       if (k + lane < s1) {
-        sv = __ldg(a.succ_idx + k + lane);
+        if (k != s0) sv = __ldg(a.succ_idx + k + lane);
         rd = --npred[sv] == 0;  // distinct successors
       }
       const unsigned m = __ballot_sync(0xffffffffu, rd);
-      if (rd) ready[R + __popc(m & lt)] = sv;
+      if (rd) ready[R + __popc(m & lt)] = (unsigned short)sv;
       R += __popc(m);
     }
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) freed += __shfl_xor_sync(0xffffffffu, freed, d);
-    live += out[bi];
+    live += ob_bi;
     peak = max(peak, live);
-    live -= freed;
-    if (lane == 0) a.order[ob + step] = a.gop[ob + bi];
+    live += dsel - ob_bi;
+    if (lane == 0) ord[step] = bi;
     __syncwarp();
   }
+  map_order(n);
   if (lane == 0) {
     a.peak[w] = peak;
     a.status[w] = 0;
   }
 }
 
-static int launch_k4(const K4Args& a, size_t smem, cudaStream_t s) {
-  RM_CUDA(smem_optin(k4_greedy));
-  k4_greedy<<<a.W, 32, smem, s>>>(a);
+template <typename DT>
+static int launch_k4_t(const K4Args& a, size_t smem, bool any_global, cudaStream_t s) {
+  RM_CUDA(smem_optin(k4_greedy<true, DT>));
+  k4_greedy<true, DT><<<a.W, 32, smem, s>>>(a);
+  RM_LAUNCH_CHECK("k4_greedy launch");
+  if (any_global) k4_greedy<false, DT><<<a.W, 32, 0, s>>>(a);
   RM_LAUNCH_CHECK("k4_greedy launch");
   return RM_OK;
 }
@@ -247,9 +298,12 @@ extern "C" int rm_greedy_windows(RmGraph* g, int32_t W, const int64_t* win_ptr,
   std::vector<int32_t> loc(n, -1), tloc(T, -1);
   std::vector<uint8_t> is_lin(T, 0), is_lout(T, 0);
   std::vector<int64_t> op_base(W + 1, 0), ten_base(W + 1, 0), start_live(W, 0);
-  std::vector<int32_t> gop, npred0, in_idx, succ_idx, count0, tc_idx;
+  std::vector<int32_t> gop, npred0, succ_idx, count0;
+  std::vector<uint32_t> in_idx, cw0;
+  // (tracked tensor, local op) pairs with an odd number of consumer entries
+  std::unordered_set<uint64_t> odd;
   std::vector<int64_t> in_sz;
-  std::vector<int64_t> out_b, in_ptr(1, 0), succ_ptr(1, 0), tsize, tc_ptr(1, 0);
+  std::vector<int64_t> out_b, in_ptr(1, 0), succ_ptr(1, 0), tsize;
   std::vector<int32_t> ops, rel, tmp;
   std::vector<std::vector<int32_t>> succ;
   std::vector<uint8_t> held;
@@ -300,12 +354,20 @@ extern "C" int rm_greedy_windows(RmGraph* g, int32_t W, const int64_t* win_ptr,
       }
       if (is_lin[t]) sl += g->size[t];
       if (!held[r]) {  // held tensors never free: the device never needs them
-        tloc[t] = nt++;
+        tloc[t] = nt;
         tsize.push_back(g->size[t]);
         count0.push_back(local);
-        for (int k = g->cons_ptr[t]; k < g->cons_ptr[t + 1]; ++k)
-          if (loc[g->cons_idx[k]] >= 0) tc_idx.push_back(loc[g->cons_idx[k]]);
-        tc_ptr.push_back((int64_t)tc_idx.size());
+        // XOR of (local op + 1) over the tensor's local consumer entries
+        uint32_t x = 0;
+        for (int k = g->cons_ptr[t]; k < g->cons_ptr[t + 1]; ++k) {
+          const int j = loc[g->cons_idx[k]];
+          if (j < 0) continue;
+          x ^= uint32_t(j + 1);
+          const uint64_t key = (uint64_t(uint32_t(nt)) << 32) | uint32_t(j);
+          if (!odd.erase(key)) odd.insert(key);
+        }
+        cw0.push_back(uint32_t(std::min(local, 65535)) | (x << 16));
+        ++nt;
       }
     }
     start_live[w] = sl;
@@ -322,8 +384,11 @@ extern "C" int rm_greedy_windows(RmGraph* g, int32_t W, const int64_t* win_ptr,
         if (tloc[g->in_idx[k]] >= 0) tmp.push_back(tloc[g->in_idx[k]]);
       std::sort(tmp.begin(), tmp.end());
       tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
-      in_idx.insert(in_idx.end(), tmp.begin(), tmp.end());
-      for (const int32_t t : tmp) in_sz.push_back(tsize[size_t(tb + t)]);
+      for (const int32_t t : tmp) {
+        const bool o = odd.count((uint64_t(uint32_t(t)) << 32) | uint32_t(i)) != 0;
+        in_idx.push_back(uint32_t(t) | (o ? 0x80000000u : 0u));
+        in_sz.push_back(tsize[size_t(tb + t)]);
+      }
       in_ptr.push_back((int64_t)in_idx.size());
       tmp.clear();
       for (int k = g->in_ptr[v]; k < g->in_ptr[v + 1]; ++k) {
@@ -346,6 +411,7 @@ extern "C" int rm_greedy_windows(RmGraph* g, int32_t W, const int64_t* win_ptr,
     for (int t : rel) tloc[t] = -1;
     for (int64_t k = lin_ptr[w]; k < lin_ptr[w + 1]; ++k) is_lin[lin_idx[k]] = 0;
     for (int64_t k = lout_ptr[w]; k < lout_ptr[w + 1]; ++k) is_lout[lout_idx[k]] = 0;
+    odd.clear();
   }
   // device layout: window w owns nops+1 op slots from opb_dev[w] (the extra
   // slot is the tail entry of its in/succ pointer arrays)
@@ -369,11 +435,31 @@ extern "C" int rm_greedy_windows(RmGraph* g, int32_t W, const int64_t* win_ptr,
   int dev = 0, max_smem = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  const size_t limit = size_t(max_smem) - 1024;
+  size_t limit = size_t(max_smem) - 1024;
+  // test hook: a lower shared-memory budget sends windows to the global-scratch form
+  if (const char* e = getenv("RM_K4_SMEM_LIMIT")) limit = std::min(limit, (size_t)strtoull(e, nullptr, 10));
+  // 32-bit scores in units of 2^shift (shift = the common power of two of
+  // every size the kernel adds) when every op's out bytes and summed tracked
+  // input bytes -- the bounds of its score -- stay below 2^30 units
+  int shift = 62;
+  auto tz = [&](int64_t v) {
+    if (v > 0) shift = std::min(shift, __builtin_ctzll((unsigned long long)v));
+  };
+  for (const int64_t v : out_b) tz(v);
+  for (const int64_t v : tsize) tz(v);
+  for (const int64_t v : start_live) tz(v);
+  if (shift == 62) shift = 0;
+  bool d32 = true;
+  for (size_t i = 0; i + 1 < in_ptr.size() && d32; ++i) {
+    int64_t sin = 0;
+    for (int64_t k = in_ptr[i]; k < in_ptr[i + 1]; ++k) sin += in_sz[size_t(k)];
+    if ((out_b[i] >> shift) >= (int64_t(1) << 30) || (sin >> shift) >= (int64_t(1) << 30)) d32 = false;
+  }
+  const int dbytes = d32 ? 4 : 8;
   std::vector<int64_t> goff(W, -1);
   size_t gbytes = 0, smem = 16;
   for (int w = 0; w < W; ++w) {
-    const size_t b = k4_bytes(op_base[w + 1] - op_base[w], ten_base[w + 1] - ten_base[w]);
+    const size_t b = k4_bytes(op_base[w + 1] - op_base[w], ten_base[w + 1] - ten_base[w], dbytes);
     if (b <= limit) {
       smem = std::max(smem, b);
     } else {
@@ -392,8 +478,9 @@ extern "C" int rm_greedy_windows(RmGraph* g, int32_t W, const int64_t* win_ptr,
       out_w[opb_dev[w] + i] = out_b[op_base[w] + i];
     }
   Scratch sc(s);
-  int64_t *d_ob, *d_tb, *d_out, *d_inp, *d_sup, *d_tsz, *d_sl, *d_peak, *d_goff, *d_tcp;
-  int32_t *d_gop, *d_np, *d_ini, *d_sui, *d_c0, *d_ord, *d_st, *d_tci;
+  int64_t *d_ob, *d_tb, *d_out, *d_inp, *d_sup, *d_tsz, *d_sl, *d_peak, *d_goff;
+  int32_t *d_gop, *d_np, *d_sui, *d_ord, *d_st;
+  uint32_t *d_ini, *d_cw0;
   unsigned char* d_g = nullptr;
   auto up = [&](auto** d, const auto& v) -> cudaError_t {
     cudaError_t e = sc.alloc(d, v.size());
@@ -405,7 +492,7 @@ extern "C" int rm_greedy_windows(RmGraph* g, int32_t W, const int64_t* win_ptr,
   for (int w = 0; w < W; ++w) nops[w] = (int32_t)(op_base[w + 1] - op_base[w]);
   // the device's compact working set (K4Layout) and packed argmin key
   for (int w = 0; w < W; ++w)
-    if (nops[w] >= 65536) return fail(RM_ERR_CAPACITY, "greedy window above 65,535 ops");
+    if (nops[w] >= 65535) return fail(RM_ERR_CAPACITY, "greedy window above 65,534 ops");
   for (const int32_t c : count0)
     if (c > 65535) return fail(RM_ERR_CAPACITY, "greedy window: a tensor with more than 65,535 local uses");
   for (const int32_t d : npred0)
@@ -424,9 +511,7 @@ extern "C" int rm_greedy_windows(RmGraph* g, int32_t W, const int64_t* win_ptr,
   RM_CUDA(up(&d_ini, in_idx));
   RM_CUDA(up(&d_sup, succ_ptr_w));
   RM_CUDA(up(&d_sui, succ_idx));
-  RM_CUDA(up(&d_c0, count0));
-  RM_CUDA(up(&d_tcp, tc_ptr));
-  RM_CUDA(up(&d_tci, tc_idx));
+  RM_CUDA(up(&d_cw0, cw0));
   RM_CUDA(up(&d_tsz, tsize));
   RM_CUDA(up(&d_sl, start_live));
   RM_CUDA(up(&d_goff, goff));
@@ -441,9 +526,9 @@ extern "C" int rm_greedy_windows(RmGraph* g, int32_t W, const int64_t* win_ptr,
   if (gbytes) RM_CUDA(sc.alloc(&d_g, gbytes));
   int64_t* d_insz;
   RM_CUDA(up(&d_insz, in_sz));
-  K4Args a{W, d_ob, d_nops, d_tb, d_gop, d_out, d_np, d_inp, d_ini, d_insz, d_sup, d_sui, d_c0, d_tcp, d_tci,
-           d_tsz, d_sl, d_ord, d_peak, d_st, d_g, d_goff};
-  int rc = launch_k4(a, smem, s);
+  K4Args a{W, d_ob, d_nops, d_tb, d_gop, d_out, d_np, d_inp, d_ini, d_insz, d_sup, d_sui, d_cw0,
+           d_tsz, d_sl, d_ord, d_peak, d_st, d_g, d_goff, d32 ? shift : 0};
+  int rc = d32 ? launch_k4_t<int>(a, smem, gbytes > 0, s) : launch_k4_t<long long>(a, smem, gbytes > 0, s);
   if (rc) return rc;
   std::vector<int32_t> ord_w(opb_dev[W]), st_dev(W);
   if (opb_dev[W])

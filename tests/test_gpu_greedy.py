@@ -82,3 +82,34 @@ def test_config_error_live_in_unconsumed():
         greedy_order(OrderingProblem(g, ops, frozenset({unused})))
     with pytest.raises(ConfigError):
         greedy_order(OrderingProblem(g, ops, ops_per_step=0))
+
+
+def test_scratch_forms_and_64bit_scores(monkeypatch):
+    """The working set in global scratch (windows above the shared-memory
+    budget, forced here by the RM_K4_SMEM_LIMIT test hook) next to windows in
+    shared memory, in one call; and the 64-bit score form (one tensor of
+    2^40 + 4 KiB bytes, above the 32-bit form's 2^30 units)."""
+    import copy
+
+    doc = gg.layered_dag_doc(layers=60, width=20)
+    big = copy.deepcopy(doc)
+    t = next(t for t in big["tensors"] if any(t["id"] in o["inputs"] for o in big["ops"]))
+    t["size_bytes"] = 2 ** 40 + 4096
+    for d in (doc, big):
+        g = load_graph(d)
+        n = len(g.ops)
+        whole = tuple(range(n))
+        sub = tuple(range(100, 180))
+        inside = set(sub)
+        lin = frozenset(t for v in sub for t in g.ops[v].inputs if g.tensors[t].producer not in inside)
+        lout = frozenset(t for v in sub for t in g.ops[v].outputs
+                         if any(c not in inside for c in g.tensors[t].consumers))
+        probs = [OrderingProblem(g, whole), OrderingProblem(g, sub, lin, lout)]
+        want = [O.greedy_order(g, whole), O.greedy_order(g, sub, lin, lout)]
+        for limit in (None, "20000", "0"):
+            if limit is None:
+                monkeypatch.delenv("RM_K4_SMEM_LIMIT", raising=False)
+            else:
+                monkeypatch.setenv("RM_K4_SMEM_LIMIT", limit)
+            got = [(s.order, s.peak) for s in greedy_orders(probs)]
+            assert got == want, (limit, d is big)
