@@ -56,6 +56,7 @@ struct K4Args {
   const int64_t* in_ptr;    // [NO+1] into in_idx
   const uint32_t* in_idx;   // window-local tensor index | odd-multiplicity bit << 31
   const int64_t* in_sz;     // size of each in_idx entry's tensor (loaded in parallel with it)
+  const uint2* in_pk;       // 32-bit score form: {in_idx entry, size >> shift} in one 8-byte load
   const int64_t* succ_ptr;  // [NO+1] into succ_idx (window-local op index)
   const int32_t* succ_idx;
   const uint32_t* cw0;      // [NT_] tracked tensors: consumer-entry count | XOR(local op + 1) << 16
@@ -145,7 +146,9 @@ __global__ void __launch_bounds__(32) k4_greedy(const K4Args a) {
       // input frees when its count is 1, and counts only fall when an op runs
       long long freed = 0;
       for (int64_t k = in_ptr[i]; k < in_ptr[i + 1]; ++k) {
-        const uint32_t t = __ldg(a.in_idx + k) & 0x7fffffffu;
+        uint32_t t;
+        if constexpr (D32) t = __ldg(a.in_pk + k).x & 0x7fffffffu;
+        else t = __ldg(a.in_idx + k) & 0x7fffffffu;
         if ((cw0[t] & 0xffffu) == 1u) freed += tsize[t];
       }
       delta[i] = (DT)((out[i] - freed) >> sh);
@@ -205,8 +208,20 @@ __global__ void __launch_bounds__(32) k4_greedy(const K4Args a) {
     const uint32_t s0 = sup[bi], s1 = sup[bi + 1];
     const long long ob_bi = out[bi];
     const bool hin = i0 + lane < i1, hsu = s0 + lane < s1;
-    uint32_t e = hin ? __ldg(a.in_idx + i0 + lane) : 0u;
-    long long tsz = hin ? __ldg(a.in_sz + i0 + lane) : 0;
+    // an input entry and its tensor's size (units of 2^sh in the 32-bit form)
+    auto ld_in = [&](uint32_t k, uint32_t& e, long long& tsz) {
+      if constexpr (D32) {
+        const uint2 v = __ldg(a.in_pk + k);
+        e = v.x;
+        tsz = v.y;
+      } else {
+        e = __ldg(a.in_idx + k);
+        tsz = __ldg(a.in_sz + k);
+      }
+    };
+    uint32_t e = 0u;
+    long long tsz = 0;
+    if (hin) ld_in(i0 + lane, e, tsz);
     int sv = hsu ? __ldg(a.succ_idx + s0 + lane) : 0;
     // the hole the pick leaves is filled by the list's last entry (unordered
     // list); appends below start at the old last slot, so skip a self-move
@@ -225,17 +240,14 @@ __global__ void __launch_bounds__(32) k4_greedy(const K4Args a) {
         if (c == 1u && x != 0u)
         {
           if constexpr (D32)
-            atomicAdd(reinterpret_cast<int*>(delta) + ((x >> 16) - 1u), -(int)(tsz >> sh));
+            atomicAdd(reinterpret_cast<int*>(delta) + ((x >> 16) - 1u), -(int)tsz);
           else
             atomicAdd(reinterpret_cast<unsigned long long*>(delta) + ((x >> 16) - 1u), (unsigned long long)(-tsz));
         }
       }
       k += 32;
       if (k - lane >= i1) break;
-      if (k < i1) {
-        e = __ldg(a.in_idx + k);
-        tsz = __ldg(a.in_sz + k);
-      }
+      if (k < i1) ld_in(k, e, tsz);
     }
     // ---- successors: predecessor counts, newly ready ops appended
     for (uint32_t k = s0; k < s1; k += 32) {
@@ -526,8 +538,17 @@ extern "C" int rm_greedy_windows(RmGraph* g, int32_t W, const int64_t* win_ptr,
   if (gbytes) RM_CUDA(sc.alloc(&d_g, gbytes));
   int64_t* d_insz;
   RM_CUDA(up(&d_insz, in_sz));
-  K4Args a{W, d_ob, d_nops, d_tb, d_gop, d_out, d_np, d_inp, d_ini, d_insz, d_sup, d_sui, d_cw0,
-           d_tsz, d_sl, d_ord, d_peak, d_st, d_g, d_goff, d32 ? shift : 0};
+  uint32_t* d_inpk = nullptr;
+  if (d32) {
+    std::vector<uint32_t> pk(2 * in_idx.size());
+    for (size_t k = 0; k < in_idx.size(); ++k) {
+      pk[2 * k] = in_idx[k];
+      pk[2 * k + 1] = uint32_t(in_sz[k] >> shift);
+    }
+    RM_CUDA(up(&d_inpk, pk));
+  }
+  K4Args a{W, d_ob, d_nops, d_tb, d_gop, d_out, d_np, d_inp, d_ini, d_insz, reinterpret_cast<const uint2*>(d_inpk),
+           d_sup, d_sui, d_cw0, d_tsz, d_sl, d_ord, d_peak, d_st, d_g, d_goff, d32 ? shift : 0};
   int rc = d32 ? launch_k4_t<int>(a, smem, gbytes > 0, s) : launch_k4_t<long long>(a, smem, gbytes > 0, s);
   if (rc) return rc;
   std::vector<int32_t> ord_w(opb_dev[W]), st_dev(W);
