@@ -39,7 +39,6 @@
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
-#include <unordered_set>
 
 #include "roam_internal.h"
 
@@ -312,8 +311,7 @@ extern "C" int rm_greedy_windows(RmGraph* g, int32_t W, const int64_t* win_ptr,
   std::vector<int64_t> op_base(W + 1, 0), ten_base(W + 1, 0), start_live(W, 0);
   std::vector<int32_t> gop, npred0, succ_idx, count0;
   std::vector<uint32_t> in_idx, cw0;
-  // (tracked tensor, local op) pairs with an odd number of consumer entries
-  std::unordered_set<uint64_t> odd;
+  std::vector<uint8_t> par;  // per local op: odd number of entries in the tensor at hand
   std::vector<int64_t> in_sz;
   std::vector<int64_t> out_b, in_ptr(1, 0), succ_ptr(1, 0), tsize;
   std::vector<int32_t> ops, rel, tmp;
@@ -375,8 +373,6 @@ extern "C" int rm_greedy_windows(RmGraph* g, int32_t W, const int64_t* win_ptr,
           const int j = loc[g->cons_idx[k]];
           if (j < 0) continue;
           x ^= uint32_t(j + 1);
-          const uint64_t key = (uint64_t(uint32_t(nt)) << 32) | uint32_t(j);
-          if (!odd.erase(key)) odd.insert(key);
         }
         cw0.push_back(uint32_t(std::min(local, 65535)) | (x << 16));
         ++nt;
@@ -397,8 +393,7 @@ extern "C" int rm_greedy_windows(RmGraph* g, int32_t W, const int64_t* win_ptr,
       std::sort(tmp.begin(), tmp.end());
       tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
       for (const int32_t t : tmp) {
-        const bool o = odd.count((uint64_t(uint32_t(t)) << 32) | uint32_t(i)) != 0;
-        in_idx.push_back(uint32_t(t) | (o ? 0x80000000u : 0u));
+        in_idx.push_back(uint32_t(t));  // the parity bit is set below
         in_sz.push_back(tsize[size_t(tb + t)]);
       }
       in_ptr.push_back((int64_t)in_idx.size());
@@ -418,12 +413,28 @@ extern "C" int rm_greedy_windows(RmGraph* g, int32_t W, const int64_t* win_ptr,
     }
     op_base[w + 1] = (int64_t)gop.size();
     ten_base[w + 1] = tb + nt;
+    // parity bits: an op whose entries in a tracked tensor's consumer list
+    // are odd in number flags its input entry for that tensor
+    par.assign(nw, 0);
+    for (const int t : rel) {
+      const int tl = tloc[t];
+      if (tl < 0) continue;
+      for (int k = g->cons_ptr[t]; k < g->cons_ptr[t + 1]; ++k)
+        if (loc[g->cons_idx[k]] >= 0) par[loc[g->cons_idx[k]]] ^= 1;
+      for (int k = g->cons_ptr[t]; k < g->cons_ptr[t + 1]; ++k) {
+        const int j = loc[g->cons_idx[k]];
+        if (j < 0 || !par[j]) continue;
+        par[j] = 0;
+        const int64_t q = op_base[w] + j;
+        for (int64_t e = in_ptr[q]; e < in_ptr[q + 1]; ++e)
+          if (in_idx[e] == uint32_t(tl)) in_idx[e] |= 0x80000000u;
+      }
+    }  // (every par[j] is back to 0: even ones never left it, odd ones were cleared)
     // reset the per-window marks
     for (int v : ops) loc[v] = -1;
     for (int t : rel) tloc[t] = -1;
     for (int64_t k = lin_ptr[w]; k < lin_ptr[w + 1]; ++k) is_lin[lin_idx[k]] = 0;
     for (int64_t k = lout_ptr[w]; k < lout_ptr[w + 1]; ++k) is_lout[lout_idx[k]] = 0;
-    odd.clear();
   }
   // device layout: window w owns nops+1 op slots from opb_dev[w] (the extra
   // slot is the tail entry of its in/succ pointer arrays)
